@@ -1,0 +1,252 @@
+"""Oracle plan interpreter with redundant computation, preemption injection and
+recovery (O4-O6) — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Semantics:
+* Each node n runs its own stage and keeps a replica (parameters AND Adam
+  state) of stage (n+1) mod P. The replica is kept identical by
+  gradient forwarding: after its last backward, stage n sends its fp32
+  gradient sum to node n-1, and both apply the same Adam (Q1 reading).
+* FRC_FWD(k) on node n is exactly FNC_{n+1}(k) with the replica weights
+  (P:429); its saved set and output are retained for a lazy BRC (P:456,
+  P:524; Q10/Q22 readings).
+* A preemption of node v at instruction pi (Q12): v executes its first pi
+  instructions; the survivors run to quiescence (lockstep round-robin, Q14);
+  everything v held is lost; messages v had sent stay delivered.
+* Recovery: the shadow u = v-1 promotes the replica, the
+  successor w = v+1 is rerouted to u and re-sends the gradients it sent to
+  v this step (Q3 reading), u runs the victim's lost work (lazy BRC for every
+  micro-batch in ascending order, Q2/Q20) merged with its own, then Adam for
+  both stages. Later steps run the static failover plans.
+
+The interpreter stores data under the plan's symbolic keys (plan.inputs_of /
+plan.outputs_of), so local data edges created by the merge need no special
+casing. Pins: tests/test_oracle_pipeline.py (brute force O2, 1F1B == GPipe,
+FRC == FNC and replica == primary exactly, injection sweep == failure-free
+exactly, FATAL cases).
+"""
+from collections import deque
+
+import numpy as np
+
+from . import model
+from . import plan as pl
+
+
+class Node:
+    def __init__(self, nid):
+        self.nid = nid
+        self.copies = {}      # stage -> dict(p, m, v, t, g, role)
+        self.store = {}
+
+
+class Pipeline:
+    """P logical nodes executing instruction lists over fp64 numpy data."""
+
+    def __init__(self, cfg, flat_params, rc=True, layers_per_stage=None,
+                 lr=1e-4, b1=0.9, b2=0.999, eps=1e-8):
+        self.cfg = cfg
+        m = cfg.model
+        self.P, self.M, self.rc = cfg.stages, cfg.microbatches, rc
+        self.lay = model.Layout(m)
+        self.ranges = pl.partition(m.n_layer, self.P, layers_per_stage)
+        self.hp = (lr, b1, b2, eps)
+        self.nodes = {n: Node(n) for n in range(self.P)}
+        self.mode = "normal"
+        self.victim = None
+        self.dead = set()
+        self.plans = pl.normal_plans(self.P, self.M, rc)
+        self.host = {s: s for s in range(self.P)}
+        self.replica_on = {s: ((s - 1) % self.P if rc else None) for s in range(self.P)}
+        flat = np.asarray(flat_params, dtype=np.float64)
+        for s in range(self.P):
+            self._install(self.nodes[s], s, flat, "primary")
+            if rc:
+                self._install(self.nodes[(s - 1) % self.P], s, flat, "replica")
+        self.pending = None        # armed injection (v, pi)
+        self.interrupted = None    # state between a preempted step and recover()
+        self.step_no = 0
+
+    # ------------------------------------------------------------------ state
+    def stage_bounds(self, X):
+        a, b = self.ranges[X]
+        return self.lay.range_of_units(a, b)
+
+    def _install(self, node, X, flat, role):
+        lo, hi = self.stage_bounds(X)
+        node.copies[X] = {"p": flat[lo:hi].copy(), "m": np.zeros(hi - lo),
+                          "v": np.zeros(hi - lo), "t": 0, "g": np.zeros(hi - lo), "role": role}
+
+    def params(self, X):
+        return self.nodes[self.host[X]].copies[X]
+
+    def full_params(self):
+        return np.concatenate([self.params(X)["p"] for X in range(self.P)])
+
+    def full_grads(self):
+        return np.concatenate([self.params(X)["g"] for X in range(self.P)])
+
+    def full_adam(self):
+        return (np.concatenate([self.params(X)["m"] for X in range(self.P)]),
+                np.concatenate([self.params(X)["v"] for X in range(self.P)]))
+
+    # ------------------------------------------------------------- execution
+    def _stage_fwd(self, X, c, x, k):
+        a, b = self.ranges[X]
+        lo, hi = self.stage_bounds(X)
+        th = self.lay.tensors(c["p"], lo, hi)
+        tok, tgt = self.tokens[k], self.targets[k]
+        saved = []
+        for unit in range(a, b + 1):
+            x, sv = model.unit_fwd(self.lay, unit, th, x, tok, tgt, self.n_tok)
+            saved.append(sv)
+        return x, saved
+
+    def _stage_bwd(self, X, c, saved, d, k):
+        a, b = self.ranges[X]
+        lo, hi = self.stage_bounds(X)
+        th = self.lay.tensors(c["p"], lo, hi)
+        gr = self.lay.tensors(c["g"], lo, hi)
+        tok, tgt = self.tokens[k], self.targets[k]
+        for unit, sv in zip(reversed(range(a, b + 1)), reversed(saved)):
+            d = model.unit_bwd(self.lay, unit, th, gr, sv, d, tok, tgt, self.n_tok)
+        return d
+
+    def _exec(self, n, ins, msg):
+        node = self.nodes[n]
+        st = node.store
+        P, k, X = self.P, ins.mb, ins.stage
+        kd = ins.kind
+        if kd == pl.LOAD_INPUTS:
+            for j in range(self.M):
+                st[("tok", j)] = self.tokens[j]
+                st[("tgt", j)] = self.targets[j]
+        elif kd in (pl.FWD, pl.FRC_FWD):
+            c = node.copies[X]
+            if kd == pl.FRC_FWD:
+                assert c["role"] == "replica" and X == (n + 1) % P
+            x_in = None if X == 0 else st[("act", X, k)]
+            if X == 0:
+                assert ("tok", k) in st
+            out, saved = self._stage_fwd(X, c, x_in, k)
+            st[("saved", X, k)] = saved
+            st[("act", X + 1, k) if X < P - 1 else ("loss", k)] = out
+        elif kd == pl.BWD:
+            c = node.copies[X]
+            d = None if X == P - 1 else st[("dact", X + 1, k)]
+            din = self._stage_bwd(X, c, st[("saved", X, k)], d, k)
+            if X > 0:
+                st[("dact", X, k)] = din
+            if k == self.M - 1:
+                st[("gradsum", X)] = c["g"]
+        elif kd in pl.SENDS:
+            payload = {pl.SEND_ACT: lambda: st[("act", X + 1, k)],
+                       pl.SEND_GRAD: lambda: st[("dact", X, k)],
+                       pl.RESEND_GRAD: lambda: st[("dact", X, k)],
+                       pl.REPLICA_SEND: lambda: st[("gradsum", X)].copy()}[kd]()
+            self.payloads[id(msg)] = payload
+        elif kd in pl.RECVS:
+            payload = self.payloads.pop(id(msg))
+            if kd == pl.RECV_ACT:
+                st[("act", X, k)] = payload
+            elif kd == pl.RECV_GRAD:
+                st[("dact", X + 1, k)] = payload
+            else:
+                c = node.copies[X]
+                c["g"][:] = payload
+                st[("gradsum", X)] = c["g"]
+        elif kd == pl.APPLY:
+            c = node.copies[X]
+            lr, b1, b2, eps = self.hp
+            c["t"] += 1
+            c["p"], c["m"], c["v"] = model.adam_update(c["p"], c["g"], c["m"], c["v"], c["t"],
+                                                       lr, b1, b2, eps)
+        else:
+            raise ValueError(kd)
+
+    def _run(self, plans, pcs, channels, cap=None):
+        return pl.lockstep(plans, pcs, channels, cap, on_exec=self._exec)
+
+    def _begin_step(self, tokens, targets):
+        m = self.cfg.model
+        mb = self.cfg.micro_batch
+        self.tokens = [tokens[k * mb:(k + 1) * mb] for k in range(self.M)]
+        self.targets = [targets[k * mb:(k + 1) * mb] for k in range(self.M)]
+        self.n_tok = self.M * mb * m.seq_len
+        self.payloads = {}
+        for n, node in self.nodes.items():
+            node.store = {}
+            for c in node.copies.values():
+                c["g"][:] = 0.0
+
+    def _end_step(self):
+        loss = 0.0
+        for k in range(self.M):
+            vals = [node.store[("loss", k)] for n, node in self.nodes.items()
+                    if n not in self.dead and ("loss", k) in node.store]
+            loss += vals[0]
+        self.step_no += 1
+        self.last_stores = {n: node.store for n, node in self.nodes.items()}
+        return loss
+
+    # ------------------------------------------------------------ public API
+    def preempt(self, v, pi):
+        """Arm a preemption of node v after pi instructions of the next step."""
+        if self.mode != "normal" or not self.rc:
+            raise pl.Fatal("no replica available for the victim")
+        self.pending = (v, pi)
+
+    def step(self, tokens, targets):
+        """Run one step. Returns ('ok', loss) or ('preempted', cut info)."""
+        if self.interrupted is not None:
+            raise RuntimeError("recover() pending")
+        self._begin_step(tokens, targets)
+        live = {n: p for n, p in self.plans.items() if n not in self.dead}
+        if self.pending is None:
+            pcs, ch = self._run(live, None, None)
+            if any(pcs[n] < len(live[n]) for n in live):
+                raise pl.PlanError("deadlock in a failure-free step")
+            return "ok", self._end_step()
+        v, pi = self.pending
+        self.pending = None
+        pcs, ch = self._run(live, None, None, cap={v: pi})
+        assert pcs[v] == pi
+        for key in list(ch):
+            if key[1] == v:
+                for m in ch[key]:
+                    self.payloads.pop(id(m), None)
+                del ch[key]
+        self.dead.add(v)
+        self.nodes[v].store = {}
+        self.nodes[v].copies = {}
+        self.interrupted = (v, pcs, ch)
+        return "preempted", {"victim": v, "pcs": dict(pcs)}
+
+    def recover(self):
+        """Run the recovery continuation of the interrupted step; install the
+        failover plans for later steps. Returns (loss, info)."""
+        v, pcs, ch = self.interrupted
+        P, M = self.P, self.M
+        u = (v - 1) % P
+        new, info = pl.recovery_plans(self.plans, P, M, v, pcs, ch)
+        self.recovery_info = info
+        self.continuation = new
+        # promote the replica (the shadow executes the victim's work)
+        c = self.nodes[u].copies[v]
+        c["role"] = "primary"
+        self.host[v] = u
+        self.mode = "failover"
+        self.victim = v
+        _, self.replica_on = pl.failover_topology(P, v)
+        live = {n: p for n, p in new.items()}
+        pcs2, ch = self._run(live, {n: 0 for n in live}, ch)
+        if any(pcs2[n] < len(live[n]) for n in live):
+            raise pl.PlanError("deadlock in recovery continuation")
+        self.plans = pl.failover_plans(P, M, v)
+        self.interrupted = None
+        return self._end_step(), info
+
+    def dump(self):
+        host, rep = (self.host, self.replica_on)
+        mode = self.mode
+        return pl.dump(self.P, self.M, self.rc, self.ranges, self.plans, host, rep, None, mode,
+                       self.victim)

@@ -1,0 +1,172 @@
+"""Pins for oracle/pipeline.py:
+
+* pipelined == brute-force single-device step (P:140-142 synchronous
+  micro-batching keeps one consistent model state), 1F1B == GPipe;
+* FRC^n_{n+1} output and saved set == FNC_{n+1} exactly;
+* replica == primary exactly after every step ("same model parameters
+  and optimizer states");
+* an injected preemption + recovery gives loss, gradients, parameters and
+  Adam state EXACTLY equal to the failure-free run (north star), for every
+  victim and every injection point on C0 and on random tiny pipelines;
+* consecutive preemptions are FATAL.
+"""
+import dataclasses
+import random
+
+import numpy as np
+import pytest
+
+from oracle import model, pipeline, plan as pl
+from synth import get_config, make_params, make_tokens
+
+
+def tiny(P, M, L=None, mb=1, S=8, H=16, nh=2, V=32, causal=True):
+    c0 = get_config("C0")
+    L = P if L is None else L
+    m = dataclasses.replace(c0.model, n_layer=L, d_model=H, n_head=nh, d_ff=4 * H, vocab=V,
+                            vocab_sample=V, seq_len=S, causal=causal)
+    return dataclasses.replace(c0, name="tiny", model=m, stages=P, microbatches=M, micro_batch=mb)
+
+
+def brute(cfg, flat, steps, lr=1e-4):
+    lay = model.Layout(cfg.model)
+    p, m, v = flat.astype(np.float64), np.zeros(lay.total), np.zeros(lay.total)
+    out = []
+    for t in range(1, steps + 1):
+        tok, tgt = make_tokens(cfg, t - 1)
+        loss, g, p, m, v = model.train_step(lay, p, m, v, t, tok, tgt, lr, 0.9, 0.999, 1e-8)
+        out.append((loss, g, p.copy(), m.copy(), v.copy()))
+    return out
+
+
+@pytest.mark.parametrize("rc", [False, True])
+def test_pipelined_equals_brute_force_c0(rc):
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    ref = brute(cfg, flat, 2)
+    pp = pipeline.Pipeline(cfg, flat, rc=rc)
+    for t in range(2):
+        tok, tgt = make_tokens(cfg, t)
+        status, loss = pp.step(tok, tgt)
+        assert status == "ok"
+        rl, rg, rp, rm, rv = ref[t]
+        assert abs(loss - rl) <= 1e-12 * abs(rl)
+        assert np.abs(pp.full_grads() - rg).max() <= 1e-12 * np.abs(rg).max()
+        assert np.abs(pp.full_params() - rp).max() <= 1e-12 * np.abs(rp).max()
+
+
+def test_1f1b_equals_gpipe():
+    cfg = tiny(3, 4)
+    flat = make_params(cfg.model)
+    a = pipeline.Pipeline(cfg, flat, rc=False)
+    b = pipeline.Pipeline(cfg, flat, rc=False)
+    b.plans = {s: pl.gpipe_plan(s, 3, 4) for s in range(3)}
+    tok, tgt = make_tokens(cfg, 0)
+    la = a.step(tok, tgt)[1]
+    lb = b.step(tok, tgt)[1]
+    assert abs(la - lb) <= 1e-13 * abs(la)
+    assert np.allclose(a.full_grads(), b.full_grads(), rtol=0, atol=1e-14)
+
+
+def _frc_equals_fnc(pp):
+    P = pp.P
+    stores = pp.last_stores
+    for n in range(P):
+        X = (n + 1) % P
+        for k in range(pp.M):
+            frc_saved = stores[n][("saved", X, k)]
+            fnc_saved = stores[X][("saved", X, k)]
+            for a, b in zip(frc_saved, fnc_saved):
+                assert a.keys() == b.keys()
+                for key in a:
+                    if key in ("s1", "s2", "ln"):
+                        assert all(np.array_equal(x, y) for x, y in zip(a[key], b[key]))
+                    else:
+                        assert np.array_equal(a[key], b[key])
+            okey = ("act", X + 1, k) if X < P - 1 else ("loss", k)
+            assert np.array_equal(np.asarray(stores[n][okey]), np.asarray(stores[X][okey]))
+
+
+def test_frc_is_fnc_and_replica_is_primary():
+    cfg = tiny(3, 4)
+    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=True)
+    for t in range(3):
+        tok, tgt = make_tokens(cfg, t)
+        pp.step(tok, tgt)
+        _frc_equals_fnc(pp)
+        for s in range(3):
+            prim = pp.nodes[s].copies[s]
+            rep = pp.nodes[(s - 1) % 3].copies[s]
+            for key in ("p", "m", "v", "g"):
+                assert np.array_equal(prim[key], rep[key])
+            assert prim["t"] == rep["t"]
+
+
+def _run(cfg, flat, steps, inject=None):
+    pp = pipeline.Pipeline(cfg, flat, rc=True)
+    res = []
+    for t in range(steps):
+        tok, tgt = make_tokens(cfg, t)
+        if inject is not None and inject[0] == t:
+            pp.preempt(inject[1], inject[2])
+        status, val = pp.step(tok, tgt)
+        if status == "preempted":
+            val, info = pp.recover()
+        res.append((val, pp.full_grads().copy(), pp.full_params().copy(),
+                    *[a.copy() for a in pp.full_adam()]))
+    return pp, res
+
+
+def _same(a, b):
+    assert a[0] == b[0]
+    for x, y in zip(a[1:], b[1:]):
+        assert np.array_equal(x, y)
+
+
+def test_c0_injection_sweep_exact():
+    """C0 (BASELINE configs[0]): every victim, every injection point."""
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    _, ref = _run(cfg, flat, 2)
+    plans = pl.normal_plans(cfg.stages, cfg.microbatches, True)
+    for v in range(cfg.stages):
+        for pi in range(len(plans[v]) + 1):
+            pp, res = _run(cfg, flat, 2, inject=(0, v, pi))
+            _same(res[0], ref[0])        # the interrupted step
+            _same(res[1], ref[1])        # a following step on the failover plan
+            assert pp.mode == "failover"
+
+
+def test_random_tiny_injections_exact():
+    r = random.Random(11)
+    for _ in range(12):
+        P = r.randint(2, 5)
+        M = r.randint(1, 6)
+        cfg = tiny(P, M, L=P + r.randint(0, 2), causal=bool(r.randint(0, 1)))
+        flat = make_params(cfg.model)
+        _, ref = _run(cfg, flat, 2)
+        plans = pl.normal_plans(P, M, True)
+        for _ in range(4):
+            v = r.randrange(P)
+            pi = r.randint(0, len(plans[v]))
+            _, res = _run(cfg, flat, 2, inject=(0, v, pi))
+            _same(res[0], ref[0])
+            _same(res[1], ref[1])
+
+
+def test_second_preemption_is_fatal():
+    cfg = get_config("C0")
+    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=True)
+    tok, tgt = make_tokens(cfg, 0)
+    pp.preempt(1, 5)
+    assert pp.step(tok, tgt)[0] == "preempted"
+    pp.recover()
+    with pytest.raises(pl.Fatal):     # P:464, Q18: no redundancy left
+        pp.preempt(0, 0)
+
+
+def test_no_rc_preemption_is_fatal():
+    cfg = get_config("C0")
+    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=False)
+    with pytest.raises(pl.Fatal):
+        pp.preempt(1, 3)
