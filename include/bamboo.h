@@ -1,0 +1,225 @@
+/*
+ * bamboo.h — C ABI of the B200-native Bamboo redundant-computation pipeline
+ * (arXiv 2204.12013; PAPER.md = /root/reference/PAPER.md line numbers "P:N").
+ *
+ * The library runs a synchronous 1F1B pipeline-parallel training step of a
+ * GPT/BERT-style transformer in which every node also runs
+ * a redundant forward (FRC) of its successor's layers in the pipeline bubbles
+ * and keeps a replica of the successor's parameters and
+ * Adam state. A preempted node's predecessor (its "shadow") promotes
+ * that replica, runs the lazy redundant backward (BRC) and the weight update,
+ * and the pipeline continues on a merged failover schedule
+ * without a checkpoint restart.
+ *
+ * Processes and devices. One process per GPU. A context hosts the pipeline
+ * NODES mapped to its rank (node n runs stage n until a failover); several
+ * nodes may share one process/GPU (stages > GPUs). Nodes on different ranks
+ * exchange activations, gradients and replica gradients with NCCL P2P over
+ * NVLink on 2-rank communicators, one per (src node, dst node, message kind)
+ * edge, created inside bb_init from the 128-byte ncclUniqueId the caller
+ * broadcasts (bb_nccl_unique_id on rank 0).
+ *
+ * Conventions for every entry point:
+ *  - Returns bb_status (0 = BB_OK). No exception, exit() or abort() crosses
+ *    the ABI; CUDA / NCCL failures map to BB_E_CUDA / BB_E_NCCL and the
+ *    message is kept per context (bb_last_error).
+ *  - Host pointers passed in are borrowed for the duration of the call only
+ *    (copied before return). Output host buffers are caller-owned.
+ *  - Device pointers (bb_op_* only) are caller-owned CUDA device memory on the
+ *    current device; the call is asynchronous on the given stream.
+ *  - A context is not thread-safe: one call at a time.
+ *  - After BB_E_PREEMPTED only bb_recover, bb_read_state, bb_*_dump,
+ *    bb_last_error and bb_destroy are legal; after BB_E_FATAL only
+ *    bb_read_state, bb_*_dump, bb_last_error and bb_destroy.
+ */
+#ifndef BAMBOO_H
+#define BAMBOO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BB_OK = 0,
+  BB_E_INVAL = -1,        /* bad argument / configuration                                  */
+  BB_E_CUDA = -2,         /* CUDA runtime or driver error                                   */
+  BB_E_NCCL = -3,         /* NCCL error                                                     */
+  BB_E_OOM = -4,          /* device allocation failed                                       */
+  BB_E_PREEMPTED = -5,    /* step interrupted by an injected preemption: call bb_recover    */
+  BB_E_FATAL = -6,        /* unrecoverable: consecutive / unprotected stage lost    */
+  BB_E_STATE = -7,        /* call not legal in the current state                            */
+  BB_E_UNSUPPORTED = -8   /* valid request this build does not implement                    */
+} bb_status;
+
+typedef enum { BB_RC_NONE = 0, BB_RC_EFLB = 1 /* eager FRC, lazy BRC */ } bb_rc_mode;
+typedef enum { BB_PREC_BF16 = 0, BB_PREC_FP32_CHECK = 1 } bb_precision;
+
+/* Transformer shape (readings in DESIGN.md): pre-LN GPT-2 block,
+ * GELU-tanh, learned positions, untied LM head without bias, LN eps 1e-5.
+ * causal = 1 for GPT (causal mask), 0 for BERT (bidirectional). vocab is the
+ * padded vocabulary used by the embedding and the head. d_model % n_head == 0
+ * and d_model, d_ff, vocab multiples of 8 are required. */
+typedef struct {
+  int n_layer, d_model, n_head, d_ff, vocab, seq_len, causal;
+} bb_model;
+
+typedef struct {
+  int micro_batch;              /* sequences per micro-batch (mb)                          */
+  bb_rc_mode rc;                /* BB_RC_EFLB needs stages >= 2 (no successor otherwise)   */
+  bb_precision prec;            /* bf16 operands + fp32 accumulate, or all-fp32 check mode */
+  const int *layers_per_stage;  /* [stages] transformer blocks per stage, NULL = even split
+                                   with the remainder on the last stages          */
+  float lr, beta1, beta2, eps;  /* Adam, bias-corrected, no weight decay          */
+  int world_rank, world_size;   /* this process / number of processes (1 = no NCCL)        */
+  int device;                   /* CUDA device ordinal this process uses                   */
+  const int *node_rank;         /* [stages] process rank hosting node n; NULL = contiguous
+                                   blocks of ceil(stages/world_size) nodes per rank        */
+  const void *nccl_id;          /* 128-byte ncclUniqueId (same on all ranks) or NULL       */
+  int profile;                  /* 1 = time every GEMM launch with CUDA events            */
+} bb_opts;
+
+typedef struct {
+  float loss;            /* mean token cross-entropy of the step (NaN on ranks without stage P-1) */
+  float step_ms;         /* host wall time of the call                                    */
+  float device_ms;       /* max over local nodes of main-stream time of the step          */
+  int gpu_launches;      /* kernels this process launched during the call                 */
+  uint64_t h2d_bytes, d2h_bytes;
+} bb_step_stats;
+
+typedef struct {
+  int victim, shadow, successor;
+  int commit;            /* 1 = victim had already delivered its gradient sum (no BRC)    */
+  int brc_mb;            /* micro-batches whose backward was recomputed (lazy BRC)        */
+  int frc_done_mb;       /* micro-batches whose retained FRC result was reused            */
+  int resent_mb;         /* gradients the successor re-sent to the shadow                 */
+  float recover_ms;      /* host wall time of bb_recover                                   */
+  float loss;            /* loss of the interrupted step (NaN where not local)           */
+} bb_recovery_stats;
+
+/* Fill *o with defaults: micro_batch 1, rc EFLB, bf16, Adam(1e-4, 0.9, 0.999, 1e-8),
+ * single process on device 0. */
+void bb_default_opts(bb_opts *o);
+
+/* Write a fresh ncclUniqueId (128 bytes) into out (rank 0 only). */
+bb_status bb_nccl_unique_id(void *out, size_t cap);
+
+/* Create a context for `stages` pipeline stages (P) and `microbatches` (M) per
+ * step. Partitions layers, builds every node's static plan
+ * (1F1B P:497; eager FRC P:520-521), allocates parameters, replicas
+ * (P:429), activation stashes and FRC retention in HBM, creates
+ * streams and the NCCL edge communicators. Errors: BB_E_INVAL for
+ * n_layer < stages, rc with stages < 2, bad shapes; BB_E_OOM; BB_E_CUDA/NCCL. */
+bb_status bb_init(const bb_model *m, int stages, int microbatches, const bb_opts *o,
+                  void **ctx_out);
+
+/* Load parameters from `host` = the full canonical flat fp32 vector of n
+ * values (order in DESIGN.md "Parameter layout"). Every rank passes the same
+ * vector; each copies the slices of the stages it hosts and of the replicas
+ * it keeps. Resets Adam state and step count. */
+bb_status bb_load_params(void *ctx, const float *host, size_t n);
+
+/* One training step over M*mb sequences: tokens, targets = host int32 arrays
+ * [M*mb, seq_len] row-major (micro-batch k = rows k*mb..k*mb+mb-1). Every rank
+ * passes the full arrays and uploads what its nodes need (the last node
+ * fetches inputs for its FRC). Returns BB_E_PREEMPTED if an armed injection
+ * fired (bb_recover must follow). st may be NULL. */
+bb_status bb_step(void *ctx, const int32_t *tokens, const int32_t *targets, bb_step_stats *st);
+
+/* Arm a preemption of node `stage` after it has executed `at_instr` (pi)
+ * instructions of its list in the next step (0 <= pi <= list length). Must be
+ * called with the same arguments on every rank. BB_E_FATAL if the pipeline has
+ * no redundancy left for that node (rc off, or already in failover mode:
+ * P:464). */
+bb_status bb_preempt(void *ctx, int stage, int at_instr);
+
+/* Finish the interrupted step on the survivors: the shadow promotes the
+ * replica, runs FRC catch-up, the lazy BRC for every micro-batch of the step,
+ * the successor re-sends its retained gradients and is rerouted, and both
+ * stages' Adam updates run; later steps use the merged failover
+ * plan. Called on every rank (the victim's rank drains and NaN-poisons the
+ * victim's memory). r may be NULL. */
+bb_status bb_recover(void *ctx, bb_recovery_stats *r);
+
+enum { BB_STATE_PARAMS = 0, BB_STATE_GRADS = 1, BB_STATE_ADAM_M = 2, BB_STATE_ADAM_V = 3 };
+/* Copy stage `stage`'s fp32 state (what = BB_STATE_*) into host[n], n = the
+ * stage's parameter count. replica = 0 reads the copy the stage runs on
+ * (primary; the promoted replica after a failover), 1 reads the replica kept
+ * by its predecessor. BB_E_INVAL if that copy is not hosted by this process. */
+bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n);
+
+/* Number of parameters of `stage` and its offset in the canonical flat vector. */
+bb_status bb_stage_params(void *ctx, int stage, size_t *offset, size_t *count);
+
+/* Text dump of the current plans: header, stage
+ * assignment, one instruction per line. Writes at most cap bytes (NUL
+ * terminated) and the required size (including NUL) into *needed. */
+bb_status bb_schedule_dump(void *ctx, char *buf, size_t cap, size_t *needed);
+
+/* Text dump of the last recovery: the cut (instructions executed per node)
+ * and the continuation lists, same line format. */
+bb_status bb_recovery_dump(void *ctx, char *buf, size_t cap, size_t *needed);
+
+/* Per-kernel-class device time of the last step (profile = 1): for each class
+ * c < *n_classes: name, launches, total ms, algorithmic flops or bytes. */
+typedef struct { char name[32]; int launches; double ms; double work; } bb_kernel_stat;
+bb_status bb_kernel_stats(void *ctx, bb_kernel_stat *out, int cap, int *n_classes);
+
+/* Host-only (no GPU, no context): the plan text of a configuration.
+ * victim < 0: the normal plans (same text as bb_schedule_dump after bb_init);
+ * victim >= 0 and at_instr >= 0: the cut and continuation lists of an
+ * injection at (victim, at_instr) (same text as bb_recovery_dump);
+ * victim >= 0 and at_instr < 0: the static failover plans after losing victim. */
+bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb_opts *o,
+                       int victim, int at_instr, char *buf, size_t cap, size_t *needed);
+
+bb_status bb_last_error(const void *ctx, char *buf, size_t cap);
+void bb_destroy(void *ctx);
+
+/* ---- single-op entry points (kernel parity tests and roofline timing) ----
+ * All pointers are device pointers; `stream` is a cudaStream_t (0 = default).
+ * bf16 data is passed as uint16 bit patterns. */
+
+/* D[m][n] = sum_k A(m,k) B(n,k) with A(m,k) = A[m*lda+k] (a_mn = 0) or
+ * A[k*lda+m] (a_mn = 1), B likewise; epilogue `epi`:
+ *   0 STORE      C[m*ldc+n] = D                          (C dtype = act dtype)
+ *   1 BIAS       C = D + bias[n]
+ *   2 BIAS_RES   C = D + bias[n] + res[m*ldc+n]
+ *   3 BIAS_GELU  aux[m*ldc+n] = D + bias[n] (pre-activation), C = gelu_tanh(pre)
+ *   4 GELU_BWD   C = D * gelu_tanh'(aux[m*ldc+n])
+ *   5 ACC_F32    Cf32[m*ldc+n] += D                      (fp32 output)
+ * prec = BB_PREC_BF16 (bf16 operands, tcgen05 tensor cores, fp32 accumulate)
+ * or BB_PREC_FP32_CHECK (fp32 SIMT). impl: 0 = default, 1 = force SIMT. */
+bb_status bb_op_gemm(int prec, int impl, int M, int N, int K, const void *A, int lda, int a_mn,
+                     const void *B, int ldb, int b_mn, int epi, void *C, int ldc,
+                     const void *bias, const void *res, void *aux, void *stream);
+
+/* Attention over qkv [B*S, 3H] (columns [q|k|v], head h at h*d): o [B*S, H],
+ * lse [B, nh, S] fp32. Backward: dqkv [B*S, 3H] from do, o, lse. */
+bb_status bb_op_attention_fwd(int prec, int B, int S, int H, int nh, int causal, const void *qkv,
+                              void *o, float *lse, void *stream);
+bb_status bb_op_attention_bwd(int prec, int B, int S, int H, int nh, int causal, const void *qkv,
+                              const void *o, const float *lse, const void *dout, void *dqkv,
+                              void *stream);
+/* LayerNorm over rows [R, H]: y, mean, rstd; backward dx = dres + LN'(dy),
+ * dg/db accumulated (+=) into fp32 [H]. dres may be NULL. */
+bb_status bb_op_layernorm_fwd(int prec, int R, int H, const void *x, const void *g, const void *b,
+                              void *y, float *mean, float *rstd, void *stream);
+bb_status bb_op_layernorm_bwd(int prec, int R, int H, const void *dy, const void *x,
+                              const float *mean, const float *rstd, const void *g,
+                              const void *dres, void *dx, float *dg, float *db, void *stream);
+/* Cross-entropy over logits [R, V] (overwritten with dlogits = (softmax -
+ * onehot)/n_tok), loss_rows[R] fp32 = (lse - logit[target]) / n_tok. */
+bb_status bb_op_cross_entropy(int prec, int R, int V, void *logits, const int32_t *targets,
+                              float n_tok, float *loss_rows, void *stream);
+/* Adam on n fp32 values (bias-corrected, step t >= 1); also writes the bf16
+ * working copy when w16 != NULL. */
+bb_status bb_op_adam(size_t n, float *p, const float *g, float *m, float *v, uint16_t *w16, int t,
+                     float lr, float b1, float b2, float eps, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAMBOO_H */

@@ -517,3 +517,22 @@ def simulate_times(plans, P, fwd_t, bwd_t, frc=True):
     if any(pcs[n] < len(plans[n]) for n in plans):
         raise PlanError("replay deadlock")
     return t_node, timeline
+
+
+def dump_lines(plans):
+    out = []
+    for n in sorted(plans):
+        for i, ins in enumerate(plans[n]):
+            out.append(f"{n} {i} {ins.kind} {_f(ins.mb)} {_f(ins.peer)} {_f(ins.stage)}")
+    return "".join(line + "\n" for line in out)
+
+
+def recovery_dump(P, M, v, pi):
+    """Cut + continuation text of an injection at (v, pi) (DESIGN.md format)."""
+    plans = normal_plans(P, M, True)
+    pcs, ch = cut(plans, v, pi)
+    new, info = recovery_plans(plans, P, M, v, pcs, ch)
+    hdr = (f"# bamboo-recovery v1 P={P} M={M} victim={v} shadow={info['shadow']} "
+           f"successor={info['successor']} commit={1 if info['commit'] else 0}\n")
+    hdr += "# cut" + "".join(f" {n}:{pcs[n]}" for n in sorted(pcs)) + "\n"
+    return hdr + dump_lines(new)

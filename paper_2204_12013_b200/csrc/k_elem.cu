@@ -1,0 +1,370 @@
+// k_elem.cu — bandwidth-bound kernels of the hot path: LayerNorm fwd/bwd,
+// deterministic column reductions (bias / LN-parameter gradients), token +
+// position embedding fwd/bwd, softmax cross-entropy, fixed-order sums, Adam
+// and casts. All reductions use a fixed order so that the redundant
+// computation on another node reproduces the normal one bit for bit
+// ("exactly the same computation").
+#include <cfloat>
+
+#include "k_common.cuh"
+
+namespace bb {
+namespace k {
+
+namespace {
+constexpr float LN_EPS = 1e-5f;
+
+// ------------------------------------------------------------- LayerNorm
+template <typename T>
+__global__ void ln_fwd_kernel(int R, int H, const T *__restrict__ x, const T *__restrict__ g,
+                              const T *__restrict__ b, T *__restrict__ y, float *__restrict__ mean,
+                              float *__restrict__ rstd) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const T *xr = x + (size_t)row * H;
+  float s = 0.f;
+  for (int i = lane; i < H; i += 32) s += to_f(xr[i]);
+  const float mu = warp_sum(s) / H;
+  float q = 0.f;
+  for (int i = lane; i < H; i += 32) {
+    const float d = to_f(xr[i]) - mu;
+    q += d * d;
+  }
+  const float rs = rsqrtf(warp_sum(q) / H + LN_EPS);
+  T *yr = y + (size_t)row * H;
+  for (int i = lane; i < H; i += 32)
+    yr[i] = from_f<T>((to_f(xr[i]) - mu) * rs * to_f(g[i]) + to_f(b[i]));
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+template <typename T>
+__global__ void ln_bwd_dx_kernel(int R, int H, const T *__restrict__ dy, const T *__restrict__ x,
+                                 const float *__restrict__ mean, const float *__restrict__ rstd,
+                                 const T *__restrict__ g, const T *__restrict__ dres,
+                                 T *__restrict__ dx) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const size_t off = (size_t)row * H;
+  const float mu = mean[row], rs = rstd[row];
+  float s1 = 0.f, s2 = 0.f;
+  for (int i = lane; i < H; i += 32) {
+    const float gd = to_f(dy[off + i]) * to_f(g[i]);
+    const float xh = (to_f(x[off + i]) - mu) * rs;
+    s1 += gd;
+    s2 += gd * xh;
+  }
+  const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
+  for (int i = lane; i < H; i += 32) {
+    const float gd = to_f(dy[off + i]) * to_f(g[i]);
+    const float xh = (to_f(x[off + i]) - mu) * rs;
+    float v = rs * (gd - m1 - xh * m2);
+    if (dres) v += to_f(dres[off + i]);
+    dx[off + i] = from_f<T>(v);
+  }
+}
+
+// ------------------------------------------------------- column reductions
+constexpr int CR_ROWS = 64, CR_COLS = 128;
+
+template <typename T>
+__global__ void colreduce_partial_kernel(int mode, int R, int N, const T *__restrict__ A,
+                                         const T *__restrict__ X, const float *__restrict__ mean,
+                                         const float *__restrict__ rstd, float *__restrict__ part) {
+  const int n = blockIdx.x * CR_COLS + threadIdx.x;
+  const int r0 = blockIdx.y * CR_ROWS;
+  if (n >= N) return;
+  const int r1 = min(R, r0 + CR_ROWS);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) {
+    const size_t idx = (size_t)r * N + n;
+    float a = to_f(A[idx]);
+    if (mode == 1) a *= (to_f(X[idx]) - mean[r]) * rstd[r];
+    s += a;
+  }
+  part[(size_t)blockIdx.y * N + n] = s;
+}
+
+__global__ void colreduce_final_kernel(int chunks, int N, const float *__restrict__ part,
+                                       float *__restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int c = 0; c < chunks; ++c) s += part[(size_t)c * N + n];
+  out[n] += s;
+}
+
+// -------------------------------------------------------------- embedding
+template <typename T>
+__global__ void embed_fwd_kernel(int R, int S, int H, const int32_t *__restrict__ tok,
+                                 const T *__restrict__ E, const T *__restrict__ Pos,
+                                 T *__restrict__ x) {
+  const int r = blockIdx.x;
+  const T *e = E + (size_t)tok[r] * H;
+  const T *p = Pos + (size_t)(r % S) * H;
+  T *o = x + (size_t)r * H;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) o[i] = from_f<T>(to_f(e[i]) + to_f(p[i]));
+}
+
+template <typename T>
+__global__ void embed_bwd_tok_kernel(int H, const int32_t *__restrict__ uniq,
+                                     const int32_t *__restrict__ offs,
+                                     const int32_t *__restrict__ pos, const T *__restrict__ dx,
+                                     float *__restrict__ dE) {
+  const int u = blockIdx.x;
+  const int a = offs[u], b = offs[u + 1];
+  float *out = dE + (size_t)uniq[u] * H;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+    float s = 0.f;
+    for (int p = a; p < b; ++p) s += to_f(dx[(size_t)pos[p] * H + i]);
+    out[i] += s;
+  }
+}
+
+template <typename T>
+__global__ void embed_bwd_pos_kernel(int Bsz, int S, int H, const T *__restrict__ dx,
+                                     float *__restrict__ dPos) {
+  const int sidx = blockIdx.x;
+  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < Bsz; ++b) s += to_f(dx[((size_t)b * S + sidx) * H + i]);
+    dPos[(size_t)sidx * H + i] += s;
+  }
+}
+
+// ---------------------------------------------------------- cross-entropy
+constexpr int CE_T = 512;
+
+__device__ __forceinline__ void online_merge(float &m, float &s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  s = s * __expf(m - mn) + s2 * __expf(m2 - mn);
+  m = mn;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CE_T) ce_kernel(int V, T *__restrict__ logits,
+                                                   const int32_t *__restrict__ tgt, float inv_ntok,
+                                                   float *__restrict__ loss_rows) {
+  const int r = blockIdx.x;
+  T *row = logits + (size_t)r * V;
+  float m = -INFINITY, s = 0.f;
+  for (int i = threadIdx.x; i < V; i += CE_T) {
+    const float v = to_f(row[i]);
+    if (v > m) {
+      s = s * __expf(m - v) + 1.f;
+      m = v;
+    } else {
+      s += __expf(v - m);
+    }
+  }
+  // fixed-order reduction of (m, s) pairs: warp tree, then warp 0 over warps
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    online_merge(m, s, m2, s2);
+  }
+  __shared__ float sm[CE_T / 32], ss[CE_T / 32];
+  __shared__ float lse_sh;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) {
+    sm[w] = m;
+    ss[w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+    m = lane < CE_T / 32 ? sm[lane] : -INFINITY;
+    s = lane < CE_T / 32 ? ss[lane] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      online_merge(m, s, m2, s2);
+    }
+    if (lane == 0) lse_sh = m + logf(s);
+  }
+  __syncthreads();
+  const float lse = lse_sh;
+  const int t = tgt[r];
+  if (threadIdx.x == 0) loss_rows[r] = (lse - to_f(row[t])) * inv_ntok;
+  __syncthreads();   // the target logit is read before being overwritten
+  for (int i = threadIdx.x; i < V; i += CE_T) {
+    const float p = __expf(to_f(row[i]) - lse);
+    row[i] = from_f<T>((p - (i == t ? 1.f : 0.f)) * inv_ntok);
+  }
+}
+
+__global__ void sum_fixed_kernel(int n, const float *__restrict__ x, float *__restrict__ out) {
+  __shared__ float sh[1024];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += 1024) s += x[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// ---------------------------------------------------------------- Adam
+__global__ void adam_kernel(size_t n, float *__restrict__ p, const float *__restrict__ g,
+                            float *__restrict__ m, float *__restrict__ v,
+                            __nv_bfloat16 *__restrict__ w16, float lr, float b1, float b2,
+                            float eps, float bc1, float bc2) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float pi = p[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    p[i] = pi;
+    if (w16) w16[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+__global__ void cast_kernel(size_t n, const float *__restrict__ s, __nv_bfloat16 *__restrict__ d) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+int grid_for(size_t n, int tpb) {
+  size_t b = (n + tpb - 1) / tpb;
+  const size_t cap = 148 * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+}  // namespace
+
+#define BB_DISPATCH(bf16, KERNEL, GRID, BLOCK, STREAM, ...)                         \
+  do {                                                                              \
+    if (bf16)                                                                       \
+      KERNEL<__nv_bfloat16><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);              \
+    else                                                                            \
+      KERNEL<float><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                      \
+    ++g_launches;                                                                   \
+  } while (0)
+
+template <typename T> static const T *cp(const void *p) { return reinterpret_cast<const T *>(p); }
+template <typename T> static T *mp(void *p) { return reinterpret_cast<T *>(p); }
+
+cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
+                          void *y, float *mean, float *rstd, cudaStream_t s) {
+  const int grid = (R + 7) / 8;
+  if (bf16)
+    ln_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(x),
+        cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(b), mp<__nv_bfloat16>(y), mean, rstd);
+  else
+    ln_fwd_kernel<float><<<grid, 256, 0, s>>>(R, H, cp<float>(x), cp<float>(g), cp<float>(b),
+                                              mp<float>(y), mean, rstd);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const void *dy, const void *x,
+                             const float *mean, const float *rstd, const void *g,
+                             const void *dres, void *dx, cudaStream_t s) {
+  const int grid = (R + 7) / 8;
+  if (bf16)
+    ln_bwd_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(dy),
+        cp<__nv_bfloat16>(x), mean, rstd, cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(dres),
+        mp<__nv_bfloat16>(dx));
+  else
+    ln_bwd_dx_kernel<float><<<grid, 256, 0, s>>>(R, H, cp<float>(dy), cp<float>(x), mean, rstd,
+                                                 cp<float>(g), cp<float>(dres), mp<float>(dx));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+size_t colreduce_partial_floats(int R, int N) {
+  return (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;
+}
+
+cudaError_t colreduce(bool bf16, int mode, int R, int N, const void *A, const void *X,
+                      const float *mean, const float *rstd, float *partial, float *out,
+                      cudaStream_t s) {
+  const int chunks = (R + CR_ROWS - 1) / CR_ROWS;
+  dim3 grid((N + CR_COLS - 1) / CR_COLS, chunks);
+  if (bf16)
+    colreduce_partial_kernel<__nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
+        mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+  else
+    colreduce_partial_kernel<float><<<grid, CR_COLS, 0, s>>>(mode, R, N, cp<float>(A),
+                                                             cp<float>(X), mean, rstd, partial);
+  colreduce_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(chunks, N, partial, out);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const void *E,
+                      const void *Pos, void *x, cudaStream_t s) {
+  if (bf16)
+    embed_fwd_kernel<__nv_bfloat16><<<R, 128, 0, s>>>(R, S, H, tok, cp<__nv_bfloat16>(E),
+        cp<__nv_bfloat16>(Pos), mp<__nv_bfloat16>(x));
+  else
+    embed_fwd_kernel<float><<<R, 128, 0, s>>>(R, S, H, tok, cp<float>(E), cp<float>(Pos),
+                                              mp<float>(x));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t embed_bwd(bool bf16, int R, int S, int H, int U, const int32_t *uniq,
+                      const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
+                      float *dPos, cudaStream_t s) {
+  if (bf16) {
+    embed_bwd_tok_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(H, uniq, offs, pos,
+                                                          cp<__nv_bfloat16>(dx), dE);
+    embed_bwd_pos_kernel<__nv_bfloat16><<<S, 128, 0, s>>>(R / S, S, H, cp<__nv_bfloat16>(dx),
+                                                          dPos);
+  } else {
+    embed_bwd_tok_kernel<float><<<U, 128, 0, s>>>(H, uniq, offs, pos, cp<float>(dx), dE);
+    embed_bwd_pos_kernel<float><<<S, 128, 0, s>>>(R / S, S, H, cp<float>(dx), dPos);
+  }
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *targets,
+                          float inv_ntok, float *loss_rows, cudaStream_t s) {
+  if (bf16)
+    ce_kernel<__nv_bfloat16><<<R, CE_T, 0, s>>>(V, mp<__nv_bfloat16>(logits), targets, inv_ntok,
+                                                 loss_rows);
+  else
+    ce_kernel<float><<<R, CE_T, 0, s>>>(V, mp<float>(logits), targets, inv_ntok, loss_rows);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s) {
+  sum_fixed_kernel<<<1, 1024, 0, s>>>(n, x, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t adam(size_t n, float *p, const float *g, float *m, float *v, void *w16, float lr,
+                 float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  adam_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, p, g, m, v, mp<__nv_bfloat16>(w16), lr, b1, b2,
+                                                eps, bc1, bc2);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t cast_f32_to_bf16(size_t n, const float *src, void *dst, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  cast_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, src, mp<__nv_bfloat16>(dst));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t fill_nan(void *p, size_t bytes, cudaStream_t s) {
+  return cudaMemsetAsync(p, 0xFF, bytes, s);
+}
+
+}  // namespace k
+}  // namespace bb

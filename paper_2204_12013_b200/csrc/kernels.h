@@ -1,0 +1,74 @@
+// kernels.h — launchers of the sm_100a kernels (host-callable, no templates).
+// `bf16` selects the activation/parameter storage type: true = __nv_bfloat16
+// (bf16 mode), false = float (fp32 check mode). Accumulation is fp32 always.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace bb {
+namespace k {
+
+enum Epi : int { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_RES = 2, EPI_BIAS_GELU = 3,
+                 EPI_GELU_BWD = 4, EPI_ACC_F32 = 5 };
+
+// D[m][n] = sum_k A(m,k) B(n,k); A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m] (a_mn=1).
+struct Gemm {
+  int M, N, K;
+  const void *A; int lda; bool a_mn;
+  const void *B; int ldb; bool b_mn;
+  int epi;
+  void *C; int ldc;
+  const void *bias;   // [N] storage type
+  const void *res;    // [M][ldc] storage type (EPI_BIAS_RES)
+  void *aux;          // pre-activation [M][ldc] storage type (BIAS_GELU out, GELU_BWD in)
+};
+
+// Global launch counter (kernels launched by this library in this process).
+extern long long g_launches;
+
+cudaError_t gemm_simt(bool bf16, const Gemm &g, cudaStream_t s);
+cudaError_t gemm_tc(const Gemm &g, cudaStream_t s);        // bf16, tcgen05 + TMA
+bool gemm_tc_supported(const Gemm &g);
+
+cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const void *E,
+                      const void *Pos, void *x, cudaStream_t s);
+// Deterministic embedding backward: tokens of the micro-batch grouped by id
+// (host-built CSR: uniq[U], offs[U+1], pos[R] ascending within a group).
+cudaError_t embed_bwd(bool bf16, int R, int S, int H, int U, const int32_t *uniq,
+                      const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
+                      float *dPos, cudaStream_t s);
+
+cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
+                          void *y, float *mean, float *rstd, cudaStream_t s);
+// dx = dres + LN'(dy) (dres may be null). Parameter grads via colreduce.
+cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const void *dy, const void *x,
+                             const float *mean, const float *rstd, const void *g,
+                             const void *dres, void *dx, cudaStream_t s);
+// Deterministic column reductions, two passes through `partial` (>= colreduce_partial_floats):
+//   mode 0: out[n] += sum_r A[r][n]                     (bias gradient)
+//   mode 1: out[n] += sum_r A[r][n] * (X[r][n]-mean[r])*rstd[r]   (LN gamma gradient)
+size_t colreduce_partial_floats(int R, int N);
+cudaError_t colreduce(bool bf16, int mode, int R, int N, const void *A, const void *X,
+                      const float *mean, const float *rstd, float *partial, float *out,
+                      cudaStream_t s);
+
+cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
+                          void *o, float *lse, cudaStream_t s);
+// scratch: B*nh*S floats.
+cudaError_t attention_bwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
+                          const void *o, const float *lse, const void *dout, void *dqkv,
+                          float *scratch, cudaStream_t s);
+
+cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *targets,
+                          float inv_ntok, float *loss_rows, cudaStream_t s);
+// out[0] = sum of x[0..n) in a fixed order (single block).
+cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s);
+
+cudaError_t adam(size_t n, float *p, const float *g, float *m, float *v, void *w16, float lr,
+                 float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s);
+cudaError_t cast_f32_to_bf16(size_t n, const float *src, void *dst, cudaStream_t s);
+cudaError_t fill_nan(void *p, size_t bytes, cudaStream_t s);
+
+}  // namespace k
+}  // namespace bb

@@ -1,0 +1,110 @@
+// plan.h — static pipeline plans, the preemption cut, and the recovery /
+// failover plan transforms (host C++, pure integer logic).
+//
+// Rules (PAPER.md line numbers P:N; readings Q* in DESIGN.md):
+//  * contiguous layer shards, remainder on the last stages (Q6);
+//  * PipeDream 1F1B per stage;
+//  * replica of stage n on node n-1, node P-1 for stage 0, the
+//    last node loads the inputs;
+//  * FRC_FWD(k) right after SEND_ACT(k); on the last stage before RECV_ACT(k)
+//    (Q4);
+//  * failover = merge of the victim's and the shadow's lists with the four
+//    rules of P:538-545 (Q5), a lost step recomputed by lazy BRC (Q2).
+#pragma once
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace bb {
+
+enum Kind : int8_t {
+  LOAD_INPUTS, FWD, FRC_FWD, BWD, SEND_ACT, RECV_ACT, SEND_GRAD, RECV_GRAD, RESEND_GRAD,
+  REPLICA_SEND, REPLICA_RECV, APPLY
+};
+const char *kind_name(Kind k);
+bool is_send(Kind k);
+bool is_recv(Kind k);
+inline bool is_comm(Kind k) { return is_send(k) || is_recv(k); }
+
+struct Instr {
+  Kind kind;
+  int mb;     // -1 = none
+  int peer;   // node id, -1 = none
+  int stage;  // logical stage the node acts for, -1 = none
+};
+
+enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2 };
+struct Msg {
+  MsgKind kind;
+  int mb;
+  int stage;   // producing stage
+  bool operator==(const Msg &o) const { return kind == o.kind && mb == o.mb && stage == o.stage; }
+};
+Msg message_of(const Instr &i);
+
+// Data keys of the symbolic store (mirrors of the runtime buffers).
+enum KeyType : int8_t { K_TOK, K_TGT, K_ACT, K_DACT, K_SAVED, K_LOSS, K_GRADSUM };
+struct Key {
+  KeyType t;
+  int a, b;
+  bool operator<(const Key &o) const { return std::tie(t, a, b) < std::tie(o.t, o.a, o.b); }
+  bool operator==(const Key &o) const { return t == o.t && a == o.a && b == o.b; }
+};
+std::vector<Key> inputs_of(const Instr &i, int P);
+std::vector<Key> outputs_of(const Instr &i, int P, int M);
+
+using Plans = std::map<int, std::vector<Instr>>;
+using ChanKey = std::tuple<int, int, int>;                  // (src node, dst node, MsgKind)
+using Channels = std::map<ChanKey, std::deque<Msg>>;
+
+struct PlanError : std::exception {
+  std::string msg;
+  explicit PlanError(std::string m) : msg(std::move(m)) {}
+  const char *what() const noexcept override { return msg.c_str(); }
+};
+
+// Stage unit ranges [a, b] inclusive (units: 0 emb, 1..L blocks, L+1 head).
+std::vector<std::pair<int, int>> partition(int n_layer, int P, const int *layers_per_stage);
+
+std::vector<Instr> stage_plan(int s, int P, int M, bool rc);
+Plans normal_plans(int P, int M, bool rc);
+
+// Round-robin lockstep (one instruction per node per round, ascending node
+// id); RECVs wait for their message, SENDs are buffered per (src,dst,kind).
+// cap: node -> max instructions. on_exec(node, instr).
+void lockstep(const Plans &plans, std::map<int, int> &pcs, Channels &ch,
+              const std::map<int, int> &cap,
+              const std::function<void(int, const Instr &)> &on_exec = nullptr);
+
+struct Cut {
+  std::map<int, int> pcs;   // instructions executed per node
+  Channels ch;              // undelivered messages (to the victim removed)
+};
+Cut cut(const Plans &plans, int victim, int pi);
+
+struct RecoveryInfo {
+  int victim = -1, shadow = -1, successor = -1;
+  bool commit = false;
+  std::vector<int> frc_done, brc_mb, resend;
+};
+Plans recovery_plans(const Plans &plans, int P, int M, int victim, const std::map<int, int> &pcs,
+                     const Channels &ch, RecoveryInfo *info);
+Plans failover_plans(int P, int M, int victim);
+
+struct Topology {
+  std::vector<int> host;        // stage -> node
+  std::vector<int> replica_on;  // stage -> node holding its replica, -1 none
+};
+Topology normal_topology(int P, bool rc);
+Topology failover_topology(int P, int victim);
+
+std::string dump(int P, int M, bool rc, const std::vector<std::pair<int, int>> &ranges,
+                 const Plans &plans, const Topology &topo, const std::vector<int> &node_device,
+                 bool failover, int victim);
+std::string dump_lines(const Plans &plans);
+
+}  // namespace bb

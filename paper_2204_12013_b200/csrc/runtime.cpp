@@ -1,0 +1,1144 @@
+// runtime.cpp — see runtime.h. Interprets the per-node instruction lists of
+// plan.h by enqueuing kernels and NCCL P2P on CUDA streams; no host blocking
+// on the GPU except at the end of a step.
+#include "runtime.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+namespace bb {
+
+namespace {
+struct RtError {
+  bb_status st;
+  std::string msg;
+};
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw RtError{e_ == cudaErrorMemoryAllocation ? BB_E_OOM : BB_E_CUDA,                \
+                    std::string(#x) + ": " + cudaGetErrorString(e_)};                      \
+  } while (0)
+#define NK(x)                                                                              \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess)                                                                 \
+      throw RtError{BB_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)};           \
+  } while (0)
+
+constexpr size_t ALIGN = 256;
+size_t al(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+void *dmalloc(size_t bytes) {
+  void *p = nullptr;
+  if (bytes == 0) bytes = ALIGN;
+  CK(cudaMalloc(&p, bytes));
+  return p;
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+}  // namespace
+
+// ------------------------------------------------------------ param layout
+size_t unit_param_count(const Dims &d, int unit) {
+  const size_t H = d.H, F = d.F, V = d.V, S = d.S;
+  if (unit == 0) return V * H + S * H;
+  if (unit == d.L + 1) return 2 * H + V * H;
+  return 2 * H + 3 * H * H + 3 * H + H * H + H + 2 * H + F * H + F + H * F + H;
+}
+
+std::vector<std::pair<size_t, size_t>> unit_param_ranges(const Dims &d) {
+  std::vector<std::pair<size_t, size_t>> r;
+  size_t off = 0;
+  for (int u = 0; u < d.L + 2; ++u) {
+    const size_t n = unit_param_count(d, u);
+    r.push_back({off, n});
+    off += n;
+  }
+  return r;
+}
+
+static StageInfo make_stage(const Dims &d, int X, int ua, int ub) {
+  StageInfo si;
+  si.X = X;
+  si.ua = ua;
+  si.ub = ub;
+  auto ur = unit_param_ranges(d);
+  si.poff = ur[ua].first;
+  si.pcount = ur[ub].first + ur[ub].second - si.poff;
+  const size_t H = d.H, F = d.F, V = d.V, S = d.S;
+  const size_t R = d.R(), T = 0;  // placeholder
+  (void)T;
+  size_t slot = 0;
+  for (int u = ua; u <= ub; ++u) {
+    UnitP p{};
+    p.unit = u;
+    size_t o = ur[u].first - si.poff;
+    UnitS s{};
+    if (u == 0) {
+      p.kind = 0;
+      p.tok = o;
+      p.pos = o + V * H;
+    } else if (u == d.L + 1) {
+      p.kind = 2;
+      p.lnfg = o;
+      p.lnfb = o + H;
+      p.whead = o + 2 * H;
+    } else {
+      p.kind = 1;
+      p.ln1g = o; o += H;
+      p.ln1b = o; o += H;
+      p.wqkv = o; o += 3 * H * H;
+      p.bqkv = o; o += 3 * H;
+      p.wo = o; o += H * H;
+      p.bo = o; o += H;
+      p.ln2g = o; o += H;
+      p.ln2b = o; o += H;
+      p.w1 = o; o += F * H;
+      p.b1 = o; o += F;
+      p.w2 = o; o += H * F;
+      p.b2 = o; o += H;
+    }
+    si.up.push_back(p);
+    si.us.push_back(s);
+  }
+  (void)S;
+  (void)R;
+  si.slot_bytes = 0;
+  return si;
+}
+
+// Saved-set layout (needs the storage type size).
+static void layout_slots(const Dims &d, size_t tsz, StageInfo &si) {
+  const size_t H = d.H, F = d.F, V = d.V, R = d.R();
+  const size_t B = d.mb, nh = d.nh, S = d.S;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o += al(bytes);
+    return r;
+  };
+  for (size_t i = 0; i < si.up.size(); ++i) {
+    const UnitP &p = si.up[i];
+    UnitS &s = si.us[i];
+    const bool last = (int)i == (int)si.up.size() - 1;
+    if (p.kind == 1) {
+      s.h1 = take(R * H * tsz);
+      s.mean1 = take(R * 4);
+      s.rstd1 = take(R * 4);
+      s.qkv = take(R * 3 * H * tsz);
+      s.o = take(R * H * tsz);
+      s.lse = take(B * nh * S * 4);
+      s.x1 = take(R * H * tsz);
+      s.h2 = take(R * H * tsz);
+      s.mean2 = take(R * 4);
+      s.rstd2 = take(R * 4);
+      s.pre = take(R * F * tsz);
+      s.act = take(R * F * tsz);
+    } else if (p.kind == 2) {
+      s.hf = take(R * H * tsz);
+      s.meanf = take(R * 4);
+      s.rstdf = take(R * 4);
+      s.dlog = take(R * V * tsz);
+    }
+    if (!last && p.kind != 2) s.out = take(R * H * tsz);
+  }
+  si.slot_bytes = al(o);
+}
+
+// ================================================================ helpers
+namespace {
+cudaEvent_t new_event(Node &nd) {
+  if (nd.evnext == nd.evpool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    nd.evpool.push_back(e);
+  }
+  return nd.evpool[nd.evnext++];
+}
+
+cudaEvent_t record(Node &nd, cudaStream_t s) {
+  cudaEvent_t e = new_event(nd);
+  CK(cudaEventRecord(e, s));
+  return e;
+}
+
+void wait_ev(cudaStream_t s, cudaEvent_t e) {
+  if (e) CK(cudaStreamWaitEvent(s, e, 0));
+}
+
+void *arena_alloc(Node &nd, size_t bytes) {
+  const size_t b = al(bytes);
+  if (nd.arena_used + b > nd.arena_bytes) throw RtError{BB_E_OOM, "step arena exhausted"};
+  void *p = nd.arena + nd.arena_used;
+  nd.arena_used += b;
+  return p;
+}
+
+const Entry &need(Node &nd, const Key &k) {
+  auto it = nd.store.find(k);
+  if (it == nd.store.end()) {
+    std::ostringstream o;
+    o << "node " << nd.n << ": missing data key (" << (int)k.t << "," << k.a << "," << k.b << ")";
+    throw RtError{BB_E_STATE, o.str()};
+  }
+  return it->second;
+}
+
+struct Prof {
+  Ctx &c;
+  Node &nd;
+  cudaStream_t s;
+  int cls;
+  double work;
+  cudaEvent_t a = nullptr;
+  Prof(Ctx &c_, Node &nd_, cudaStream_t s_, int cls_, double w) : c(c_), nd(nd_), s(s_), cls(cls_), work(w) {
+    if (c.o.profile) a = take();
+    if (a) CK(cudaEventRecord(a, s));
+  }
+  cudaEvent_t take() {
+    if (c.prof_next == c.prof_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c.prof_pool.push_back(e);
+    }
+    return c.prof_pool[c.prof_next++];
+  }
+  ~Prof() noexcept(false) {
+    if (!a) return;
+    cudaEvent_t b = take();
+    CK(cudaEventRecord(b, s));
+    c.prof.push_back({cls, a, b, work});
+  }
+};
+
+enum ProfCls { PC_GEMM_FWD = 0, PC_GEMM_DX, PC_GEMM_DW, PC_ATTN_FWD, PC_ATTN_BWD, PC_LN, PC_CE,
+               PC_EMB, PC_ADAM, PC_REDUCE, PC_N };
+const char *prof_names[PC_N] = {"gemm_fwd", "gemm_dx", "gemm_dw", "attn_fwd", "attn_bwd",
+                                "layernorm", "cross_entropy", "embedding", "adam", "colreduce"};
+
+void gemm(Ctx &c, Node &nd, cudaStream_t s, int cls, const k::Gemm &g) {
+  Prof pf(c, nd, s, cls, 2.0 * g.M * (double)g.N * g.K);
+  cudaError_t e;
+  if (c.bf16 && k::gemm_tc_supported(g))
+    e = k::gemm_tc(g, s);
+  else
+    e = k::gemm_simt(c.bf16, g, s);
+  CK(e);
+}
+}  // namespace
+
+// ============================================================== unit math
+namespace {
+const void *pw(const Ctx &c, const Copy &cp, size_t off) {
+  return static_cast<const char *>(cp.work) + off * c.act_bytes;
+}
+float *pg(const Copy &cp, size_t off) { return cp.grad + off; }
+
+// Forward of stage X for micro-batch k on stream s. Returns the output
+// pointer (activation in the arena) or nullptr for the last stage.
+void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStream_t s,
+                   const void *x_in, void *x_out, float *loss_rows) {
+  const Dims &d = c.d;
+  const StageInfo &si = c.stages[X];
+  char *sl = cp.slots + (size_t)slot * si.slot_bytes;
+  const int R = d.R(), H = d.H, F = d.F;
+  const bool b16 = c.bf16;
+  const void *x = x_in;
+  for (size_t i = 0; i < si.up.size(); ++i) {
+    const UnitP &p = si.up[i];
+    const UnitS &u = si.us[i];
+    const bool last = i + 1 == si.up.size();
+    void *out = last ? x_out : (p.kind == 2 ? nullptr : sl + u.out);
+    if (p.kind == 0) {
+      Prof pf(c, nd, s, PC_EMB, 0);
+      CK(k::embed_fwd(b16, R, d.S, H, nd.d_tok + (size_t)k * R, pw(c, cp, p.tok),
+                      pw(c, cp, p.pos), out, s));
+    } else if (p.kind == 1) {
+      {
+        Prof pf(c, nd, s, PC_LN, 0);
+        CK(k::layernorm_fwd(b16, R, H, x, pw(c, cp, p.ln1g), pw(c, cp, p.ln1b), sl + u.h1,
+                            (float *)(sl + u.mean1), (float *)(sl + u.rstd1), s));
+      }
+      gemm(c, nd, s, PC_GEMM_FWD,
+           {R, 3 * H, H, sl + u.h1, H, false, pw(c, cp, p.wqkv), H, false, k::EPI_BIAS,
+            sl + u.qkv, 3 * H, pw(c, cp, p.bqkv), nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_ATTN_FWD, 0);
+        CK(k::attention_fwd(b16, d.mb, d.S, H, d.nh, d.causal, sl + u.qkv, sl + u.o,
+                            (float *)(sl + u.lse), s));
+      }
+      gemm(c, nd, s, PC_GEMM_FWD,
+           {R, H, H, sl + u.o, H, false, pw(c, cp, p.wo), H, false, k::EPI_BIAS_RES, sl + u.x1, H,
+            pw(c, cp, p.bo), x, nullptr});
+      {
+        Prof pf(c, nd, s, PC_LN, 0);
+        CK(k::layernorm_fwd(b16, R, H, sl + u.x1, pw(c, cp, p.ln2g), pw(c, cp, p.ln2b),
+                            sl + u.h2, (float *)(sl + u.mean2), (float *)(sl + u.rstd2), s));
+      }
+      gemm(c, nd, s, PC_GEMM_FWD,
+           {R, F, H, sl + u.h2, H, false, pw(c, cp, p.w1), H, false, k::EPI_BIAS_GELU, sl + u.act,
+            F, pw(c, cp, p.b1), nullptr, sl + u.pre});
+      gemm(c, nd, s, PC_GEMM_FWD,
+           {R, H, F, sl + u.act, F, false, pw(c, cp, p.w2), F, false, k::EPI_BIAS_RES, out, H,
+            pw(c, cp, p.b2), sl + u.x1, nullptr});
+    } else {
+      {
+        Prof pf(c, nd, s, PC_LN, 0);
+        CK(k::layernorm_fwd(b16, R, H, x, pw(c, cp, p.lnfg), pw(c, cp, p.lnfb), sl + u.hf,
+                            (float *)(sl + u.meanf), (float *)(sl + u.rstdf), s));
+      }
+      gemm(c, nd, s, PC_GEMM_FWD,
+           {R, d.V, H, sl + u.hf, H, false, pw(c, cp, p.whead), H, false, k::EPI_STORE,
+            sl + u.dlog, d.V, nullptr, nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_CE, 0);
+        const float inv = 1.0f / (float)((double)d.M * d.mb * d.S);
+        CK(k::cross_entropy(b16, R, d.V, sl + u.dlog, nd.d_tgt + (size_t)k * R, inv, loss_rows,
+                            s));
+        CK(k::sum_fixed(R, loss_rows, cp.loss + k, s));
+      }
+    }
+    x = out;
+  }
+}
+
+// Backward of stage X for micro-batch k (main stream). dout = gradient w.r.t.
+// the stage output (nullptr for the last stage); x_in = stage input act.
+// Writes the gradient w.r.t. the stage input into dx_out (if X > 0).
+void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStream_t s,
+                    const void *x_in, const void *dout, void *dx_out) {
+  const Dims &d = c.d;
+  const StageInfo &si = c.stages[X];
+  char *sl = cp.slots + (size_t)slot * si.slot_bytes;
+  const int R = d.R(), H = d.H, F = d.F;
+  const bool b16 = c.bf16;
+  const void *dy = dout;
+  int flip = 0;
+  for (int i = (int)si.up.size() - 1; i >= 0; --i) {
+    const UnitP &p = si.up[i];
+    const UnitS &u = si.us[i];
+    const void *x = i == 0 ? x_in : (const void *)(sl + si.us[i - 1].out);
+    void *dx = i == 0 ? dx_out : nd.sH[3 + flip];
+    flip ^= 1;
+    if (p.kind == 0) {
+      Prof pf(c, nd, s, PC_EMB, 0);
+      const int32_t *csr = nd.d_csr + (size_t)k * c.csr_stride;
+      const int U = c.csr_U[k];
+      CK(k::embed_bwd(b16, R, d.S, H, U, csr, csr + R, csr + 2 * R + 1, dy, pg(cp, p.tok),
+                      pg(cp, p.pos), s));
+    } else if (p.kind == 2) {
+      gemm(c, nd, s, PC_GEMM_DX,
+           {R, H, d.V, sl + u.dlog, d.V, false, pw(c, cp, p.whead), H, true, k::EPI_STORE,
+            nd.sH[0], H, nullptr, nullptr, nullptr});
+      gemm(c, nd, s, PC_GEMM_DW,
+           {d.V, H, R, sl + u.dlog, d.V, true, sl + u.hf, H, true, k::EPI_ACC_F32,
+            pg(cp, p.whead), H, nullptr, nullptr, nullptr});
+      Prof pf(c, nd, s, PC_LN, 0);
+      CK(k::layernorm_bwd_dx(b16, R, H, nd.sH[0], x, (float *)(sl + u.meanf),
+                             (float *)(sl + u.rstdf), pw(c, cp, p.lnfg), nullptr, dx, s));
+      CK(k::colreduce(b16, 1, R, H, nd.sH[0], x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
+                      nd.s_part, pg(cp, p.lnfg), s));
+      CK(k::colreduce(b16, 0, R, H, nd.sH[0], nullptr, nullptr, nullptr, nd.s_part,
+                      pg(cp, p.lnfb), s));
+    } else {
+      void *dpre = nd.sF, *dh2 = nd.sH[0], *dx1 = nd.sH[1], *dO = nd.sH[2], *dqkv = nd.s3;
+      gemm(c, nd, s, PC_GEMM_DX,
+           {R, F, H, dy, H, false, pw(c, cp, p.w2), F, true, k::EPI_GELU_BWD, dpre, F, nullptr,
+            nullptr, sl + u.pre});
+      gemm(c, nd, s, PC_GEMM_DW,
+           {H, F, R, dy, H, true, sl + u.act, F, true, k::EPI_ACC_F32, pg(cp, p.w2), F, nullptr,
+            nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_REDUCE, 0);
+        CK(k::colreduce(b16, 0, R, H, dy, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.b2), s));
+      }
+      gemm(c, nd, s, PC_GEMM_DX,
+           {R, H, F, dpre, F, false, pw(c, cp, p.w1), H, true, k::EPI_STORE, dh2, H, nullptr,
+            nullptr, nullptr});
+      gemm(c, nd, s, PC_GEMM_DW,
+           {F, H, R, dpre, F, true, sl + u.h2, H, true, k::EPI_ACC_F32, pg(cp, p.w1), H, nullptr,
+            nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_REDUCE, 0);
+        CK(k::colreduce(b16, 0, R, F, dpre, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.b1),
+                        s));
+      }
+      {
+        Prof pf(c, nd, s, PC_LN, 0);
+        CK(k::layernorm_bwd_dx(b16, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
+                               (float *)(sl + u.rstd2), pw(c, cp, p.ln2g), dy, dx1, s));
+        CK(k::colreduce(b16, 1, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
+                        (float *)(sl + u.rstd2), nd.s_part, pg(cp, p.ln2g), s));
+        CK(k::colreduce(b16, 0, R, H, dh2, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.ln2b),
+                        s));
+      }
+      gemm(c, nd, s, PC_GEMM_DX,
+           {R, H, H, dx1, H, false, pw(c, cp, p.wo), H, true, k::EPI_STORE, dO, H, nullptr,
+            nullptr, nullptr});
+      gemm(c, nd, s, PC_GEMM_DW,
+           {H, H, R, dx1, H, true, sl + u.o, H, true, k::EPI_ACC_F32, pg(cp, p.wo), H, nullptr,
+            nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_REDUCE, 0);
+        CK(k::colreduce(b16, 0, R, H, dx1, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.bo), s));
+      }
+      {
+        Prof pf(c, nd, s, PC_ATTN_BWD, 0);
+        CK(k::attention_bwd(b16, d.mb, d.S, H, d.nh, d.causal, sl + u.qkv, sl + u.o,
+                            (float *)(sl + u.lse), dO, dqkv, nd.s_attn, s));
+      }
+      void *dh1 = nd.sH[0];
+      gemm(c, nd, s, PC_GEMM_DX,
+           {R, H, 3 * H, dqkv, 3 * H, false, pw(c, cp, p.wqkv), H, true, k::EPI_STORE, dh1, H,
+            nullptr, nullptr, nullptr});
+      gemm(c, nd, s, PC_GEMM_DW,
+           {3 * H, H, R, dqkv, 3 * H, true, sl + u.h1, H, true, k::EPI_ACC_F32, pg(cp, p.wqkv), H,
+            nullptr, nullptr, nullptr});
+      {
+        Prof pf(c, nd, s, PC_REDUCE, 0);
+        CK(k::colreduce(b16, 0, R, 3 * H, dqkv, nullptr, nullptr, nullptr, nd.s_part,
+                        pg(cp, p.bqkv), s));
+      }
+      {
+        Prof pf(c, nd, s, PC_LN, 0);
+        CK(k::layernorm_bwd_dx(b16, R, H, dh1, x, (float *)(sl + u.mean1),
+                               (float *)(sl + u.rstd1), pw(c, cp, p.ln1g), dx1, dx, s));
+        CK(k::colreduce(b16, 1, R, H, dh1, x, (float *)(sl + u.mean1), (float *)(sl + u.rstd1),
+                        nd.s_part, pg(cp, p.ln1g), s));
+        CK(k::colreduce(b16, 0, R, H, dh1, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.ln1b),
+                        s));
+      }
+    }
+    dy = dx;
+  }
+}
+}  // namespace
+
+
+// ============================================================ interpreter
+namespace {
+bool is_local(const Ctx &c, int n) { return c.node_rank[n] == c.o.world_rank; }
+
+size_t msg_count(const Ctx &c, MsgKind kind, int stage) {
+  if (kind == MSG_GRADSUM) return c.stages[stage].pcount;
+  return (size_t)c.d.R() * c.d.H;
+}
+size_t msg_bytes(const Ctx &c, MsgKind kind, int stage) {
+  return msg_count(c, kind, stage) * (kind == MSG_GRADSUM ? sizeof(float) : c.act_bytes);
+}
+ncclDataType_t msg_type(const Ctx &c, MsgKind kind) {
+  if (kind == MSG_GRADSUM || !c.bf16) return ncclFloat32;
+  return ncclBfloat16;
+}
+
+Key payload_key(const Instr &ins) {
+  switch (ins.kind) {
+    case SEND_ACT: return {K_ACT, ins.stage + 1, ins.mb};
+    case SEND_GRAD:
+    case RESEND_GRAD: return {K_DACT, ins.stage, ins.mb};
+    default: return {K_GRADSUM, ins.stage, 0};
+  }
+}
+
+struct Phase {
+  bool drop_to_victim = false;   // prefix of an interrupted step
+  int victim = -1;
+};
+
+// Execute one instruction of node nd; false = blocked on a local message.
+bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
+  const Dims &d = c.d;
+  const int P = d.P, M = d.M, k = ins.mb, X = ins.stage;
+  switch (ins.kind) {
+    case LOAD_INPUTS: {
+      const size_t n = (size_t)M * d.R();
+      CK(cudaMemcpyAsync(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice, nd.main));
+      CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice, nd.main));
+      CK(cudaMemcpyAsync(nd.d_csr, c.h_csr, (size_t)M * c.csr_stride * 4, cudaMemcpyHostToDevice,
+                         nd.main));
+      c.h2d += 2 * n * 4 + (size_t)M * c.csr_stride * 4;
+      cudaEvent_t e = record(nd, nd.main);
+      for (int j = 0; j < M; ++j) {
+        nd.store[{K_TOK, j, 0}] = {nd.d_tok + (size_t)j * d.R(), e};
+        nd.store[{K_TGT, j, 0}] = {nd.d_tgt + (size_t)j * d.R(), e};
+      }
+      return true;
+    }
+    case FWD:
+    case FRC_FWD: {
+      Copy &cp = nd.copies.at(X);
+      cudaStream_t s = ins.kind == FRC_FWD ? nd.frc : nd.main;
+      const void *x_in = nullptr;
+      if (X == 0) {
+        wait_ev(s, need(nd, {K_TOK, k, 0}).ev);
+      } else {
+        const Entry &e = need(nd, {K_ACT, X, k});
+        wait_ev(s, e.ev);
+        x_in = e.p;
+      }
+      if (X == P - 1) wait_ev(s, need(nd, {K_TGT, k, 0}).ev);
+      if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
+      const int slot = cp.free_slots.back();
+      cp.free_slots.pop_back();
+      void *out = X < P - 1 ? arena_alloc(nd, msg_bytes(c, MSG_ACT, X)) : nullptr;
+      stage_forward(c, nd, cp, X, k, slot, s, x_in, out,
+                    s == nd.main ? nd.s_loss_main : nd.s_loss_frc);
+      cudaEvent_t e = record(nd, s);
+      nd.store[{K_SAVED, X, k}] = {nullptr, e, slot};
+      if (X < P - 1)
+        nd.store[{K_ACT, X + 1, k}] = {out, e};
+      else
+        nd.store[{K_LOSS, k, 0}] = {cp.loss + k, e};
+      return true;
+    }
+    case BWD: {
+      Copy &cp = nd.copies.at(X);
+      const Entry sv = need(nd, {K_SAVED, X, k});
+      wait_ev(nd.main, sv.ev);
+      const void *dout = nullptr;
+      if (X < P - 1) {
+        const Entry &e = need(nd, {K_DACT, X + 1, k});
+        wait_ev(nd.main, e.ev);
+        dout = e.p;
+      }
+      const void *x_in = X == 0 ? nullptr : need(nd, {K_ACT, X, k}).p;
+      void *dx = X > 0 ? arena_alloc(nd, msg_bytes(c, MSG_GRAD, X)) : nullptr;
+      stage_backward(c, nd, cp, X, k, sv.slot, nd.main, x_in, dout, dx);
+      cudaEvent_t e = record(nd, nd.main);
+      cp.free_slots.push_back(sv.slot);
+      if (X > 0) nd.store[{K_DACT, X, k}] = {dx, e};
+      if (k == M - 1) nd.store[{K_GRADSUM, X, 0}] = {cp.grad, e};
+      return true;
+    }
+    case SEND_ACT:
+    case SEND_GRAD:
+    case RESEND_GRAD:
+    case REPLICA_SEND: {
+      const Msg m = message_of(ins);
+      const ChanKey ck{nd.n, ins.peer, (int)m.kind};
+      if (ph.drop_to_victim && ins.peer == ph.victim) {
+        // the victim never receives it: a survivor cannot deliver to a dead node
+        const int sent = ++c.sent_to_victim[ck];
+        auto it = c.victim_consumed.find(ck);
+        if (it == c.victim_consumed.end() || sent > it->second) return true;
+      }
+      const Entry &pl = need(nd, payload_key(ins));
+      const size_t bytes = msg_bytes(c, m.kind, m.stage);
+      if (is_local(c, ins.peer)) {
+        Node &dst = c.nodes.at(ins.peer);
+        void *dp = m.kind == MSG_GRADSUM ? (void *)dst.copies.at(X).grad : arena_alloc(dst, bytes);
+        wait_ev(nd.main, pl.ev);
+        CK(cudaMemcpyAsync(dp, pl.p, bytes, cudaMemcpyDeviceToDevice, nd.main));
+        c.mail[ck].push_back({dp, record(nd, nd.main)});
+      } else {
+        EdgeComm &ed = c.edges.at(std::make_tuple(nd.n, ins.peer, (int)m.kind));
+        wait_ev(ed.stream, pl.ev);
+        NK(ncclSend(pl.p, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 1, ed.comm,
+                    ed.stream));
+      }
+      return true;
+    }
+    case RECV_ACT:
+    case RECV_GRAD:
+    case REPLICA_RECV: {
+      const Msg m = message_of(ins);
+      const ChanKey ck{ins.peer, nd.n, (int)m.kind};
+      Entry got;
+      if (is_local(c, ins.peer)) {
+        auto it = c.mail.find(ck);
+        if (it == c.mail.end() || it->second.empty()) return false;
+        got = it->second.front();
+        it->second.pop_front();
+      } else {
+        EdgeComm &ed = c.edges.at(std::make_tuple(ins.peer, nd.n, (int)m.kind));
+        void *dp = m.kind == MSG_GRADSUM ? (void *)nd.copies.at(X).grad
+                                         : arena_alloc(nd, msg_bytes(c, m.kind, m.stage));
+        NK(ncclRecv(dp, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 0, ed.comm,
+                    ed.stream));
+        got = {dp, record(nd, ed.stream)};
+      }
+      if (ins.kind == RECV_ACT)
+        nd.store[{K_ACT, X, k}] = got;
+      else if (ins.kind == RECV_GRAD)
+        nd.store[{K_DACT, X + 1, k}] = got;
+      else
+        nd.store[{K_GRADSUM, X, 0}] = {nd.copies.at(X).grad, got.ev};
+      return true;
+    }
+    case APPLY: {
+      Copy &cp = nd.copies.at(X);
+      wait_ev(nd.main, need(nd, {K_GRADSUM, X, 0}).ev);
+      wait_ev(nd.main, record(nd, nd.frc));   // the FRC stream read these parameters
+      cp.t += 1;
+      const double b1 = c.o.beta1, b2 = c.o.beta2;
+      const float bc1 = (float)(1.0 - std::pow(b1, cp.t)), bc2 = (float)(1.0 - std::pow(b2, cp.t));
+      Prof pf(c, nd, nd.main, PC_ADAM, 16.0 * c.stages[X].pcount);
+      CK(k::adam(c.stages[X].pcount, cp.master, cp.grad, cp.m, cp.v, c.bf16 ? cp.work : nullptr,
+                 c.o.lr, c.o.beta1, c.o.beta2, c.o.eps, bc1, bc2, nd.main));
+      return true;
+    }
+  }
+  return true;
+}
+
+// Run the local nodes' lists; lim[n] caps node n (prefix of an interrupted step).
+void run(Ctx &c, const Plans &lists, const std::map<int, int> *lim, const Phase &ph) {
+  std::map<int, size_t> pc;
+  for (auto &kv : c.nodes)
+    if (kv.second.alive && lists.count(kv.first)) pc[kv.first] = 0;
+  bool progress = true;
+  while (progress) {
+    progress = false;
+    for (auto &kv : pc) {
+      Node &nd = c.nodes.at(kv.first);
+      const auto &seq = lists.at(kv.first);
+      size_t cap = seq.size();
+      if (lim) cap = std::min(cap, (size_t)lim->at(kv.first));
+      while (kv.second < cap && exec(c, nd, seq[kv.second], ph)) {
+        ++kv.second;
+        progress = true;
+      }
+    }
+  }
+  for (auto &kv : pc) {
+    const auto &seq = lists.at(kv.first);
+    size_t cap = seq.size();
+    if (lim) cap = std::min(cap, (size_t)lim->at(kv.first));
+    if (kv.second < cap) {
+      std::ostringstream o;
+      o << "local deadlock at node " << kv.first << " instruction " << kv.second;
+      throw RtError{BB_E_STATE, o.str()};
+    }
+  }
+}
+
+void sync_all(Ctx &c, bool comm_too) {
+  for (auto &kv : c.nodes) {
+    CK(cudaStreamSynchronize(kv.second.main));
+    CK(cudaStreamSynchronize(kv.second.frc));
+  }
+  if (comm_too)
+    for (auto &kv : c.edges) CK(cudaStreamSynchronize(kv.second.stream));
+}
+
+void begin_step(Ctx &c) {
+  c.mail.clear();
+  c.prof.clear();
+  c.prof_next = 0;
+  c.h2d = c.d2h = 0;
+  c.launches_at_start = k::g_launches;
+  for (auto &kv : c.nodes) {
+    Node &nd = kv.second;
+    if (!nd.alive) continue;
+    nd.evnext = 0;
+    nd.store.clear();
+    nd.arena_used = 0;
+    for (auto &cc : nd.copies) {
+      Copy &cp = cc.second;
+      cp.free_slots.clear();
+      for (int i = cp.nslots - 1; i >= 0; --i) cp.free_slots.push_back(i);
+      CK(cudaMemsetAsync(cp.grad, 0, c.stages[cp.X].pcount * sizeof(float), nd.main));
+    }
+    CK(cudaEventRecord(nd.t0, nd.main));
+  }
+}
+
+// Host staging: tokens, targets and the per-micro-batch token CSR used by the
+// deterministic embedding backward.
+void stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
+  const Dims &d = c.d;
+  const size_t R = d.R();
+  std::memcpy(c.h_tok, tok, (size_t)d.M * R * 4);
+  std::memcpy(c.h_tgt, tgt, (size_t)d.M * R * 4);
+  std::vector<int32_t> idx(R);
+  for (int k = 0; k < d.M; ++k) {
+    const int32_t *t = tok + (size_t)k * R;
+    int32_t *blob = c.h_csr + (size_t)k * c.csr_stride;
+    int32_t *uniq = blob, *offs = blob + R, *pos = blob + 2 * R + 1;
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return t[a] < t[b]; });
+    int U = 0;
+    for (size_t i = 0; i < R; ++i) {
+      if (i == 0 || t[idx[i]] != t[idx[i - 1]]) {
+        uniq[U] = t[idx[i]];
+        offs[U] = (int)i;
+        ++U;
+      }
+      pos[i] = idx[i];
+    }
+    offs[U] = (int)R;
+    c.csr_U[k] = U;
+  }
+}
+
+float read_loss(Ctx &c) {
+  const int X = c.d.P - 1;
+  const int n = c.topo.host[X];
+  if (!c.nodes.count(n) || !c.nodes.at(n).alive) return NAN;
+  Node &nd = c.nodes.at(n);
+  Copy &cp = nd.copies.at(X);
+  float *tmp = nd.s_loss_main;   // scratch: loss rows are no longer needed
+  CK(k::sum_fixed(c.d.M, cp.loss, tmp, nd.main));
+  float h = NAN;
+  CK(cudaMemcpyAsync(&h, tmp, 4, cudaMemcpyDeviceToHost, nd.main));
+  CK(cudaStreamSynchronize(nd.main));
+  c.d2h += 4;
+  return h;
+}
+
+void finish_stats(Ctx &c, bb_step_stats *st, double t0) {
+  if (!st) return;
+  float dev = 0.f;
+  for (auto &kv : c.nodes) {
+    Node &nd = kv.second;
+    if (!nd.alive) continue;
+    CK(cudaEventRecord(nd.t1, nd.main));
+    CK(cudaEventSynchronize(nd.t1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, nd.t0, nd.t1));
+    dev = std::max(dev, ms);
+  }
+  st->device_ms = dev;
+  st->step_ms = (float)(now_ms() - t0);
+  st->gpu_launches = (int)(k::g_launches - c.launches_at_start);
+  st->h2d_bytes = c.h2d;
+  st->d2h_bytes = c.d2h;
+}
+}  // namespace
+
+// ================================================================= API
+bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
+  try {
+    if (!m || P < 1 || M < 1) throw RtError{BB_E_INVAL, "bad arguments"};
+    bb_opts def;
+    bb_default_opts(&def);
+    c.o = o ? *o : def;
+    if (c.o.world_size < 1 || c.o.world_rank < 0 || c.o.world_rank >= c.o.world_size)
+      throw RtError{BB_E_INVAL, "bad world rank/size"};
+    if (m->n_layer < P) throw RtError{BB_E_INVAL, "n_layer < stages"};
+    if (c.o.rc != BB_RC_NONE && P < 2) throw RtError{BB_E_INVAL, "RC needs stages >= 2"};
+    if (m->n_head <= 0 || m->d_model % m->n_head) throw RtError{BB_E_INVAL, "d_model % n_head"};
+    if (m->d_model % 8 || m->d_ff % 8 || m->vocab % 8 || m->d_model / m->n_head > 64)
+      throw RtError{BB_E_INVAL, "d_model, d_ff, vocab must be multiples of 8; head dim <= 64"};
+    if (c.o.micro_batch < 1) throw RtError{BB_E_INVAL, "micro_batch < 1"};
+    c.d = {m->n_layer, m->d_model, m->n_head, m->d_ff, m->vocab, m->seq_len, m->causal ? 1 : 0,
+           P, M, c.o.micro_batch};
+    c.bf16 = c.o.prec == BB_PREC_BF16;
+    c.act_bytes = c.bf16 ? 2 : 4;
+    const bool rc = c.o.rc != BB_RC_NONE;
+    try {
+      c.ranges = partition(m->n_layer, P, c.o.layers_per_stage);
+      c.plans = normal_plans(P, M, rc);
+    } catch (const PlanError &e) {
+      throw RtError{BB_E_INVAL, e.msg};
+    }
+    c.topo = normal_topology(P, rc);
+    for (int X = 0; X < P; ++X) {
+      c.stages.push_back(make_stage(c.d, X, c.ranges[X].first, c.ranges[X].second));
+      layout_slots(c.d, c.act_bytes, c.stages.back());
+    }
+    auto ur = unit_param_ranges(c.d);
+    c.total_params = ur.back().first + ur.back().second;
+    // node -> rank
+    c.node_rank.resize(P);
+    const int per = (P + c.o.world_size - 1) / c.o.world_size;
+    for (int n = 0; n < P; ++n) {
+      c.node_rank[n] = c.o.node_rank ? c.o.node_rank[n] : std::min(n / per, c.o.world_size - 1);
+      if (c.node_rank[n] < 0 || c.node_rank[n] >= c.o.world_size)
+        throw RtError{BB_E_INVAL, "bad node_rank"};
+    }
+    c.node_device.assign(P, 0);
+    for (int n = 0; n < P; ++n) c.node_device[n] = c.node_rank[n];
+    CK(cudaSetDevice(c.o.device));
+    const size_t R = c.d.R();
+    c.csr_stride = 3 * R + 1;
+    CK(cudaMallocHost(&c.h_tok, (size_t)M * R * 4));
+    CK(cudaMallocHost(&c.h_tgt, (size_t)M * R * 4));
+    CK(cudaMallocHost(&c.h_csr, (size_t)M * c.csr_stride * 4));
+    c.csr_U.assign(M, 0);
+    int lo_prio = 0, hi_prio = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    const size_t act = R * c.d.H * c.act_bytes;
+    for (int n = 0; n < P; ++n) {
+      if (c.node_rank[n] != c.o.world_rank) continue;
+      Node &nd = c.nodes[n];
+      nd.n = n;
+      CK(cudaStreamCreateWithPriority(&nd.main, cudaStreamNonBlocking, hi_prio));
+      CK(cudaStreamCreateWithPriority(&nd.frc, cudaStreamNonBlocking, lo_prio));
+      CK(cudaEventCreate(&nd.t0));
+      CK(cudaEventCreate(&nd.t1));
+      std::vector<std::pair<int, bool>> hosted{{n, false}};
+      if (rc) hosted.push_back({(n + 1) % P, true});
+      for (auto &h : hosted) {
+        const int X = h.first;
+        const StageInfo &si = c.stages[X];
+        Copy &cp = nd.copies[X];
+        cp.X = X;
+        cp.replica = h.second;
+        cp.master = (float *)dmalloc(si.pcount * 4);
+        cp.m = (float *)dmalloc(si.pcount * 4);
+        cp.v = (float *)dmalloc(si.pcount * 4);
+        cp.grad = (float *)dmalloc(si.pcount * 4);
+        cp.work = c.bf16 ? dmalloc(si.pcount * 2) : (void *)cp.master;
+        cp.nslots = h.second ? M : std::min(M, P - X);
+        cp.slots = (char *)dmalloc(si.slot_bytes * cp.nslots);
+        if (X == P - 1) cp.loss = (float *)dmalloc(M * 4);
+      }
+      nd.arena_bytes = 12 * (size_t)M * al(act) + ALIGN;
+      nd.arena = (char *)dmalloc(nd.arena_bytes);
+      const size_t F = c.d.F, H = c.d.H;
+      nd.sF = dmalloc(R * F * c.act_bytes);
+      nd.s3 = dmalloc(R * 3 * H * c.act_bytes);
+      for (auto &p : nd.sH) p = dmalloc(R * H * c.act_bytes);
+      nd.s_part = (float *)dmalloc(
+          k::colreduce_partial_floats((int)R, (int)std::max(F, 3 * H)) * 4);
+      nd.s_attn = (float *)dmalloc((size_t)c.d.mb * c.d.nh * c.d.S * 4);
+      nd.s_loss_main = (float *)dmalloc(R * 4);
+      nd.s_loss_frc = (float *)dmalloc(R * 4);
+      nd.d_tok = (int32_t *)dmalloc((size_t)M * R * 4);
+      nd.d_tgt = (int32_t *)dmalloc((size_t)M * R * 4);
+      nd.d_csr = (int32_t *)dmalloc((size_t)M * c.csr_stride * 4);
+    }
+    // NCCL edges: one 2-rank communicator per (src node, dst node, kind) whose
+    // endpoints live on different ranks; ring distance <= 2 covers the normal
+    // pipeline, the replica ring and the failover skip edges.
+    if (c.o.world_size > 1) {
+      if (!c.o.nccl_id) throw RtError{BB_E_INVAL, "nccl_id required for world_size > 1"};
+      ncclUniqueId id;
+      std::memcpy(&id, c.o.nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&c.world, c.o.world_size, id, c.o.world_rank));
+      std::set<std::tuple<int, int, int>> want;
+      auto add = [&](int a, int b, int kind) {
+        a = (a % P + P) % P;
+        b = (b % P + P) % P;
+        if (a != b && c.node_rank[a] != c.node_rank[b]) want.insert({a, b, kind});
+      };
+      for (int a = 0; a < P; ++a) {
+        if (a < P - 1) add(a, a + 1, MSG_ACT);
+        add(a, a + 2, MSG_ACT);
+        if (a > 0) add(a, a - 1, MSG_GRAD);
+        add(a, a - 2, MSG_GRAD);
+        add(a, a - 1, MSG_GRADSUM);
+      }
+      std::vector<std::tuple<int, int, int>> todo(want.begin(), want.end());
+      int color_base = 0;
+      while (!todo.empty()) {
+        // one round = a matching over ranks
+        std::set<int> busy;
+        std::vector<std::tuple<int, int, int>> round, rest;
+        for (auto &e : todo) {
+          const int ra = c.node_rank[std::get<0>(e)], rb = c.node_rank[std::get<1>(e)];
+          if (busy.count(ra) || busy.count(rb)) {
+            rest.push_back(e);
+            continue;
+          }
+          busy.insert(ra);
+          busy.insert(rb);
+          round.push_back(e);
+        }
+        int color = NCCL_SPLIT_NOCOLOR, key = 0;
+        const std::tuple<int, int, int> *mine = nullptr;
+        for (size_t i = 0; i < round.size(); ++i) {
+          const int ra = c.node_rank[std::get<0>(round[i])], rb = c.node_rank[std::get<1>(round[i])];
+          if (ra == c.o.world_rank || rb == c.o.world_rank) {
+            color = color_base + (int)i;
+            key = ra == c.o.world_rank ? 0 : 1;
+            mine = &round[i];
+          }
+        }
+        ncclComm_t nc = nullptr;
+        NK(ncclCommSplit(c.world, color, key, &nc, nullptr));
+        if (mine) {
+          EdgeComm ed;
+          ed.src = std::get<0>(*mine);
+          ed.dst = std::get<1>(*mine);
+          ed.kind = std::get<2>(*mine);
+          ed.comm = nc;
+          CK(cudaStreamCreateWithPriority(&ed.stream, cudaStreamNonBlocking, hi_prio));
+          c.edges[*mine] = ed;
+        }
+        color_base += (int)round.size();
+        todo = rest;
+      }
+    }
+    CK(cudaDeviceSynchronize());
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+bb_status rt_load_params(Ctx &c, const float *host, size_t n) {
+  try {
+    if (n != c.total_params) throw RtError{BB_E_INVAL, "parameter count mismatch"};
+    for (auto &kv : c.nodes) {
+      Node &nd = kv.second;
+      for (auto &cc : nd.copies) {
+        Copy &cp = cc.second;
+        const StageInfo &si = c.stages[cp.X];
+        CK(cudaMemcpy(cp.master, host + si.poff, si.pcount * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(cp.m, 0, si.pcount * 4));
+        CK(cudaMemset(cp.v, 0, si.pcount * 4));
+        if (c.bf16) CK(k::cast_f32_to_bf16(si.pcount, cp.master, cp.work, nd.main));
+        cp.t = 0;
+      }
+    }
+    CK(cudaDeviceSynchronize());
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats *st) {
+  const double t0 = now_ms();
+  try {
+    if (c.fatal) return BB_E_FATAL;
+    if (c.interrupted) throw RtError{BB_E_STATE, "bb_recover pending"};
+    if (!tok || !tgt) throw RtError{BB_E_INVAL, "null tokens/targets"};
+    CK(cudaSetDevice(c.o.device));
+    begin_step(c);
+    stage_inputs(c, tok, tgt);
+    if (!c.armed) {
+      run(c, c.plans, nullptr, Phase{});
+      sync_all(c, true);
+      if (st) st->loss = read_loss(c);
+      finish_stats(c, st, t0);
+      return BB_OK;
+    }
+    // injected preemption: every rank computes the same cut (Q12/Q14)
+    c.armed = false;
+    const int v = c.inj_v;
+    try {
+      c.cut = cut(c.plans, v, c.inj_pi);
+    } catch (const PlanError &e) {
+      throw RtError{BB_E_INVAL, e.msg};
+    }
+    // messages the victim consumed before dying, per channel
+    c.victim_consumed.clear();
+    c.sent_to_victim.clear();
+    {
+      std::map<int, int> pcs;
+      Channels ch;
+      std::map<int, int> cap{{v, c.inj_pi}};
+      lockstep(c.plans, pcs, ch, cap, [&](int n, const Instr &ins) {
+        if (n == v && is_recv(ins.kind))
+          ++c.victim_consumed[ChanKey{ins.peer, v, (int)message_of(ins).kind}];
+      });
+    }
+    Phase ph;
+    ph.drop_to_victim = true;
+    ph.victim = v;
+    run(c, c.plans, &c.cut.pcs, ph);
+    sync_all(c, false);   // pending sends wait for the continuation's receives
+    c.interrupted = true;
+    if (st) {
+      st->loss = NAN;
+      finish_stats(c, st, t0);
+    }
+    return BB_E_PREEMPTED;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+bb_status rt_preempt(Ctx &c, int stage, int at_instr) {
+  if (c.fatal) return BB_E_FATAL;
+  if (c.interrupted) {
+    c.err = "recovery pending";
+    return BB_E_STATE;
+  }
+  if (stage < 0 || stage >= c.d.P) {
+    c.err = "unknown stage";
+    return BB_E_INVAL;
+  }
+  if (c.o.rc == BB_RC_NONE || c.failover) {
+    // no replica of the victim exists (no RC, or redundancy already spent: P:464, Q18)
+    c.err = "no redundancy left for the victim";
+    return BB_E_FATAL;
+  }
+  if (at_instr < 0 || at_instr > (int)c.plans.at(stage).size()) {
+    c.err = "injection point beyond the victim's list";
+    return BB_E_INVAL;
+  }
+  c.armed = true;
+  c.inj_v = stage;
+  c.inj_pi = at_instr;
+  return BB_OK;
+}
+
+bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
+  const double t0 = now_ms();
+  try {
+    if (!c.interrupted) throw RtError{BB_E_STATE, "no interrupted step"};
+    const int P = c.d.P, M = c.d.M, v = c.inj_v, u = (v - 1 + P) % P;
+    try {
+      c.continuation = recovery_plans(c.plans, P, M, v, c.cut.pcs, c.cut.ch, &c.rinfo);
+    } catch (const PlanError &e) {
+      throw RtError{BB_E_STATE, e.msg};
+    }
+    {
+      std::ostringstream o;
+      o << "# bamboo-recovery v1 P=" << P << " M=" << M << " victim=" << v << " shadow=" << u
+        << " successor=" << c.rinfo.successor << " commit=" << (c.rinfo.commit ? 1 : 0) << '\n';
+      o << "# cut";
+      for (auto &kv : c.cut.pcs) o << ' ' << kv.first << ':' << kv.second;
+      o << '\n' << dump_lines(c.continuation);
+      c.recovery_text = o.str();
+    }
+    // promote the replica on the shadow; the victim stops
+    if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = false;
+    Phase ph;
+    run(c, c.continuation, nullptr, ph);
+    sync_all(c, true);
+    if (c.nodes.count(v)) {
+      // the victim's memory is gone: NaN-poison everything it held
+      Node &nd = c.nodes.at(v);
+      for (auto &cc : nd.copies) {
+        Copy &cp = cc.second;
+        const size_t n = c.stages[cp.X].pcount;
+        CK(k::fill_nan(cp.master, n * 4, nd.main));
+        CK(k::fill_nan(cp.m, n * 4, nd.main));
+        CK(k::fill_nan(cp.v, n * 4, nd.main));
+        CK(k::fill_nan(cp.grad, n * 4, nd.main));
+        if (c.bf16) CK(k::fill_nan(cp.work, n * 2, nd.main));
+        CK(k::fill_nan(cp.slots, c.stages[cp.X].slot_bytes * cp.nslots, nd.main));
+      }
+      CK(k::fill_nan(nd.arena, nd.arena_bytes, nd.main));
+      CK(cudaStreamSynchronize(nd.main));
+      nd.alive = false;
+    }
+    c.topo = failover_topology(P, v);
+    try {
+      c.plans = failover_plans(P, M, v);
+    } catch (const PlanError &e) {
+      throw RtError{BB_E_STATE, e.msg};
+    }
+    c.failover = true;
+    c.victim = v;
+    c.interrupted = false;
+    if (r) {
+      r->victim = v;
+      r->shadow = u;
+      r->successor = c.rinfo.successor;
+      r->commit = c.rinfo.commit ? 1 : 0;
+      r->brc_mb = (int)c.rinfo.brc_mb.size();
+      r->frc_done_mb = (int)c.rinfo.frc_done.size();
+      r->resent_mb = (int)c.rinfo.resend.size();
+      r->loss = read_loss(c);
+      r->recover_ms = (float)(now_ms() - t0);
+    }
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    c.fatal = e.st != BB_E_INVAL;
+    return e.st;
+  }
+}
+
+bb_status rt_read_state(Ctx &c, int X, int replica, int what, float *host, size_t n) {
+  try {
+    if (X < 0 || X >= c.d.P) throw RtError{BB_E_INVAL, "bad stage"};
+    const int node = replica ? c.topo.replica_on[X] : c.topo.host[X];
+    if (node < 0 || !c.nodes.count(node) || !c.nodes.at(node).alive)
+      throw RtError{BB_E_INVAL, "copy not hosted by this process"};
+    Copy &cp = c.nodes.at(node).copies.at(X);
+    if (n != c.stages[X].pcount) throw RtError{BB_E_INVAL, "size mismatch"};
+    const float *src = what == BB_STATE_PARAMS ? cp.master
+                       : what == BB_STATE_GRADS ? cp.grad
+                       : what == BB_STATE_ADAM_M ? cp.m
+                       : what == BB_STATE_ADAM_V ? cp.v : nullptr;
+    if (!src) throw RtError{BB_E_INVAL, "bad state kind"};
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(host, src, n * 4, cudaMemcpyDeviceToHost));
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+std::string rt_dump(const Ctx &c) {
+  return dump(c.d.P, c.d.M, c.o.rc != BB_RC_NONE, c.ranges, c.plans, c.topo, c.node_device,
+              c.failover, c.victim);
+}
+
+bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n) {
+  try {
+    std::vector<bb_kernel_stat> acc(PC_N);
+    for (int i = 0; i < PC_N; ++i) {
+      std::memset(&acc[i], 0, sizeof(bb_kernel_stat));
+      std::strncpy(acc[i].name, prof_names[i], sizeof(acc[i].name) - 1);
+    }
+    for (auto &r : c.prof) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(r.b));
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      acc[r.cls].launches += 1;
+      acc[r.cls].ms += ms;
+      acc[r.cls].work += r.work;
+    }
+    if (n) *n = PC_N;
+    for (int i = 0; i < PC_N && i < cap; ++i) out[i] = acc[i];
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+void rt_destroy(Ctx &c) {
+  cudaDeviceSynchronize();
+  for (auto &kv : c.edges)
+    if (kv.second.comm) ncclCommDestroy(kv.second.comm);
+  if (c.world) ncclCommDestroy(c.world);
+  for (auto &kv : c.nodes) {
+    Node &nd = kv.second;
+    for (auto &cc : nd.copies) {
+      Copy &cp = cc.second;
+      cudaFree(cp.master);
+      cudaFree(cp.m);
+      cudaFree(cp.v);
+      cudaFree(cp.grad);
+      if (c.bf16) cudaFree(cp.work);
+      cudaFree(cp.slots);
+      if (cp.loss) cudaFree(cp.loss);
+    }
+    cudaFree(nd.arena);
+    cudaFree(nd.sF);
+    cudaFree(nd.s3);
+    for (auto p : nd.sH) cudaFree(p);
+    cudaFree(nd.s_part);
+    cudaFree(nd.s_attn);
+    cudaFree(nd.s_loss_main);
+    cudaFree(nd.s_loss_frc);
+    cudaFree(nd.d_tok);
+    cudaFree(nd.d_tgt);
+    cudaFree(nd.d_csr);
+    for (auto e : nd.evpool) cudaEventDestroy(e);
+    cudaEventDestroy(nd.t0);
+    cudaEventDestroy(nd.t1);
+    cudaStreamDestroy(nd.main);
+    cudaStreamDestroy(nd.frc);
+  }
+  for (auto e : c.prof_pool) cudaEventDestroy(e);
+  if (c.h_tok) cudaFreeHost(c.h_tok);
+  if (c.h_tgt) cudaFreeHost(c.h_tgt);
+  if (c.h_csr) cudaFreeHost(c.h_csr);
+}
+
+}  // namespace bb

@@ -1,0 +1,159 @@
+// runtime.h — per-process execution of the pipeline plans on one B200.
+//
+// One process per GPU hosts one or more pipeline NODES (node n runs stage n
+// until a failover moves a stage to its shadow). Each node owns a high-
+// priority main stream and a low-priority FRC stream (FRC fills the 1F1B
+// bubbles and overlaps the next forward), its parameter copies
+// (own stage + the successor's replica with Adam state), saved-set
+// slot pools (1F1B stash; full FRC retention, P:524 / Q10), a per-step arena
+// for activations and input-gradients (retained for a lazy-BRC resend, Q3) and
+// a backward scratch. Nodes on other ranks are reached over NCCL P2P edges.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "bamboo.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace bb {
+
+struct Dims {
+  int L, H, nh, F, V, S, causal;
+  int P, M, mb;
+  int R() const { return mb * S; }
+  int d() const { return H / nh; }
+};
+
+// Parameter tensors of one unit, offsets relative to the stage's flat slice.
+struct UnitP {
+  int unit, kind;   // kind 0 embedding, 1 block, 2 head
+  size_t tok, pos;
+  size_t ln1g, ln1b, wqkv, bqkv, wo, bo, ln2g, ln2b, w1, b1, w2, b2;
+  size_t lnfg, lnfb, whead;
+};
+// Saved-set tensors of one unit inside a slot (byte offsets).
+struct UnitS {
+  size_t out;                                                    // unit output (not last unit)
+  size_t h1, mean1, rstd1, qkv, o, lse, x1, h2, mean2, rstd2, pre, act;   // block
+  size_t hf, meanf, rstdf, dlog;                                 // head
+};
+struct StageInfo {
+  int X, ua, ub;
+  size_t poff, pcount;
+  std::vector<UnitP> up;
+  std::vector<UnitS> us;
+  size_t slot_bytes;
+};
+
+struct Entry {
+  void *p = nullptr;
+  cudaEvent_t ev = nullptr;
+  int slot = -1;
+};
+
+struct Copy {
+  int X = -1;
+  bool replica = false;   // kept for the predecessor's successor (false once promoted)
+  float *master = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
+  void *work = nullptr;   // bf16 working copy (== master in fp32 check mode)
+  int t = 0;
+  char *slots = nullptr;
+  int nslots = 0;
+  std::vector<int> free_slots;
+  float *loss = nullptr;  // [M] per-micro-batch losses (stage P-1 only)
+};
+
+struct Node {
+  int n = -1;
+  bool alive = true;
+  cudaStream_t main = nullptr, frc = nullptr;
+  std::map<int, Copy> copies;
+  std::map<Key, Entry> store;
+  char *arena = nullptr;
+  size_t arena_bytes = 0, arena_used = 0;
+  // backward scratch (main stream)
+  void *sF = nullptr, *s3 = nullptr, *sH[5] = {};
+  float *s_part = nullptr, *s_attn = nullptr, *s_loss_main = nullptr, *s_loss_frc = nullptr;
+  int32_t *d_tok = nullptr, *d_tgt = nullptr, *d_csr = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  std::vector<Instr> plan;
+  size_t pc = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+struct EdgeComm {
+  int src = -1, dst = -1, kind = -1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double work;
+};
+
+struct Ctx {
+  Dims d{};
+  bb_opts o{};
+  bool bf16 = true;
+  size_t act_bytes = 2;   // sizeof(storage type)
+  std::vector<std::pair<int, int>> ranges;
+  std::vector<StageInfo> stages;
+  size_t total_params = 0;
+  Plans plans;
+  Topology topo;
+  bool failover = false;
+  int victim = -1;
+  bool fatal = false;
+  std::vector<int> node_rank, node_device;
+  std::map<int, Node> nodes;          // local nodes only
+  std::map<std::tuple<int, int, int>, EdgeComm> edges;
+  ncclComm_t world = nullptr;
+  // local mailboxes (per (src node, dst node, kind))
+  std::map<ChanKey, std::deque<Entry>> mail;
+  // injection / recovery state
+  bool armed = false;
+  int inj_v = -1, inj_pi = -1;
+  bool interrupted = false;
+  Cut cut;
+  std::map<ChanKey, int> victim_consumed, sent_to_victim;
+  Plans continuation;
+  RecoveryInfo rinfo;
+  std::string recovery_text;
+  // host staging
+  int32_t *h_tok = nullptr, *h_tgt = nullptr, *h_csr = nullptr;
+  std::vector<int> csr_U;
+  size_t csr_stride = 0;
+  double bc_t = 0;
+  std::string err;
+  // profiling
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_next = 0;
+  long long launches_at_start = 0;
+  uint64_t h2d = 0, d2h = 0;
+};
+
+// Implemented in runtime.cpp
+bb_status rt_init(Ctx &c, const bb_model *m, int stages, int microbatches, const bb_opts *o);
+bb_status rt_load_params(Ctx &c, const float *host, size_t n);
+bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats *st);
+bb_status rt_preempt(Ctx &c, int stage, int at_instr);
+bb_status rt_recover(Ctx &c, bb_recovery_stats *r);
+bb_status rt_read_state(Ctx &c, int stage, int replica, int what, float *host, size_t n);
+std::string rt_dump(const Ctx &c);
+void rt_destroy(Ctx &c);
+bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n);
+
+// Shared helpers
+std::vector<std::pair<size_t, size_t>> unit_param_ranges(const Dims &d);  // per unit [off, n)
+size_t unit_param_count(const Dims &d, int unit);
+
+}  // namespace bb

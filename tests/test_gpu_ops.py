@@ -1,0 +1,175 @@
+"""Per-kernel GPU parity through the C ABI's single-op entry points, against
+the oracle's fp64 ops on the same (bf16-representable) inputs. Shapes span
+several tiles plus ragged tails, every operand layout and epilogue."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as om
+from synth import round_to_bf16
+
+pytestmark = pytest.mark.gpu
+
+rng = np.random.default_rng(5)
+
+
+def dev(x, prec):
+    t = torch.tensor(np.asarray(x, np.float32), device="cuda")
+    return t.to(torch.bfloat16) if prec == "bf16" else t
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def rnd(*shape, scale=1.0):
+    return round_to_bf16((rng.standard_normal(shape) * scale).astype(np.float32)).astype(np.float64)
+
+
+GEMM_SHAPES = [(64, 64, 64), (200, 136, 72), (256, 512, 128), (1000, 328, 520), (128, 2304, 768),
+               (130, 50304 // 64, 64), (8, 24, 16), (384, 640, 1000)]
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("layout", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_gemm_layouts(prec, impl, layout, shape):
+    import paper_2204_12013_b200 as bb
+    M, N, K = shape
+    a_mn, b_mn = layout
+    A = rnd(M, K)
+    B = rnd(N, K)
+    ref = om.linear_fwd(A, B)                      # D = A B^T
+    dA = dev(A.T.copy() if a_mn else A, prec)
+    dB = dev(B.T.copy() if b_mn else B, prec)
+    C = torch.zeros((M, N), device="cuda", dtype=torch.float32)
+    bb.op_gemm(prec, impl, M, N, K, dA.data_ptr(), M if a_mn else K, a_mn, dB.data_ptr(),
+               N if b_mn else K, b_mn, 5, C.data_ptr(), N)
+    torch.cuda.synchronize()
+    got = host(C)
+    tol = 1e-5 if prec == "fp32" else 2e-5   # fp32 accumulate of exact bf16 products
+    assert np.abs(got - ref).max() <= tol * np.abs(ref).max() * max(1, K / 256)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
+def test_gemm_epilogues(prec, epi):
+    import paper_2204_12013_b200 as bb
+    M, N, K = 300, 200, 136
+    A, B = rnd(M, K), rnd(N, K)
+    bias, res, aux = rnd(N), rnd(M, N), rnd(M, N)
+    D = om.linear_fwd(A, B)
+    want_aux = None
+    if epi == 0:
+        want = D
+    elif epi == 1:
+        want = D + bias
+    elif epi == 2:
+        want = D + bias + res
+    elif epi == 3:
+        want_aux = D + bias
+        want = om.gelu_fwd(want_aux)
+    else:
+        want = om.gelu_bwd(D, aux)
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    C = torch.zeros((M, N), device="cuda", dtype=dt)
+    dAux = dev(aux, prec) if epi == 4 else torch.zeros((M, N), device="cuda", dtype=dt)
+    dbias, dres = dev(bias, prec), dev(res, prec)
+    for impl in (0, 1):
+        bb.op_gemm(prec, impl, M, N, K, dev(A, prec).data_ptr(), K, 0, dev(B, prec).data_ptr(), K,
+                   0, epi, C.data_ptr(), N, dbias.data_ptr(), dres.data_ptr(), dAux.data_ptr())
+        torch.cuda.synchronize()
+        tol = 1e-5 if prec == "fp32" else 1e-2
+        assert np.abs(host(C) - want).max() <= tol * np.abs(want).max()
+        if want_aux is not None:
+            assert np.abs(host(dAux) - want_aux).max() <= tol * np.abs(want_aux).max()
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("B,S,nh,d", [(2, 32, 2, 32), (1, 200, 3, 64), (2, 128, 2, 64)])
+def test_attention(prec, causal, B, S, nh, d):
+    import paper_2204_12013_b200 as bb
+    H = nh * d
+    qkv = rnd(B * S, 3 * H)
+    o_ref, p = om.attention_fwd(qkv, B, S, nh, causal)
+    do = rnd(B * S, H)
+    dq_ref = om.attention_bwd(do, qkv, p, B, S, nh)
+    dqkv_ = dev(qkv, prec)
+    o = torch.zeros((B * S, H), device="cuda", dtype=dqkv_.dtype)
+    lse = torch.zeros((B, nh, S), device="cuda", dtype=torch.float32)
+    bb.op_attention_fwd(prec, B, S, H, nh, causal, dqkv_.data_ptr(), o.data_ptr(), lse.data_ptr())
+    dqkv = torch.zeros_like(dqkv_)
+    bb.op_attention_bwd(prec, B, S, H, nh, causal, dqkv_.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                        dev(do, prec).data_ptr(), dqkv.data_ptr())
+    torch.cuda.synchronize()
+    tol = 1e-5 if prec == "fp32" else 1e-2
+    assert np.abs(host(o) - o_ref).max() <= tol * np.abs(o_ref).max()
+    assert np.abs(host(dqkv) - dq_ref).max() <= tol * np.abs(dq_ref).max() * 2
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("R,H", [(64, 64), (100, 768), (33, 1600)])
+def test_layernorm(prec, R, H):
+    import paper_2204_12013_b200 as bb
+    x, g, b, dy, dres = rnd(R, H), rnd(H), rnd(H), rnd(R, H), rnd(R, H)
+    y_ref, sv = om.layernorm_fwd(x, g, b)
+    dx_ref, dg_ref, db_ref = om.layernorm_bwd(dy, g, sv)
+    dx_ref = dx_ref + dres
+    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    y = torch.zeros((R, H), device="cuda", dtype=dt)
+    mean = torch.zeros(R, device="cuda")
+    rstd = torch.zeros(R, device="cuda")
+    dx = torch.zeros((R, H), device="cuda", dtype=dt)
+    dg = torch.zeros(H, device="cuda")
+    db = torch.zeros(H, device="cuda")
+    dX, dG = dev(x, prec), dev(g, prec)
+    bb.op_layernorm_fwd(prec, R, H, dX.data_ptr(), dG.data_ptr(), dev(b, prec).data_ptr(),
+                        y.data_ptr(), mean.data_ptr(), rstd.data_ptr())
+    bb.op_layernorm_bwd(prec, R, H, dev(dy, prec).data_ptr(), dX.data_ptr(), mean.data_ptr(),
+                        rstd.data_ptr(), dG.data_ptr(), dev(dres, prec).data_ptr(), dx.data_ptr(),
+                        dg.data_ptr(), db.data_ptr())
+    torch.cuda.synchronize()
+    tol = 1e-5 if prec == "fp32" else 1e-2
+    for got, want in ((y, y_ref), (dx, dx_ref), (dg, dg_ref), (db, db_ref)):
+        assert np.abs(host(got) - want).max() <= tol * np.abs(want).max()
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("R,V", [(16, 128), (7, 50304), (33, 30528)])
+def test_cross_entropy(prec, R, V):
+    import paper_2204_12013_b200 as bb
+    logits = rnd(R, V, scale=2.0)
+    tg = rng.integers(0, V, R).astype(np.int32)
+    n_tok = 4 * R
+    loss_ref, probs = om.ce_fwd(logits, tg, n_tok)
+    d_ref = om.ce_bwd(probs, tg, n_tok)
+    L = dev(logits, prec)
+    rows = torch.zeros(R, device="cuda")
+    bb.op_cross_entropy(prec, R, V, L.data_ptr(), torch.tensor(tg, device="cuda").data_ptr(),
+                        n_tok, rows.data_ptr())
+    torch.cuda.synchronize()
+    tol = 1e-5 if prec == "fp32" else 1e-2
+    assert abs(host(rows).sum() - loss_ref) <= tol * abs(loss_ref)
+    assert np.abs(host(L) - d_ref).max() <= tol * np.abs(d_ref).max()
+
+
+def test_adam_matches_oracle():
+    import paper_2204_12013_b200 as bb
+    n = 10007
+    p, m, v = rnd(n), np.zeros(n), np.zeros(n)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    dp = torch.tensor(p, device="cuda", dtype=torch.float32)
+    dm = torch.zeros(n, device="cuda")
+    dv = torch.zeros(n, device="cuda")
+    w16 = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
+    for t in range(1, 4):
+        g = rnd(n)
+        p, m, v = om.adam_update(p, g, m, v, t, lr, b1, b2, eps)
+        bb.op_adam(n, dp.data_ptr(), torch.tensor(g, device="cuda", dtype=torch.float32).data_ptr(),
+                   dm.data_ptr(), dv.data_ptr(), w16.data_ptr(), t, lr, b1, b2, eps)
+    torch.cuda.synchronize()
+    assert np.abs(host(dp) - p).max() <= 1e-6
+    assert np.abs(host(dm) - m).max() <= 1e-6 * np.abs(m).max()
+    assert np.array_equal(w16.cpu(), dp.cpu().to(torch.bfloat16))

@@ -1,0 +1,173 @@
+"""GPU parity of the full hot path through the C ABI (run under gpurun).
+
+C0 = BASELINE configs[0] (4 layers, H=64, 2 heads, S=32, P=2, M=4, mb=2) runs
+with both stages on cuda:0 (stages > GPUs share one device). Checked against
+the fp64 oracle on the same seeded inputs: plan dump byte-equal, loss,
+per-tensor gradients and post-Adam state within DESIGN.md's tolerances, FRC
+replica == primary bit for bit, and preempted + recovered == failure-free bit
+for bit (north star) plus within tolerance of the oracle.
+"""
+import numpy as np
+import pytest
+
+from oracle import model as omodel, pipeline as opipe, plan as opl
+from synth import get_config, make_params, make_tokens, depth_reduced
+from parity import TOL, check_tensors, check_params, normwise
+
+pytestmark = pytest.mark.gpu
+
+LR = 1e-4
+
+
+def _gpu(cfg, flat, prec, rc=True, **kw):
+    import paper_2204_12013_b200 as bb
+    p = bb.Pipeline(cfg.model, cfg.stages, cfg.microbatches, micro_batch=cfg.micro_batch, rc=rc,
+                    prec=prec, lr=LR, **kw)
+    p.load_params(flat)
+    return p
+
+
+def _flat_state(p, P, what):
+    return np.concatenate([p.read_state(s, what) for s in range(P)])
+
+
+def _compare_step(cfg, p, ref, prec, loss, ref_loss, steps):
+    tol = TOL[prec]
+    lay = ref.lay
+    assert abs(loss - ref_loss) <= tol * abs(ref_loss), (loss, ref_loss)
+    g = _flat_state(p, cfg.stages, "grads")
+    rg = ref.full_grads()
+    check_tensors(lay, 0, lay.total, g, rg, tol, "grad")
+    m, v = _flat_state(p, cfg.stages, "adam_m"), _flat_state(p, cfg.stages, "adam_v")
+    rm, rv = ref.full_adam()
+    check_tensors(lay, 0, lay.total, m, rm, tol, "adam_m")
+    check_tensors(lay, 0, lay.total, v, rv, 2 * tol, "adam_v")
+    check_params(lay, 0, lay.total, _flat_state(p, cfg.stages, "params"), ref.full_params(), rg,
+                 tol, LR, steps)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("rc", [True, False])
+def test_c0_steps_match_oracle(prec, rc):
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    p = _gpu(cfg, flat, prec, rc)
+    ref = opipe.Pipeline(cfg, flat, rc=rc, lr=LR)
+    want = opl.dump(cfg.stages, cfg.microbatches, rc, opl.partition(cfg.model.n_layer, cfg.stages),
+                    opl.normal_plans(cfg.stages, cfg.microbatches, rc))
+    assert p.schedule_dump() == want
+    for t in range(2):
+        tok, tgt = make_tokens(cfg, t)
+        status, st = p.step(tok, tgt)
+        assert status == "ok"
+        _, ref_loss = ref.step(tok, tgt)
+        _compare_step(cfg, p, ref, prec, st.loss, ref_loss, t + 1)
+        assert st.gpu_launches > 0
+    if rc:   # replica == primary, bit for bit
+        for s in range(cfg.stages):
+            for what in ("params", "adam_m", "adam_v", "grads"):
+                assert np.array_equal(p.read_state(s, what), p.read_state(s, what, replica=True))
+    p.close()
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_bidirectional_and_three_stages(prec):
+    import dataclasses
+    c0 = get_config("C0")
+    cfg = dataclasses.replace(c0, model=dataclasses.replace(c0.model, causal=False, n_layer=5),
+                              stages=3, microbatches=5, gpt=False)
+    flat = make_params(cfg.model)
+    p = _gpu(cfg, flat, prec)
+    ref = opipe.Pipeline(cfg, flat, rc=True, lr=LR)
+    tok, tgt = make_tokens(cfg, 0)
+    _, st = p.step(tok, tgt)
+    _, ref_loss = ref.step(tok, tgt)
+    _compare_step(cfg, p, ref, prec, st.loss, ref_loss, 1)
+    p.close()
+
+
+def _run(cfg, flat, prec, steps, inject=None):
+    p = _gpu(cfg, flat, prec)
+    out = []
+    rec = None
+    for t in range(steps):
+        tok, tgt = make_tokens(cfg, t)
+        if inject is not None and inject[0] == t:
+            p.preempt(inject[1], inject[2])
+        status, st = p.step(tok, tgt)
+        loss = st.loss
+        if status == "preempted":
+            rec = p.recover()
+            loss = rec.loss
+        out.append((loss, {w: _flat_state(p, cfg.stages, w)
+                           for w in ("params", "grads", "adam_m", "adam_v")}))
+    return p, out, rec
+
+
+@pytest.mark.parametrize("prec", ["bf16"])
+def test_c0_preemption_recovery_bitwise(prec):
+    """BASELINE configs[0]: 'one injected preemption of stage 1' — and every
+    other (victim, point) of C0: the recovered run equals the failure-free run
+    bit for bit, and the continuation plan equals the oracle's."""
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    _, ref, _ = _run(cfg, flat, prec, 2)
+    plans = opl.normal_plans(cfg.stages, cfg.microbatches, True)
+    for v in range(cfg.stages):
+        for pi in range(0, len(plans[v]) + 1):
+            p, got, rec = _run(cfg, flat, prec, 2, inject=(0, v, pi))
+            assert rec.victim == v and rec.shadow == (v - 1) % cfg.stages
+            assert p.recovery_dump() == opl.recovery_dump(cfg.stages, cfg.microbatches, v, pi)
+            for (la, sa), (lb, sb) in zip(got, ref):
+                assert la == lb, (v, pi)
+                for w in sa:
+                    assert np.array_equal(sa[w], sb[w]), (v, pi, w)
+            host, rep = opl.failover_topology(cfg.stages, v)
+            want = opl.dump(cfg.stages, cfg.microbatches, True, opl.partition(4, 2),
+                            opl.failover_plans(cfg.stages, cfg.microbatches, v), host, rep,
+                            mode="failover", victim=v)
+            assert p.schedule_dump() == want
+            p.close()
+
+
+def test_recovered_run_matches_oracle():
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    p, got, rec = _run(cfg, flat, "fp32", 2, inject=(0, 1, 9))
+    ref = opipe.Pipeline(cfg, flat, rc=True, lr=LR)
+    losses = []
+    for t in range(2):
+        tok, tgt = make_tokens(cfg, t)
+        if t == 0:
+            ref.preempt(1, 9)
+            ref.step(tok, tgt)
+            l, _ = ref.recover()
+        else:
+            _, l = ref.step(tok, tgt)
+        losses.append(l)
+    _compare_step(cfg, p, ref, "fp32", got[-1][0], losses[-1], 2)
+
+
+def test_fatal_second_preemption():
+    import paper_2204_12013_b200 as bb
+    cfg = get_config("C0")
+    p, _, _ = _run(cfg, make_params(cfg.model), "bf16", 1, inject=(0, 1, 3))
+    with pytest.raises(bb.BambooError) as e:
+        p.preempt(0, 0)
+    assert e.value.status == -6   # BB_E_FATAL
+    p.close()
+
+
+def test_depth_reduced_c1_width_parity():
+    """PT2 tier: C1 width (H=768, 12 heads, V=50304, S=1024), 1 block/stage."""
+    cfg = depth_reduced("C1", 1, 2, 1)
+    flat = make_params(cfg.model)
+    p = _gpu(cfg, flat, "bf16")
+    ref = opipe.Pipeline(cfg, flat, rc=True, lr=LR)
+    tok, tgt = make_tokens(cfg, 0)
+    _, st = p.step(tok, tgt)
+    _, ref_loss = ref.step(tok, tgt)
+    assert abs(st.loss - ref_loss) <= 1e-2 * abs(ref_loss)
+    g = _flat_state(p, cfg.stages, "grads")
+    check_tensors(ref.lay, 0, ref.lay.total, g, ref.full_grads(), 1e-2, "grad")
+    p.close()

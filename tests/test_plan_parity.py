@@ -1,0 +1,78 @@
+"""Host-side parity (no GPU): the C++ controller in libbamboo.so must emit
+byte-identical plan / failover / recovery dumps to the oracle (SURVEY.md §8(b)
+"schedule and stage assignment bit-exact"), and the library must export every
+entry point declared in include/bamboo.h."""
+import os
+import random
+import re
+
+import pytest
+
+from oracle import plan as pl
+from synth import get_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+bbl = pytest.importorskip("paper_2204_12013_b200._lib")
+
+
+def _lib_or_skip():
+    if not os.path.exists(bbl.LIB_PATH):
+        pytest.skip("libbamboo.so not built")
+    return bbl.lib()
+
+
+def test_exports_every_header_symbol():
+    lib = _lib_or_skip()
+    hdr = open(os.path.join(ROOT, "include", "bamboo.h")).read()
+    names = sorted(set(re.findall(r"^(?:bb_status|void)\s+\*?(bb_[a-z0-9_]+)\s*\(", hdr, re.M)))
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(bbl.EXPORTED) <= set(names)
+
+
+def _oracle_normal(cfg, P, M, rc, world_size=1):
+    per = -(-P // world_size)
+    dev = {n: min(n // per, world_size - 1) for n in range(P)}
+    return pl.dump(P, M, rc, pl.partition(cfg.model.n_layer, P), pl.normal_plans(P, M, rc),
+                   device=dev)
+
+
+@pytest.mark.parametrize("name", ["C0", "C1", "C2", "C3"])
+@pytest.mark.parametrize("rc", [True, False])
+def test_normal_plan_dump_matches_oracle(name, rc):
+    _lib_or_skip()
+    cfg = get_config(name)
+    P, M = cfg.stages, cfg.microbatches
+    for ws in (1, 2, P):
+        got = bbl.plan_dump(cfg.model, P, M, rc=rc, world_size=ws)
+        assert got == _oracle_normal(cfg, P, M, rc, ws)
+
+
+def test_failover_and_recovery_dumps_match_oracle():
+    _lib_or_skip()
+    r = random.Random(3)
+    cfg = get_config("C3")   # 48 layers: any P <= 8 is valid
+    cases = [(2, 4), (8, 32), (4, 8), (8, 16)] + [(r.randint(2, 8), r.randint(1, 32))
+                                                 for _ in range(12)]
+    for P, M in cases:
+        plans = pl.normal_plans(P, M, True)
+        for v in range(P):
+            host, rep = pl.failover_topology(P, v)
+            want = pl.dump(P, M, True, pl.partition(48, P), pl.failover_plans(P, M, v), host, rep,
+                           mode="failover", victim=v)
+            assert bbl.plan_dump(cfg.model, P, M, victim=v, at_instr=-1) == want
+            pis = {0, len(plans[v]), len(plans[v]) // 2} | {r.randint(0, len(plans[v]))
+                                                             for _ in range(3)}
+            for pi in sorted(pis):
+                assert bbl.plan_dump(cfg.model, P, M, victim=v, at_instr=pi) == \
+                    pl.recovery_dump(P, M, v, pi), (P, M, v, pi)
+
+
+def test_invalid_configs_rejected():
+    _lib_or_skip()
+    cfg = get_config("C0")
+    with pytest.raises(bbl.BambooError):
+        bbl.plan_dump(cfg.model, 5, 4)              # stages > n_layer
+    with pytest.raises(bbl.BambooError):
+        bbl.plan_dump(cfg.model, 1, 4, victim=0)    # no replica without RC partner
