@@ -190,6 +190,7 @@ void bb_destroy(void *ctx);
  *   3 BIAS_GELU  aux[m*ldc+n] = D + bias[n] (pre-activation), C = gelu_tanh(pre)
  *   4 GELU_BWD   C = D * gelu_tanh'(aux[m*ldc+n])
  *   5 ACC_F32    Cf32[m*ldc+n] += D                      (fp32 output)
+ *   6 STORE_F32  Cf32[m*ldc+n]  = D                      (fp32 output)
  * prec = BB_PREC_BF16 (bf16 operands, tcgen05 tensor cores, fp32 accumulate)
  * or BB_PREC_FP32_CHECK (fp32 SIMT). impl: 0 = default, 1 = force SIMT. */
 bb_status bb_op_gemm(int prec, int impl, int M, int N, int K, const void *A, int lda, int a_mn,
@@ -203,13 +204,14 @@ bb_status bb_op_attention_fwd(int prec, int B, int S, int H, int nh, int causal,
 bb_status bb_op_attention_bwd(int prec, int B, int S, int H, int nh, int causal, const void *qkv,
                               const void *o, const float *lse, const void *dout, void *dqkv,
                               void *stream);
-/* LayerNorm over rows [R, H]: y, mean, rstd; backward dx = dres + LN'(dy),
- * dg/db accumulated (+=) into fp32 [H]. dres may be NULL. */
+/* LayerNorm over rows [R, H]: y, mean, rstd; backward dx = dres + LN'(dy)
+ * with dy and dres fp32 [R, H] (dres may be NULL), dx in the act dtype,
+ * dg/db accumulated (+=) into fp32 [H]. */
 bb_status bb_op_layernorm_fwd(int prec, int R, int H, const void *x, const void *g, const void *b,
                               void *y, float *mean, float *rstd, void *stream);
-bb_status bb_op_layernorm_bwd(int prec, int R, int H, const void *dy, const void *x,
+bb_status bb_op_layernorm_bwd(int prec, int R, int H, const float *dy, const void *x,
                               const float *mean, const float *rstd, const void *g,
-                              const void *dres, void *dx, float *dg, float *db, void *stream);
+                              const float *dres, void *dx, float *dg, float *db, void *stream);
 /* Cross-entropy over logits [R, V] (overwritten with dlogits = (softmax -
  * onehot)/n_tok), loss_rows[R] fp32 = (lse - logit[target]) / n_tok. */
 bb_status bb_op_cross_entropy(int prec, int R, int V, void *logits, const int32_t *targets,

@@ -170,7 +170,7 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
 bb_status bb_op_gemm(int prec, int impl, int M, int N, int K, const void *A, int lda, int a_mn,
                      const void *B, int ldb, int b_mn, int epi, void *C, int ldc,
                      const void *bias, const void *res, void *aux, void *stream) {
-  if (epi < 0 || epi > 5 || M < 0 || N < 0 || K < 0) return BB_E_INVAL;
+  if (epi < 0 || epi > 6 || M < 0 || N < 0 || K < 0) return BB_E_INVAL;
   bb::k::Gemm g{M, N, K, A, lda, a_mn != 0, B, ldb, b_mn != 0, epi, C, ldc, bias, res, aux};
   const bool b16 = prec == BB_PREC_BF16;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -209,18 +209,19 @@ bb_status bb_op_layernorm_fwd(int prec, int R, int H, const void *x, const void 
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 
-bb_status bb_op_layernorm_bwd(int prec, int R, int H, const void *dy, const void *x,
+bb_status bb_op_layernorm_bwd(int prec, int R, int H, const float *dy, const void *x,
                               const float *mean, const float *rstd, const void *g,
-                              const void *dres, void *dx, float *dg, float *db, void *stream) {
+                              const float *dres, void *dx, float *dg, float *db, void *stream) {
   const bool b16 = prec == BB_PREC_BF16;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float *part = nullptr;
   if (cudaMallocAsync((void **)&part, bb::k::colreduce_partial_floats(R, H) * 4, s) != cudaSuccess)
     return BB_E_OOM;
-  cudaError_t e = bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, dx, s);
-  if (e == cudaSuccess) e = bb::k::colreduce(b16, 1, R, H, dy, x, mean, rstd, part, dg, s);
+  cudaError_t e = bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, nullptr, dx,
+                                          nullptr, s);
+  if (e == cudaSuccess) e = bb::k::colreduce(b16, true, 1, R, H, dy, x, mean, rstd, part, dg, s);
   if (e == cudaSuccess)
-    e = bb::k::colreduce(b16, 0, R, H, dy, nullptr, nullptr, nullptr, part, db, s);
+    e = bb::k::colreduce(b16, true, 0, R, H, dy, nullptr, nullptr, nullptr, part, db, s);
   cudaFreeAsync(part, s);
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }

@@ -65,6 +65,7 @@ __device__ __forceinline__ void epi_store(const Gemm &g, int m, int n, float acc
       break;
     }
     case EPI_ACC_F32: reinterpret_cast<float *>(g.C)[idx] += acc; break;
+    case EPI_STORE_F32: reinterpret_cast<float *>(g.C)[idx] = acc; break;
   }
 }
 

@@ -42,10 +42,11 @@ __global__ void ln_fwd_kernel(int R, int H, const T *__restrict__ x, const T *__
 }
 
 template <typename T>
-__global__ void ln_bwd_dx_kernel(int R, int H, const T *__restrict__ dy, const T *__restrict__ x,
-                                 const float *__restrict__ mean, const float *__restrict__ rstd,
-                                 const T *__restrict__ g, const T *__restrict__ dres,
-                                 T *__restrict__ dx) {
+__global__ void ln_bwd_dx_kernel(int R, int H, const float *__restrict__ dy,
+                                 const T *__restrict__ x, const float *__restrict__ mean,
+                                 const float *__restrict__ rstd, const T *__restrict__ g,
+                                 const float *__restrict__ dres32, const T *__restrict__ dresT,
+                                 T *__restrict__ dxT, float *__restrict__ dx32) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= R) return;
@@ -53,26 +54,28 @@ __global__ void ln_bwd_dx_kernel(int R, int H, const T *__restrict__ dy, const T
   const float mu = mean[row], rs = rstd[row];
   float s1 = 0.f, s2 = 0.f;
   for (int i = lane; i < H; i += 32) {
-    const float gd = to_f(dy[off + i]) * to_f(g[i]);
+    const float gd = dy[off + i] * to_f(g[i]);
     const float xh = (to_f(x[off + i]) - mu) * rs;
     s1 += gd;
     s2 += gd * xh;
   }
   const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
   for (int i = lane; i < H; i += 32) {
-    const float gd = to_f(dy[off + i]) * to_f(g[i]);
+    const float gd = dy[off + i] * to_f(g[i]);
     const float xh = (to_f(x[off + i]) - mu) * rs;
     float v = rs * (gd - m1 - xh * m2);
-    if (dres) v += to_f(dres[off + i]);
-    dx[off + i] = from_f<T>(v);
+    if (dres32) v += dres32[off + i];
+    else if (dresT) v += to_f(dresT[off + i]);
+    dxT[off + i] = from_f<T>(v);
+    if (dx32) dx32[off + i] = v;
   }
 }
 
 // ------------------------------------------------------- column reductions
 constexpr int CR_ROWS = 64, CR_COLS = 128;
 
-template <typename T>
-__global__ void colreduce_partial_kernel(int mode, int R, int N, const T *__restrict__ A,
+template <typename TA, typename T>
+__global__ void colreduce_partial_kernel(int mode, int R, int N, const TA *__restrict__ A,
                                          const T *__restrict__ X, const float *__restrict__ mean,
                                          const float *__restrict__ rstd, float *__restrict__ part) {
   const int n = blockIdx.x * CR_COLS + threadIdx.x;
@@ -266,17 +269,18 @@ cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g,
   return cudaGetLastError();
 }
 
-cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const void *dy, const void *x,
+cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const void *x,
                              const float *mean, const float *rstd, const void *g,
-                             const void *dres, void *dx, cudaStream_t s) {
+                             const float *dres32, const void *dresT, void *dxT, float *dx32,
+                             cudaStream_t s) {
   const int grid = (R + 7) / 8;
   if (bf16)
-    ln_bwd_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(dy),
-        cp<__nv_bfloat16>(x), mean, rstd, cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(dres),
-        mp<__nv_bfloat16>(dx));
+    ln_bwd_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, dy, cp<__nv_bfloat16>(x), mean,
+        rstd, cp<__nv_bfloat16>(g), dres32, cp<__nv_bfloat16>(dresT), mp<__nv_bfloat16>(dxT),
+        dx32);
   else
-    ln_bwd_dx_kernel<float><<<grid, 256, 0, s>>>(R, H, cp<float>(dy), cp<float>(x), mean, rstd,
-                                                 cp<float>(g), cp<float>(dres), mp<float>(dx));
+    ln_bwd_dx_kernel<float><<<grid, 256, 0, s>>>(R, H, dy, cp<float>(x), mean, rstd, cp<float>(g),
+                                                 dres32, cp<float>(dresT), mp<float>(dxT), dx32);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -285,17 +289,20 @@ size_t colreduce_partial_floats(int R, int N) {
   return (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;
 }
 
-cudaError_t colreduce(bool bf16, int mode, int R, int N, const void *A, const void *X,
+cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void *A, const void *X,
                       const float *mean, const float *rstd, float *partial, float *out,
                       cudaStream_t s) {
   const int chunks = (R + CR_ROWS - 1) / CR_ROWS;
   dim3 grid((N + CR_COLS - 1) / CR_COLS, chunks);
-  if (bf16)
-    colreduce_partial_kernel<__nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
+  if (bf16 && a_f32)
+    colreduce_partial_kernel<float, __nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
+        mode, R, N, cp<float>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+  else if (bf16)
+    colreduce_partial_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
         mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
   else
-    colreduce_partial_kernel<float><<<grid, CR_COLS, 0, s>>>(mode, R, N, cp<float>(A),
-                                                             cp<float>(X), mean, rstd, partial);
+    colreduce_partial_kernel<float, float><<<grid, CR_COLS, 0, s>>>(
+        mode, R, N, cp<float>(A), cp<float>(X), mean, rstd, partial);
   colreduce_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(chunks, N, partial, out);
   g_launches += 2;
   return cudaGetLastError();
@@ -313,17 +320,17 @@ cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const 
   return cudaGetLastError();
 }
 
-cudaError_t embed_bwd(bool bf16, int R, int S, int H, int U, const int32_t *uniq,
+cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const int32_t *uniq,
                       const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
                       float *dPos, cudaStream_t s) {
-  if (bf16) {
+  if (dx_f32 || !bf16) {
+    embed_bwd_tok_kernel<float><<<U, 128, 0, s>>>(H, uniq, offs, pos, cp<float>(dx), dE);
+    embed_bwd_pos_kernel<float><<<S, 128, 0, s>>>(R / S, S, H, cp<float>(dx), dPos);
+  } else {
     embed_bwd_tok_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(H, uniq, offs, pos,
                                                           cp<__nv_bfloat16>(dx), dE);
     embed_bwd_pos_kernel<__nv_bfloat16><<<S, 128, 0, s>>>(R / S, S, H, cp<__nv_bfloat16>(dx),
                                                           dPos);
-  } else {
-    embed_bwd_tok_kernel<float><<<U, 128, 0, s>>>(H, uniq, offs, pos, cp<float>(dx), dE);
-    embed_bwd_pos_kernel<float><<<S, 128, 0, s>>>(R / S, S, H, cp<float>(dx), dPos);
   }
   g_launches += 2;
   return cudaGetLastError();

@@ -10,7 +10,7 @@ namespace bb {
 namespace k {
 
 enum Epi : int { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_RES = 2, EPI_BIAS_GELU = 3,
-                 EPI_GELU_BWD = 4, EPI_ACC_F32 = 5 };
+                 EPI_GELU_BWD = 4, EPI_ACC_F32 = 5, EPI_STORE_F32 = 6 };
 
 // D[m][n] = sum_k A(m,k) B(n,k); A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m] (a_mn=1).
 struct Gemm {
@@ -35,21 +35,26 @@ cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const 
                       const void *Pos, void *x, cudaStream_t s);
 // Deterministic embedding backward: tokens of the micro-batch grouped by id
 // (host-built CSR: uniq[U], offs[U+1], pos[R] ascending within a group).
-cudaError_t embed_bwd(bool bf16, int R, int S, int H, int U, const int32_t *uniq,
+cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const int32_t *uniq,
                       const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
                       float *dPos, cudaStream_t s);
 
 cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
                           void *y, float *mean, float *rstd, cudaStream_t s);
-// dx = dres + LN'(dy) (dres may be null). Parameter grads via colreduce.
-cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const void *dy, const void *x,
+// dx = dres + LN'(dy). dy is fp32 (a GEMM output); the residual gradient
+// dres is fp32 (dres32) or storage type (dresT) or absent; dx is written in
+// the storage type (dxT, a GEMM operand) and, if dx32 != null, in fp32 too
+// (the residual-gradient chain stays fp32 inside a stage).
+cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const void *x,
                              const float *mean, const float *rstd, const void *g,
-                             const void *dres, void *dx, cudaStream_t s);
+                             const float *dres32, const void *dresT, void *dxT, float *dx32,
+                             cudaStream_t s);
 // Deterministic column reductions, two passes through `partial` (>= colreduce_partial_floats):
 //   mode 0: out[n] += sum_r A[r][n]                     (bias gradient)
 //   mode 1: out[n] += sum_r A[r][n] * (X[r][n]-mean[r])*rstd[r]   (LN gamma gradient)
 size_t colreduce_partial_floats(int R, int N);
-cudaError_t colreduce(bool bf16, int mode, int R, int N, const void *A, const void *X,
+// a_f32: A is fp32 (else storage type); X is always storage type.
+cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void *A, const void *X,
                       const float *mean, const float *rstd, float *partial, float *out,
                       cudaStream_t s);
 

@@ -316,6 +316,9 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
 // Backward of stage X for micro-batch k (main stream). dout = gradient w.r.t.
 // the stage output (nullptr for the last stage); x_in = stage input act.
 // Writes the gradient w.r.t. the stage input into dx_out (if X > 0).
+// Inside the stage the residual-gradient chain is carried in fp32 (s32) next
+// to its storage-type copy (a GEMM operand); GEMM outputs that only feed a
+// LayerNorm backward are written in fp32.
 void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStream_t s,
                     const void *x_in, const void *dout, void *dx_out) {
   const Dims &d = c.d;
@@ -323,36 +326,40 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
   char *sl = cp.slots + (size_t)slot * si.slot_bytes;
   const int R = d.R(), H = d.H, F = d.F;
   const bool b16 = c.bf16;
-  const void *dy = dout;
+  const void *dy = dout;      // storage type
+  const float *dy32 = nullptr;
   int flip = 0;
   for (int i = (int)si.up.size() - 1; i >= 0; --i) {
     const UnitP &p = si.up[i];
     const UnitS &u = si.us[i];
     const void *x = i == 0 ? x_in : (const void *)(sl + si.us[i - 1].out);
     void *dx = i == 0 ? dx_out : nd.sH[3 + flip];
+    float *dx32 = i == 0 ? nullptr : nd.s32[2 + flip];
     flip ^= 1;
     if (p.kind == 0) {
       Prof pf(c, nd, s, PC_EMB, 0);
       const int32_t *csr = nd.d_csr + (size_t)k * c.csr_stride;
       const int U = c.csr_U[k];
-      CK(k::embed_bwd(b16, R, d.S, H, U, csr, csr + R, csr + 2 * R + 1, dy, pg(cp, p.tok),
-                      pg(cp, p.pos), s));
+      CK(k::embed_bwd(b16, dy32 != nullptr, R, d.S, H, U, csr, csr + R, csr + 2 * R + 1,
+                      dy32 ? (const void *)dy32 : dy, pg(cp, p.tok), pg(cp, p.pos), s));
     } else if (p.kind == 2) {
+      float *dhf = nd.s32[0];
       gemm(c, nd, s, PC_GEMM_DX,
-           {R, H, d.V, sl + u.dlog, d.V, false, pw(c, cp, p.whead), H, true, k::EPI_STORE,
-            nd.sH[0], H, nullptr, nullptr, nullptr});
+           {R, H, d.V, sl + u.dlog, d.V, false, pw(c, cp, p.whead), H, true, k::EPI_STORE_F32,
+            dhf, H, nullptr, nullptr, nullptr});
       gemm(c, nd, s, PC_GEMM_DW,
            {d.V, H, R, sl + u.dlog, d.V, true, sl + u.hf, H, true, k::EPI_ACC_F32,
             pg(cp, p.whead), H, nullptr, nullptr, nullptr});
       Prof pf(c, nd, s, PC_LN, 0);
-      CK(k::layernorm_bwd_dx(b16, R, H, nd.sH[0], x, (float *)(sl + u.meanf),
-                             (float *)(sl + u.rstdf), pw(c, cp, p.lnfg), nullptr, dx, s));
-      CK(k::colreduce(b16, 1, R, H, nd.sH[0], x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
-                      nd.s_part, pg(cp, p.lnfg), s));
-      CK(k::colreduce(b16, 0, R, H, nd.sH[0], nullptr, nullptr, nullptr, nd.s_part,
+      CK(k::layernorm_bwd_dx(b16, R, H, dhf, x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
+                             pw(c, cp, p.lnfg), nullptr, nullptr, dx, dx32, s));
+      CK(k::colreduce(b16, true, 1, R, H, dhf, x, (float *)(sl + u.meanf),
+                      (float *)(sl + u.rstdf), nd.s_part, pg(cp, p.lnfg), s));
+      CK(k::colreduce(b16, true, 0, R, H, dhf, nullptr, nullptr, nullptr, nd.s_part,
                       pg(cp, p.lnfb), s));
     } else {
-      void *dpre = nd.sF, *dh2 = nd.sH[0], *dx1 = nd.sH[1], *dO = nd.sH[2], *dqkv = nd.s3;
+      void *dpre = nd.sF, *dx1 = nd.sH[1], *dO = nd.sH[2], *dqkv = nd.s3;
+      float *dh2 = nd.s32[0], *dx1_32 = nd.s32[1], *dh1 = nd.s32[0];
       gemm(c, nd, s, PC_GEMM_DX,
            {R, F, H, dy, H, false, pw(c, cp, p.w2), F, true, k::EPI_GELU_BWD, dpre, F, nullptr,
             nullptr, sl + u.pre});
@@ -361,27 +368,29 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
             nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, 0, R, H, dy, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.b2), s));
+        CK(k::colreduce(b16, dy32 != nullptr, 0, R, H, dy32 ? (const void *)dy32 : dy, nullptr,
+                        nullptr, nullptr, nd.s_part, pg(cp, p.b2), s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
-           {R, H, F, dpre, F, false, pw(c, cp, p.w1), H, true, k::EPI_STORE, dh2, H, nullptr,
+           {R, H, F, dpre, F, false, pw(c, cp, p.w1), H, true, k::EPI_STORE_F32, dh2, H, nullptr,
             nullptr, nullptr});
       gemm(c, nd, s, PC_GEMM_DW,
            {F, H, R, dpre, F, true, sl + u.h2, H, true, k::EPI_ACC_F32, pg(cp, p.w1), H, nullptr,
             nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, 0, R, F, dpre, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.b1),
-                        s));
+        CK(k::colreduce(b16, false, 0, R, F, dpre, nullptr, nullptr, nullptr, nd.s_part,
+                        pg(cp, p.b1), s));
       }
       {
         Prof pf(c, nd, s, PC_LN, 0);
         CK(k::layernorm_bwd_dx(b16, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
-                               (float *)(sl + u.rstd2), pw(c, cp, p.ln2g), dy, dx1, s));
-        CK(k::colreduce(b16, 1, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
+                               (float *)(sl + u.rstd2), pw(c, cp, p.ln2g), dy32,
+                               dy32 ? nullptr : dy, dx1, dx1_32, s));
+        CK(k::colreduce(b16, true, 1, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
                         (float *)(sl + u.rstd2), nd.s_part, pg(cp, p.ln2g), s));
-        CK(k::colreduce(b16, 0, R, H, dh2, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.ln2b),
-                        s));
+        CK(k::colreduce(b16, true, 0, R, H, dh2, nullptr, nullptr, nullptr, nd.s_part,
+                        pg(cp, p.ln2b), s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, H, dx1, H, false, pw(c, cp, p.wo), H, true, k::EPI_STORE, dO, H, nullptr,
@@ -391,36 +400,38 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
             nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, 0, R, H, dx1, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.bo), s));
+        CK(k::colreduce(b16, true, 0, R, H, dx1_32, nullptr, nullptr, nullptr, nd.s_part,
+                        pg(cp, p.bo), s));
       }
       {
         Prof pf(c, nd, s, PC_ATTN_BWD, 0);
         CK(k::attention_bwd(b16, d.mb, d.S, H, d.nh, d.causal, sl + u.qkv, sl + u.o,
                             (float *)(sl + u.lse), dO, dqkv, nd.s_attn, s));
       }
-      void *dh1 = nd.sH[0];
       gemm(c, nd, s, PC_GEMM_DX,
-           {R, H, 3 * H, dqkv, 3 * H, false, pw(c, cp, p.wqkv), H, true, k::EPI_STORE, dh1, H,
+           {R, H, 3 * H, dqkv, 3 * H, false, pw(c, cp, p.wqkv), H, true, k::EPI_STORE_F32, dh1, H,
             nullptr, nullptr, nullptr});
       gemm(c, nd, s, PC_GEMM_DW,
            {3 * H, H, R, dqkv, 3 * H, true, sl + u.h1, H, true, k::EPI_ACC_F32, pg(cp, p.wqkv), H,
             nullptr, nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, 0, R, 3 * H, dqkv, nullptr, nullptr, nullptr, nd.s_part,
+        CK(k::colreduce(b16, false, 0, R, 3 * H, dqkv, nullptr, nullptr, nullptr, nd.s_part,
                         pg(cp, p.bqkv), s));
       }
       {
         Prof pf(c, nd, s, PC_LN, 0);
         CK(k::layernorm_bwd_dx(b16, R, H, dh1, x, (float *)(sl + u.mean1),
-                               (float *)(sl + u.rstd1), pw(c, cp, p.ln1g), dx1, dx, s));
-        CK(k::colreduce(b16, 1, R, H, dh1, x, (float *)(sl + u.mean1), (float *)(sl + u.rstd1),
-                        nd.s_part, pg(cp, p.ln1g), s));
-        CK(k::colreduce(b16, 0, R, H, dh1, nullptr, nullptr, nullptr, nd.s_part, pg(cp, p.ln1b),
-                        s));
+                               (float *)(sl + u.rstd1), pw(c, cp, p.ln1g), dx1_32, nullptr, dx,
+                               dx32, s));
+        CK(k::colreduce(b16, true, 1, R, H, dh1, x, (float *)(sl + u.mean1),
+                        (float *)(sl + u.rstd1), nd.s_part, pg(cp, p.ln1g), s));
+        CK(k::colreduce(b16, true, 0, R, H, dh1, nullptr, nullptr, nullptr, nd.s_part,
+                        pg(cp, p.ln1b), s));
       }
     }
     dy = dx;
+    dy32 = dx32;
   }
 }
 }  // namespace
@@ -801,6 +812,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.sF = dmalloc(R * F * c.act_bytes);
       nd.s3 = dmalloc(R * 3 * H * c.act_bytes);
       for (auto &p : nd.sH) p = dmalloc(R * H * c.act_bytes);
+      for (auto &p : nd.s32) p = (float *)dmalloc(R * H * 4);
       nd.s_part = (float *)dmalloc(
           k::colreduce_partial_floats((int)R, (int)std::max(F, 3 * H)) * 4);
       nd.s_attn = (float *)dmalloc((size_t)c.d.mb * c.d.nh * c.d.S * 4);
@@ -1122,6 +1134,7 @@ void rt_destroy(Ctx &c) {
     cudaFree(nd.sF);
     cudaFree(nd.s3);
     for (auto p : nd.sH) cudaFree(p);
+    for (auto p : nd.s32) cudaFree(p);
     cudaFree(nd.s_part);
     cudaFree(nd.s_attn);
     cudaFree(nd.s_loss_main);

@@ -78,6 +78,7 @@ struct Node {
   size_t arena_bytes = 0, arena_used = 0;
   // backward scratch (main stream)
   void *sF = nullptr, *s3 = nullptr, *sH[5] = {};
+  float *s32[4] = {};   // fp32 [R, H]: LN-input gradients and the residual-gradient chain
   float *s_part = nullptr, *s_attn = nullptr, *s_loss_main = nullptr, *s_loss_frc = nullptr;
   int32_t *d_tok = nullptr, *d_tgt = nullptr, *d_csr = nullptr;
   std::vector<cudaEvent_t> evpool;

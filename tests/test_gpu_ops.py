@@ -53,7 +53,7 @@ def test_gemm_layouts(prec, impl, layout, shape):
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
-@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 6])
 def test_gemm_epilogues(prec, epi):
     import paper_2204_12013_b200 as bb
     M, N, K = 300, 200, 136
@@ -70,9 +70,11 @@ def test_gemm_epilogues(prec, epi):
     elif epi == 3:
         want_aux = D + bias
         want = om.gelu_fwd(want_aux)
-    else:
+    elif epi == 4:
         want = om.gelu_bwd(D, aux)
-    dt = torch.bfloat16 if prec == "bf16" else torch.float32
+    else:
+        want = D
+    dt = torch.bfloat16 if prec == "bf16" and epi != 6 else torch.float32
     C = torch.zeros((M, N), device="cuda", dtype=dt)
     dAux = dev(aux, prec) if epi == 4 else torch.zeros((M, N), device="cuda", dtype=dt)
     dbias, dres = dev(bias, prec), dev(res, prec)
@@ -127,8 +129,10 @@ def test_layernorm(prec, R, H):
     dX, dG = dev(x, prec), dev(g, prec)
     bb.op_layernorm_fwd(prec, R, H, dX.data_ptr(), dG.data_ptr(), dev(b, prec).data_ptr(),
                         y.data_ptr(), mean.data_ptr(), rstd.data_ptr())
-    bb.op_layernorm_bwd(prec, R, H, dev(dy, prec).data_ptr(), dX.data_ptr(), mean.data_ptr(),
-                        rstd.data_ptr(), dG.data_ptr(), dev(dres, prec).data_ptr(), dx.data_ptr(),
+    dy32 = torch.tensor(dy, device="cuda", dtype=torch.float32)
+    dres32 = torch.tensor(dres, device="cuda", dtype=torch.float32)
+    bb.op_layernorm_bwd(prec, R, H, dy32.data_ptr(), dX.data_ptr(), mean.data_ptr(),
+                        rstd.data_ptr(), dG.data_ptr(), dres32.data_ptr(), dx.data_ptr(),
                         dg.data_ptr(), db.data_ptr())
     torch.cuda.synchronize()
     tol = 1e-5 if prec == "fp32" else 1e-2
