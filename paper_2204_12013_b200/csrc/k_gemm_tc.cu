@@ -1,9 +1,314 @@
-// k_gemm_tc.cu — tcgen05 GEMM (placeholder until the TMA/UMMA kernel lands).
+// k_gemm_tc.cu — bf16 GEMM on the 5th-generation tensor cores (sm_100a).
+//
+// D[m][n] = sum_k A(m,k) B(n,k), fp32 accumulation in TMEM, with the fused
+// epilogues of kernels.h. One 128 x BN output tile per CTA:
+//   warp 0      TMA producer: 64-wide K slabs of A and B, 128B-swizzled, into a
+//               `STAGES`-deep shared-memory ring (mbarrier full/empty pairs);
+//               K-major operands are one box per slab, MN-major operands are
+//               loaded as 64-element MN boxes (UMMA MN-major canonical layout);
+//   warp 1      allocates TMEM, one elected lane issues tcgen05.mma
+//               (kind::f16, M=128, N=BN, K=16) and tcgen05.commit's the slot
+//               back to the producer, then the accumulator to the epilogue;
+//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time (warp w reads TMEM
+//               lanes 32*(w%4)..+31 = tile rows), apply bias / residual / GELU /
+//               GELU' / fp32 accumulate, store.
+// Deterministic: every output element is produced by one thread from one
+// accumulator whose K order is fixed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "k_common.cuh"
 
 namespace bb {
 namespace k {
-bool gemm_tc_supported(const Gemm &) { return false; }
-cudaError_t gemm_tc(const Gemm &, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+constexpr int BM = 128, BK = 64;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05, version 1), 128B swizzle.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                      // version
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: bf16 x bf16 -> f32, M = 128, N = BN.
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4)                    // D format f32
+         | (1u << 7)                  // A bf16
+         | (1u << 10)                 // B bf16
+         | ((a_mn ? 1u : 0u) << 15)   // A major
+         | ((b_mn ? 1u : 0u) << 16)   // B major
+         | ((uint32_t)(n >> 3) << 17) // N / 8
+         | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, Gemm g) {
+  using L = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t *gbase = smem_raw + (base - raw);
+  const uint32_t bars = base + L::STAGES * L::STAGE;
+  // barriers: full[STAGES], empty[STAGES], tmem_full; then the TMEM address
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (L::STAGES + s); };
+  const uint32_t done_bar = bars + 8u * (2 * L::STAGES);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::STAGES * L::STAGE + 8 * (2 * L::STAGES + 1));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < L::STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % L::STAGES;
+        const uint32_t ph = (kb / L::STAGES) & 1;
+        mbar_wait(empty_bar(s), ph ^ 1);
+        const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
+        // MN-major boxes lying entirely past M (N) are skipped: they only feed
+        // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
+        const int na = g.a_mn ? min(BM / 64, (g.M - m0 + 63) / 64) : 1;
+        const int nb = g.b_mn ? min(BN / 64, (g.N - n0 + 63) / 64) : 1;
+        mbar_expect_tx(full_bar(s), (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
+                                        (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES));
+        const int k0 = kb * BK;
+        if (!g.a_mn) {
+          tma_load_2d(sa, &map_a, full_bar(s), k0, m0);
+        } else {
+          for (int j = 0; j < na; ++j)
+            tma_load_2d(sa + j * 64 * BK * 2, &map_a, full_bar(s), m0 + 64 * j, k0);
+        }
+        if (!g.b_mn) {
+          tma_load_2d(sb, &map_b, full_bar(s), k0, n0);
+        } else {
+          for (int j = 0; j < nb; ++j)
+            tma_load_2d(sb + j * 64 * BK * 2, &map_b, full_bar(s), n0 + 64 * j, k0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      const uint32_t idesc = instr_desc(BN, g.a_mn, g.b_mn);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % L::STAGES;
+        const uint32_t ph = (kb / L::STAGES) & 1;
+        mbar_wait(full_bar(s), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          // K-major: +32 B per 16-element K step inside the 128B swizzle row;
+          // MN-major: +16 rows (2 KB) per K step, 64-element MN chunks 8 KB apart.
+          const uint64_t da = g.a_mn ? smem_desc(sa + kk * 2048, 64 * BK * 2, 1024)
+                                     : smem_desc(sa + kk * 32, 16, 1024);
+          const uint64_t db = g.b_mn ? smem_desc(sb + kk * 2048, 64 * BK * 2, 1024)
+                                     : smem_desc(sb + kk * 32, 16, 1024);
+          mma_bf16(tmem, da, db, idesc, (kb | kk) != 0);
+        }
+        mma_commit(empty_bar(s));
+      }
+      mma_commit(done_bar);
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5)
+    mbar_wait(done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp % 4;               // TMEM lane quarter this warp may read
+    const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+      if (row < g.M) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + c + j;
+          if (n < g.N) epi_store<__nv_bfloat16>(g, row, n, v[j]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+  }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor map: inner dimension `inner` (contiguous), `outer` rows of
+// `ld` elements, box {64, box_outer}, 128B swizzle, zero OOB fill.
+bool make_map(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+cudaError_t launch(const Gemm &g, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  // K-major operand: tensor {K, rows}, box {64, tile rows}; MN-major: tensor {rows, K}, box {64, 64}
+  const bool ok_a = g.a_mn ? make_map(&ma, g.A, g.M, g.K, g.lda, BK)
+                           : make_map(&ma, g.A, g.K, g.M, g.lda, BM);
+  const bool ok_b = g.b_mn ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK)
+                           : make_map(&mb, g.B, g.K, g.N, g.ldb, BN);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<BN>::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
+  gemm_tc_kernel<BN><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+}  // namespace
+
+bool gemm_tc_supported(const Gemm &g) {
+  if (g.M < 1 || g.N < 1 || g.K < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) return false;
+  if (g.lda % 8 || g.ldb % 8) return false;
+  // MN-major operands need at least one 64-wide box along M / N
+  if ((g.a_mn && g.M < 64) || (g.b_mn && g.N < 64)) return false;
+  return encode_fn() != nullptr;
+}
+
+cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
+  if (g.N >= 256) return launch<256>(g, s);
+  return launch<128>(g, s);
+}
+
 }  // namespace k
 }  // namespace bb

@@ -78,8 +78,9 @@ def test_gemm_epilogues(prec, epi):
     C = torch.zeros((M, N), device="cuda", dtype=dt)
     dAux = dev(aux, prec) if epi == 4 else torch.zeros((M, N), device="cuda", dtype=dt)
     dbias, dres = dev(bias, prec), dev(res, prec)
+    dA, dB = dev(A, prec), dev(B, prec)     # keep alive until the kernels ran
     for impl in (0, 1):
-        bb.op_gemm(prec, impl, M, N, K, dev(A, prec).data_ptr(), K, 0, dev(B, prec).data_ptr(), K,
+        bb.op_gemm(prec, impl, M, N, K, dA.data_ptr(), K, 0, dB.data_ptr(), K,
                    0, epi, C.data_ptr(), N, dbias.data_ptr(), dres.data_ptr(), dAux.data_ptr())
         torch.cuda.synchronize()
         tol = 1e-5 if prec == "fp32" else 1e-2
@@ -103,8 +104,9 @@ def test_attention(prec, causal, B, S, nh, d):
     lse = torch.zeros((B, nh, S), device="cuda", dtype=torch.float32)
     bb.op_attention_fwd(prec, B, S, H, nh, causal, dqkv_.data_ptr(), o.data_ptr(), lse.data_ptr())
     dqkv = torch.zeros_like(dqkv_)
+    ddo = dev(do, prec)
     bb.op_attention_bwd(prec, B, S, H, nh, causal, dqkv_.data_ptr(), o.data_ptr(), lse.data_ptr(),
-                        dev(do, prec).data_ptr(), dqkv.data_ptr())
+                        ddo.data_ptr(), dqkv.data_ptr())
     torch.cuda.synchronize()
     tol = 1e-5 if prec == "fp32" else 1e-2
     assert np.abs(host(o) - o_ref).max() <= tol * np.abs(o_ref).max()
@@ -126,8 +128,8 @@ def test_layernorm(prec, R, H):
     dx = torch.zeros((R, H), device="cuda", dtype=dt)
     dg = torch.zeros(H, device="cuda")
     db = torch.zeros(H, device="cuda")
-    dX, dG = dev(x, prec), dev(g, prec)
-    bb.op_layernorm_fwd(prec, R, H, dX.data_ptr(), dG.data_ptr(), dev(b, prec).data_ptr(),
+    dX, dG, dB = dev(x, prec), dev(g, prec), dev(b, prec)
+    bb.op_layernorm_fwd(prec, R, H, dX.data_ptr(), dG.data_ptr(), dB.data_ptr(),
                         y.data_ptr(), mean.data_ptr(), rstd.data_ptr())
     dy32 = torch.tensor(dy, device="cuda", dtype=torch.float32)
     dres32 = torch.tensor(dres, device="cuda", dtype=torch.float32)
@@ -151,8 +153,8 @@ def test_cross_entropy(prec, R, V):
     d_ref = om.ce_bwd(probs, tg, n_tok)
     L = dev(logits, prec)
     rows = torch.zeros(R, device="cuda")
-    bb.op_cross_entropy(prec, R, V, L.data_ptr(), torch.tensor(tg, device="cuda").data_ptr(),
-                        n_tok, rows.data_ptr())
+    dtg = torch.tensor(tg, device="cuda")
+    bb.op_cross_entropy(prec, R, V, L.data_ptr(), dtg.data_ptr(), n_tok, rows.data_ptr())
     torch.cuda.synchronize()
     tol = 1e-5 if prec == "fp32" else 1e-2
     assert abs(host(rows).sum() - loss_ref) <= tol * abs(loss_ref)
@@ -171,8 +173,10 @@ def test_adam_matches_oracle():
     for t in range(1, 4):
         g = rnd(n)
         p, m, v = om.adam_update(p, g, m, v, t, lr, b1, b2, eps)
-        bb.op_adam(n, dp.data_ptr(), torch.tensor(g, device="cuda", dtype=torch.float32).data_ptr(),
-                   dm.data_ptr(), dv.data_ptr(), w16.data_ptr(), t, lr, b1, b2, eps)
+        dg = torch.tensor(g, device="cuda", dtype=torch.float32)
+        bb.op_adam(n, dp.data_ptr(), dg.data_ptr(), dm.data_ptr(), dv.data_ptr(), w16.data_ptr(), t,
+                   lr, b1, b2, eps)
+        torch.cuda.synchronize()
     torch.cuda.synchronize()
     assert np.abs(host(dp) - p).max() <= 1e-6
     assert np.abs(host(dm) - m).max() <= 1e-6 * np.abs(m).max()
