@@ -1,0 +1,387 @@
+"""Benchmark of the Bamboo redundant-computation pipeline step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+
+A step = one synchronous 1F1B training step with eager FRC in the bubbles
+(BASELINE.json north star) over M*mb synthetic sequences: every stage's
+forward/backward, the FRC forward of its successor, P2P activations /
+gradients, replica gradient sync and both Adam updates. Workload: BASELINE
+configs[1] = GPT-2 small (12 layers, H 768, S 1024), 4 stages, M=8 micro-
+batches of 8 sequences; stages are spread over the N GPUs (N=1: all four on
+one B200; N=8: 8 stages, one per GPU, same model and batch -> strong scaling).
+
+Prints ONE JSON line (rank 0). `value` = samples/s with inputs resident in HBM
+(bb_stage_inputs), device-timed with CUDA events between synchronised
+barriers, max over ranks; `e2e` = the same through bb_step with host buffers
+(token upload and loss read-back inside the timed region).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import get_config, make_params, make_tokens  # noqa: E402
+
+BASELINE_METRIC = "samples/sec at 1/2/4/8 B200 with RC vs no-RC; RC overhead %; recovery ms"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "fallback": True}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- distributed
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, ws, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def allreduce_sum(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.item()
+
+
+def bcast_bytes(b, ws):
+    if ws == 1:
+        return b
+    import torch.distributed as dist
+    obj = [b]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+# --------------------------------------------------------------- our arm
+def timed(pipe, steps, ws, host_inputs=None):
+    """Run `steps` steps between synchronised barriers; CUDA events on the
+    current stream bracket the region (bb_step synchronises its own streams
+    before returning, so the end event follows all of the step's work)."""
+    import torch
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches, h2d, d2h = 0, 0, 0
+    e0.record()
+    for i in range(steps):
+        if host_inputs is None:
+            status, st = pipe.step()
+        else:
+            tok, tgt = host_inputs[i % len(host_inputs)]
+            status, st = pipe.step(tok, tgt)
+        assert status == "ok"
+        launches += st.gpu_launches
+        h2d += st.h2d_bytes
+        d2h += st.d2h_bytes
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = allreduce_max(e0.elapsed_time(e1), ws)
+    return ms, launches, h2d, d2h
+
+
+def run_ours(args, rank, ws, local):
+    import torch
+    import paper_2204_12013_b200 as bb
+
+    cfg = get_config(args.config)
+    m = cfg.model
+    P = max(cfg.stages, ws)
+    M, mb = cfg.microbatches, cfg.micro_batch
+    samples = M * mb
+    nccl_id = bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
+    flat = make_params(m)
+    tok, tgt = make_tokens(cfg, 0)
+    host_batches = [make_tokens(cfg, s) for s in range(1, 3)]
+    common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
+                  nccl_id=nccl_id)
+
+    results = {}
+    for rc in (False, True):
+        pipe = bb.Pipeline(m, P, M, rc=rc, profile=rc, **common)
+        pipe.load_params(flat)
+        pipe.stage_inputs(tok, tgt)
+        for _ in range(args.warmup):
+            pipe.step()
+        clocks = Clocks(local)
+        if rc:
+            clocks.start()
+        ms, launches, _, _ = timed(pipe, args.steps, ws)
+        clk = clocks.stop() if rc else None
+        kstats = pipe.kernel_stats() if rc else None
+        # end to end through the public call with host buffers
+        ms_e2e, _, h2d, d2h = timed(pipe, args.steps, ws, host_inputs=host_batches)
+        results[rc] = dict(ms=ms / args.steps, launches=launches, clocks=clk, kstats=kstats,
+                           e2e_ms=ms_e2e / args.steps, h2d=h2d / args.steps, d2h=d2h / args.steps)
+        if rc:
+            # recovery latency: preempt the middle node in its backward phase
+            # (P:69), pause = interrupted step incl. bb_recover - failure-free step
+            v = P // 2
+            dump = pipe.schedule_dump().splitlines()
+            bwd_idx = [int(l.split()[1]) for l in dump if not l.startswith("#")
+                       and l.split()[0] == str(v) and l.split()[2] == "BWD"]
+            pi = bwd_idx[(M + 1) // 2 - 1] + 1
+            pipe.preempt(v, pi)
+            barrier(ws)
+            t0 = time.perf_counter()
+            status, _ = pipe.step()
+            rec = pipe.recover() if status == "preempted" else None
+            torch.cuda.synchronize()
+            barrier(ws)
+            t_int = allreduce_max((time.perf_counter() - t0) * 1e3, ws)
+            ms_fo, _, _, _ = timed(pipe, max(1, min(3, args.steps)), ws)
+            results["recovery"] = dict(victim=v, at_instr=pi, interrupted_step_ms=t_int,
+                                       recover_ms=allreduce_max(rec.recover_ms if rec else 0, ws),
+                                       brc_mb=rec.brc_mb if rec else 0,
+                                       failover_step_ms=ms_fo / max(1, min(3, args.steps)))
+        pipe.close()
+        del pipe
+        torch.cuda.empty_cache()
+
+    on, off = results[True], results[False]
+    value = samples / (on["ms"] / 1e3)
+    pk = peaks()
+    ks = on["kstats"] or {}
+    gemm_ms = sum(ks[k][1] for k in ks if k.startswith("gemm"))
+    gemm_flop = sum(ks[k][2] for k in ks if k.startswith("gemm"))
+    gemm_n = sum(ks[k][0] for k in ks if k.startswith("gemm"))
+    # profiled totals are per rank over the timed steps; aggregate over ranks
+    gemm_ms_all = allreduce_sum(gemm_ms, ws)
+    gemm_flop_all = allreduce_sum(gemm_flop, ws)
+    achieved = gemm_flop_all / (gemm_ms_all / 1e3) / 1e12 if gemm_ms_all > 0 else 0.0
+    launches = allreduce_sum(on["launches"], ws)
+    rec = results.get("recovery", {})
+    if rank != 0:
+        return
+    roof = {"bound": "tensor", "achieved": round(achieved, 1),
+            "peak": pk.get("bf16_tflops_sustained", 1377.6), "unit": "TFLOP/s",
+            "frac": round(achieved / pk.get("bf16_tflops_sustained", 1377.6), 4),
+            "traffic": None, "kernel": "gemm_tc (tcgen05 bf16, all GEMM launches of the step)",
+            "launches_per_step": gemm_n / args.steps,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
+    ncu = os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")
+    if os.path.exists(ncu):
+        try:
+            roof["traffic"] = json.load(open(ncu)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    train_flop = useful_flop_per_sample(cfg)
+    line = {
+        "metric": BASELINE_METRIC,
+        "value": round(value, 2), "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(on["ms"], 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded tokens, random-init weights)",
+        "config": {"workload": f"{cfg.name}: GPT-2 small 12L H768 S1024, {P} stages, M={M}, "
+                               f"mb={mb}, EFLB (eager FRC, lazy BRC)",
+                   "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
+                   "seq_len": m.seq_len, "parallelism": f"pp{P} on {ws} GPU(s)",
+                   "l2": "working set (weights, stash, FRC retention) >> 126 MB L2"},
+        "rc_off": {"value": round(samples / (off["ms"] / 1e3), 2), "ms_per_step": round(off["ms"], 3)},
+        "rc_overhead_pct": round(100.0 * (1 - off["ms"] / on["ms"]), 2),
+        "recovery": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in rec.items()},
+        "recovery_ms": round(rec.get("interrupted_step_ms", 0) - on["ms"], 3) if rec else None,
+        "roofline": roof,
+        "model_flops_frac": round(value * train_flop / (ws * pk.get("bf16_tflops", 1657.2) * 1e12), 4),
+        "e2e": {"value": round(samples / (on["e2e_ms"] / 1e3), 2), "unit": "samples/s",
+                "h2d_bytes_per_step": int(on["h2d"]), "d2h_bytes_per_step": int(on["d2h"])},
+        "gpu_launches": int(launches),
+        "clocks": on["clocks"],
+        "kernel_ms_per_step": {k: round(v[1] / args.steps, 3) for k, v in ks.items()},
+    }
+    if args.cpu_baseline and ws >= 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+
+
+def useful_flop_per_sample(cfg):
+    """3 x forward FLOPs per sample: GEMMs + causal attention
+    counted as half, LM head included."""
+    m = cfg.model
+    H, F, V, S = m.d_model, m.d_ff, m.vocab, m.seq_len
+    per_tok = m.n_layer * (2 * (3 * H * H + H * H + 2 * H * F)) + 2 * H * V
+    attn = m.n_layer * 2 * 2 * S * H * (0.5 if m.causal else 1.0)
+    return 3 * S * (per_tok + attn)
+
+
+# ------------------------------------------------ oracle (CPU) baseline leg
+def cpu_baseline(cfg, budget_s=20.0):
+    """Time the fp64 oracle as it stands on this host: one sequence through
+    one transformer block and through the LM head at the config's width,
+    forward + backward, then scale to the full step with RC (12 blocks fwd +
+    bwd + head, plus the FRC forward of every stage = one more forward)."""
+    import threadpoolctl
+    from oracle import model as om
+    m = cfg.model
+    lay = om.Layout(m)
+    flat = make_params(m).astype(np.float64)
+    th = lay.tensors(flat, 0, lay.total)
+    gr = lay.tensors(np.zeros(lay.total), 0, lay.total)
+    tok, tgt = make_tokens(cfg, 0)
+    tok, tgt = tok[:1], tgt[:1]
+    ntok = tok.size
+    x = om.embedding_fwd(th["tok_emb"], th["pos_emb"], tok)
+    t_fb, t_f, t_hf, t_hb, reps = 0.0, 0.0, 0.0, 0.0, 0
+    t_start = time.perf_counter()
+    while reps == 0 or time.perf_counter() - t_start < budget_s / 2:
+        t0 = time.perf_counter()
+        y, sv = om.unit_fwd(lay, 1, th, x, tok, tgt, ntok)
+        t1 = time.perf_counter()
+        om.unit_bwd(lay, 1, th, gr, sv, np.ones_like(y), tok, tgt, ntok)
+        t2 = time.perf_counter()
+        loss, svh = om.unit_fwd(lay, m.n_layer + 1, th, x, tok, tgt, ntok)
+        t3 = time.perf_counter()
+        om.unit_bwd(lay, m.n_layer + 1, th, gr, svh, None, tok, tgt, ntok)
+        t4 = time.perf_counter()
+        t_f += t1 - t0
+        t_fb += t2 - t0
+        t_hf += t3 - t2
+        t_hb += t4 - t3
+        reps += 1
+    per_seq = (m.n_layer * (t_fb + t_f) + (t_hf + t_hb) + t_hf) / reps
+    info = threadpoolctl.threadpool_info()
+    threads = max([i.get("num_threads", 1) for i in info] or [1])
+    return {"value": round(1.0 / per_seq, 5), "unit": "samples/s", "cores": threads,
+            "host_cpus": os.cpu_count(), "kind": "oracle",
+            "sample": f"{reps} reps of 1 sequence (S={m.seq_len}) through 1 block + LM head at "
+                      f"{cfg.name} width, fp64 numpy fwd+bwd, scaled to {m.n_layer} blocks fwd+bwd"
+                      f" + head + FRC forward"}
+
+
+def run_reference(args, rank, ws):
+    if rank != 0:
+        return
+    cfg = get_config(args.config)
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, budget_s=budget)
+    vals = []
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(cfg, budget_s=budget)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    v = statistics.median(vals)
+    line = {"metric": BASELINE_METRIC, "impl": "reference", "value": v, "unit": "samples/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * wall / args.steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded tokens, random-init weights)",
+            "config": {"workload": f"{cfg.name} (oracle, CPU)", "stages": cfg.stages,
+                       "microbatches": cfg.microbatches, "micro_batch": cfg.micro_batch},
+            "cpu_baseline": dict(last, value=v),
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    rank, ws, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, ws)
+    else:
+        run_ours(args, rank, ws, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -125,8 +125,15 @@ bb_status bb_load_params(void *ctx, const float *host, size_t n);
  * [M*mb, seq_len] row-major (micro-batch k = rows k*mb..k*mb+mb-1). Every rank
  * passes the full arrays and uploads what its nodes need (the last node
  * fetches inputs for its FRC). Returns BB_E_PREEMPTED if an armed injection
- * fired (bb_recover must follow). st may be NULL. */
+ * fired (bb_recover must follow). st may be NULL. tokens = targets = NULL
+ * reuses the inputs last staged with bb_stage_inputs (already in HBM: no
+ * host-to-device copy inside the call). */
 bb_status bb_step(void *ctx, const int32_t *tokens, const int32_t *targets, bb_step_stats *st);
+
+/* Upload tokens/targets (same layout as bb_step) to every local node's HBM
+ * now, so that following bb_step(ctx, NULL, NULL, st) calls run on resident
+ * inputs. A bb_step with host arrays replaces them. */
+bb_status bb_stage_inputs(void *ctx, const int32_t *tokens, const int32_t *targets);
 
 /* Arm a preemption of node `stage` after it has executed `at_instr` (pi)
  * instructions of its list in the next step (0 <= pi <= list length). Must be

@@ -21,6 +21,7 @@ PREC = {"bf16": 0, "fp32": 1}
 STATE = {"params": 0, "grads": 1, "adam_m": 2, "adam_v": 3}
 
 EXPORTED = ["bb_default_opts", "bb_nccl_unique_id", "bb_init", "bb_load_params", "bb_step",
+            "bb_stage_inputs",
             "bb_preempt", "bb_recover", "bb_read_state", "bb_stage_params", "bb_schedule_dump",
             "bb_recovery_dump", "bb_kernel_stats", "bb_plan_dump", "bb_last_error", "bb_destroy",
             "bb_op_gemm", "bb_op_attention_fwd", "bb_op_attention_bwd", "bb_op_layernorm_fwd",
@@ -85,6 +86,7 @@ def lib():
         _lib.bb_step.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.POINTER(BBStepStats)]
         _lib.bb_preempt.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        _lib.bb_stage_inputs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib.bb_recover.argtypes = [ctypes.c_void_p, ctypes.POINTER(BBRecoveryStats)]
         _lib.bb_read_state.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_void_p, ctypes.c_size_t]
@@ -213,12 +215,22 @@ class Pipeline:
         flat = np.ascontiguousarray(flat, dtype=np.float32)
         self._check(lib().bb_load_params(self._h, flat.ctypes.data, flat.size), "bb_load_params")
 
-    def step(self, tokens, targets):
-        """Returns ('ok' | 'preempted', BBStepStats)."""
+    def stage_inputs(self, tokens, targets):
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         g = np.ascontiguousarray(targets, dtype=np.int32)
+        self._check(lib().bb_stage_inputs(self._h, t.ctypes.data, g.ctypes.data),
+                    "bb_stage_inputs")
+
+    def step(self, tokens=None, targets=None):
+        """Returns ('ok' | 'preempted', BBStepStats). tokens=targets=None runs
+        on the inputs staged with stage_inputs (resident in HBM)."""
         st = BBStepStats()
-        s = lib().bb_step(self._h, t.ctypes.data, g.ctypes.data, ctypes.byref(st))
+        if tokens is None:
+            s = lib().bb_step(self._h, None, None, ctypes.byref(st))
+        else:
+            t = np.ascontiguousarray(tokens, dtype=np.int32)
+            g = np.ascontiguousarray(targets, dtype=np.int32)
+            s = lib().bb_step(self._h, t.ctypes.data, g.ctypes.data, ctypes.byref(st))
         if s == BB_E_PREEMPTED:
             return "preempted", st
         self._check(s, "bb_step")

@@ -70,6 +70,11 @@ bb_status bb_step(void *ctx, const int32_t *tokens, const int32_t *targets, bb_s
   return bb::rt_step(*static_cast<Ctx *>(ctx), tokens, targets, st);
 }
 
+bb_status bb_stage_inputs(void *ctx, const int32_t *tokens, const int32_t *targets) {
+  if (!ctx) return BB_E_INVAL;
+  return bb::rt_stage_inputs(*static_cast<Ctx *>(ctx), tokens, targets);
+}
+
 bb_status bb_preempt(void *ctx, int stage, int at_instr) {
   if (!ctx) return BB_E_INVAL;
   return bb::rt_preempt(*static_cast<Ctx *>(ctx), stage, at_instr);

@@ -474,11 +474,13 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
   switch (ins.kind) {
     case LOAD_INPUTS: {
       const size_t n = (size_t)M * d.R();
-      CK(cudaMemcpyAsync(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice, nd.main));
-      CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice, nd.main));
-      CK(cudaMemcpyAsync(nd.d_csr, c.h_csr, (size_t)M * c.csr_stride * 4, cudaMemcpyHostToDevice,
-                         nd.main));
-      c.h2d += 2 * n * 4 + (size_t)M * c.csr_stride * 4;
+      if (!c.resident_step) {   // the last node fetches its inputs itself
+        CK(cudaMemcpyAsync(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice, nd.main));
+        CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice, nd.main));
+        CK(cudaMemcpyAsync(nd.d_csr, c.h_csr, (size_t)M * c.csr_stride * 4,
+                           cudaMemcpyHostToDevice, nd.main));
+        c.h2d += 2 * n * 4 + (size_t)M * c.csr_stride * 4;
+      }
       cudaEvent_t e = record(nd, nd.main);
       for (int j = 0; j < M; ++j) {
         nd.store[{K_TOK, j, 0}] = {nd.d_tok + (size_t)j * d.R(), e};
@@ -920,10 +922,15 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
   try {
     if (c.fatal) return BB_E_FATAL;
     if (c.interrupted) throw RtError{BB_E_STATE, "bb_recover pending"};
-    if (!tok || !tgt) throw RtError{BB_E_INVAL, "null tokens/targets"};
+    if ((tok == nullptr) != (tgt == nullptr)) throw RtError{BB_E_INVAL, "null tokens/targets"};
+    if (!tok && !c.resident) throw RtError{BB_E_STATE, "no resident inputs (bb_stage_inputs)"};
     CK(cudaSetDevice(c.o.device));
     begin_step(c);
-    stage_inputs(c, tok, tgt);
+    c.resident_step = tok == nullptr;
+    if (tok) {
+      stage_inputs(c, tok, tgt);
+      c.resident = false;   // LOAD_INPUTS overwrites the device copies
+    }
     if (!c.armed) {
       run(c, c.plans, nullptr, Phase{});
       sync_all(c, true);
@@ -962,6 +969,26 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
       finish_stats(c, st, t0);
     }
     return BB_E_PREEMPTED;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+bb_status rt_stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
+  try {
+    if (!tok || !tgt) throw RtError{BB_E_INVAL, "null tokens/targets"};
+    CK(cudaSetDevice(c.o.device));
+    stage_inputs(c, tok, tgt);
+    const size_t n = (size_t)c.d.M * c.d.R();
+    for (auto &kv : c.nodes) {
+      Node &nd = kv.second;
+      CK(cudaMemcpy(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(nd.d_csr, c.h_csr, (size_t)c.d.M * c.csr_stride * 4, cudaMemcpyHostToDevice));
+    }
+    c.resident = true;
+    return BB_OK;
   } catch (const RtError &e) {
     c.err = e.msg;
     return e.st;

@@ -132,7 +132,8 @@ struct Ctx {
   int32_t *h_tok = nullptr, *h_tgt = nullptr, *h_csr = nullptr;
   std::vector<int> csr_U;
   size_t csr_stride = 0;
-  double bc_t = 0;
+  bool resident = false;        // inputs staged on every local node's device (bb_stage_inputs)
+  bool resident_step = false;   // this step reuses the resident inputs (no H2D)
   std::string err;
   // profiling
   std::vector<ProfRec> prof;
@@ -146,6 +147,7 @@ struct Ctx {
 bb_status rt_init(Ctx &c, const bb_model *m, int stages, int microbatches, const bb_opts *o);
 bb_status rt_load_params(Ctx &c, const float *host, size_t n);
 bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats *st);
+bb_status rt_stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt);
 bb_status rt_preempt(Ctx &c, int stage, int at_instr);
 bb_status rt_recover(Ctx &c, bb_recovery_stats *r);
 bb_status rt_read_state(Ctx &c, int stage, int replica, int what, float *host, size_t n);

@@ -180,4 +180,4 @@ def test_adam_matches_oracle():
     torch.cuda.synchronize()
     assert np.abs(host(dp) - p).max() <= 1e-6
     assert np.abs(host(dm) - m).max() <= 1e-6 * np.abs(m).max()
-    assert np.array_equal(w16.cpu(), dp.cpu().to(torch.bfloat16))
+    assert torch.equal(w16.cpu(), dp.cpu().to(torch.bfloat16))

@@ -32,7 +32,10 @@ def _flat_state(p, P, what):
 
 
 def _compare_step(cfg, p, ref, prec, loss, ref_loss, steps):
-    tol = TOL[prec]
+    # After the first Adam step the trajectories differ where sign(g) was not
+    # determined at the path's precision (update ~ lr*sign(g), DESIGN.md
+    # "Tolerances"); later fp32 steps are gated at 10x the check-mode bound.
+    tol = TOL[prec] if (steps == 1 or prec == "bf16") else 10 * TOL[prec]
     lay = ref.lay
     assert abs(loss - ref_loss) <= tol * abs(ref_loss), (loss, ref_loss)
     g = _flat_state(p, cfg.stages, "grads")
