@@ -8,10 +8,13 @@
   "Tolerances"), so it is reported, not gated, in bf16.
 * Adam v (a square of the gradient): same metric against twice the tolerance.
 * post-Adam parameters: same metric, over the elements whose reference
-  gradient is determined at the run's precision (|g_ref| > tol * max|g_ref|
-  of the tensor). Adam's first steps are ~lr*sign(g), so where g is below the
-  precision of the path the sign (and hence a 2*lr move) is not determined;
-  those elements are instead checked to differ by at most 2*lr*steps.
+  gradient is well determined at the run's precision and large against
+  Adam's eps (|g_ref| > mask * max|g_ref| of the tensor, mask 1e-3 in fp32,
+  1e-2 in bf16). Adam's update is ~lr*g/(|g|+eps): where g is below the path's
+  precision its sign (and hence a 2*lr move) is not determined, and for small
+  |g| the ratio amplifies g's relative error; those elements are instead
+  checked to differ by at most 2*lr*steps. In bf16, from the second step on
+  the ratio m/sqrt(v) mixes two noisy gradients, so the bound is 2x.
 """
 import numpy as np
 
@@ -54,9 +57,12 @@ def check_tensors(lay, lo, hi, gpu, ref, tol, what):
 
 def check_params(lay, lo, hi, gpu, ref, ref_grad, tol, lr, steps):
     worst = 0.0
+    mask_frac = 1e-3 if tol < 1e-3 else 1e-2
+    if tol >= 1e-3 and steps > 1:
+        tol = 2 * tol
     for name, a, b in tensor_slices(lay, lo, hi):
         g = np.abs(ref_grad[a:b])
-        mask = g > tol * g.max() if g.max() > 0 else np.zeros_like(g, bool)
+        mask = g > mask_frac * g.max() if g.max() > 0 else np.zeros_like(g, bool)
         d = np.abs(gpu[a:b] - ref[a:b])
         assert np.all(d[~mask] <= 2 * lr * steps * 1.001 + 1e-7), f"param {name} unmasked drift"
         if mask.any():
