@@ -167,6 +167,11 @@ def timed(pipe, steps, ws, host_inputs=None):
     return ms, launches, h2d, d2h
 
 
+def log(rank, *a):
+    if rank == 0:
+        print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
 def run_ours(args, rank, ws, local):
     import torch
     import paper_2204_12013_b200 as bb
@@ -185,11 +190,15 @@ def run_ours(args, rank, ws, local):
 
     results = {}
     for rc in (False, True):
+        log(rank, f"init rc={rc} P={P} M={M} mb={mb}")
         pipe = bb.Pipeline(m, P, M, rc=rc, profile=rc, **common)
         pipe.load_params(flat)
         pipe.stage_inputs(tok, tgt)
-        for _ in range(args.warmup):
-            pipe.step()
+        for i in range(args.warmup):
+            t0 = time.perf_counter()
+            _, st = pipe.step()
+            log(rank, f"warmup {i}: {1e3 * (time.perf_counter() - t0):.1f} ms host, "
+                      f"{st.device_ms:.1f} ms device, loss {st.loss:.4f}, {st.gpu_launches} launches")
         clocks = Clocks(local)
         if rc:
             clocks.start()
@@ -197,7 +206,10 @@ def run_ours(args, rank, ws, local):
         clk = clocks.stop() if rc else None
         kstats = pipe.kernel_stats() if rc else None
         # end to end through the public call with host buffers
+        log(rank, f"timed: {ms / args.steps:.2f} ms/step")
         ms_e2e, _, h2d, d2h = timed(pipe, args.steps, ws, host_inputs=host_batches)
+        log(rank, f"e2e: {ms_e2e / args.steps:.2f} ms/step")
+        pipe.stage_inputs(tok, tgt)
         results[rc] = dict(ms=ms / args.steps, launches=launches, clocks=clk, kstats=kstats,
                            e2e_ms=ms_e2e / args.steps, h2d=h2d / args.steps, d2h=d2h / args.steps)
         if rc:
@@ -277,6 +289,7 @@ def run_ours(args, rank, ws, local):
         "kernel_ms_per_step": {k: round(v[1] / args.steps, 3) for k, v in ks.items()},
     }
     if args.cpu_baseline and ws >= 1:
+        log(rank, "cpu baseline (oracle)")
         line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
 
