@@ -10,14 +10,26 @@ cudaError_t attention_simt_bwd(bool bf16, int B, int S, int H, int nh, bool caus
                                const void *qkv, const void *o, const float *lse,
                                const void *dout, void *dqkv, float *scratch, cudaStream_t s);
 
+bool attention_tc_supported(int H, int nh);
+cudaError_t attention_tc_fwd(int B, int S, int H, int nh, bool causal, const void *qkv, void *o,
+                             float *lse, cudaStream_t s);
+cudaError_t attention_tc_bwd(int B, int S, int H, int nh, bool causal, const void *qkv,
+                             const void *o, const float *lse, const void *dout, void *dqkv,
+                             float *scratch, cudaStream_t s);
+
+// bf16: tensor-core flash attention (head dim 32/64); fp32 check mode: SIMT.
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s) {
+  if (bf16 && attention_tc_supported(H, nh))
+    return attention_tc_fwd(B, S, H, nh, causal, qkv, o, lse, s);
   return attention_simt_fwd(bf16, B, S, H, nh, causal, qkv, o, lse, s);
 }
 
 cudaError_t attention_bwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           const void *o, const float *lse, const void *dout, void *dqkv,
                           float *scratch, cudaStream_t s) {
+  if (bf16 && attention_tc_supported(H, nh))
+    return attention_tc_bwd(B, S, H, nh, causal, qkv, o, lse, dout, dqkv, scratch, s);
   return attention_simt_bwd(bf16, B, S, H, nh, causal, qkv, o, lse, dout, dqkv, scratch, s);
 }
 
