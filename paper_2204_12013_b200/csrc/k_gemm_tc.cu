@@ -112,15 +112,85 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Pair epilogue: columns n, n+1 of row m (n even; N, ldc even in every use).
+__device__ __forceinline__ void epi_store2(const Gemm &g, int m, int n, float a0, float a1) {
+  const size_t idx = (size_t)m * g.ldc + n;
+  const bool two = n + 1 < g.N;
+  auto ld2 = [&](const void *p) -> float2 {
+    const __nv_bfloat16 *q = reinterpret_cast<const __nv_bfloat16 *>(p);
+    if (two) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(q));
+    return make_float2(__bfloat162float(q[0]), 0.f);
+  };
+  auto st2 = [&](void *p, float x, float y) {
+    __nv_bfloat16 *q = reinterpret_cast<__nv_bfloat16 *>(p);
+    if (two)
+      *reinterpret_cast<__nv_bfloat162 *>(q) = __floats2bfloat162_rn(x, y);
+    else
+      q[0] = __float2bfloat16_rn(x);
+  };
+  __nv_bfloat16 *C = reinterpret_cast<__nv_bfloat16 *>(g.C);
+  switch (g.epi) {
+    case EPI_STORE: st2(C + idx, a0, a1); break;
+    case EPI_BIAS: {
+      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
+      st2(C + idx, a0 + b.x, a1 + b.y);
+      break;
+    }
+    case EPI_BIAS_RES: {
+      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
+      const float2 r = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.res) + idx);
+      st2(C + idx, a0 + b.x + r.x, a1 + b.y + r.y);
+      break;
+    }
+    case EPI_BIAS_GELU: {
+      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
+      const float p0 = a0 + b.x, p1 = a1 + b.y;
+      st2(reinterpret_cast<__nv_bfloat16 *>(g.aux) + idx, p0, p1);
+      st2(C + idx, gelu_f(p0), gelu_f(p1));
+      break;
+    }
+    case EPI_GELU_BWD: {
+      const float2 p = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.aux) + idx);
+      st2(C + idx, a0 * gelu_grad_f(p.x), a1 * gelu_grad_f(p.y));
+      break;
+    }
+    case EPI_ACC_F32: {
+      float *Cf = reinterpret_cast<float *>(g.C) + idx;
+      if (two) {
+        float2 c = *reinterpret_cast<float2 *>(Cf);
+        c.x += a0;
+        c.y += a1;
+        *reinterpret_cast<float2 *>(Cf) = c;
+      } else {
+        Cf[0] += a0;
+      }
+      break;
+    }
+    case EPI_STORE_F32: {
+      float *Cf = reinterpret_cast<float *>(g.C) + idx;
+      if (two)
+        *reinterpret_cast<float2 *>(Cf) = make_float2(a0, a1);
+      else
+        Cf[0] = a0;
+      break;
+    }
+  }
+}
+
 template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_LD = 65;                       // floats per staged row (padded)
+  static constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;   // 4 epilogue warps x 32 x 64 fp32
+  static constexpr int BYTES = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Persistent: CTA b processes output tiles b, b + gridDim.x, ... (N-fastest
+// raster so consecutive CTAs share the A slab in L2). Two TMEM accumulators
+// (2 x BN columns) let the epilogue of tile j overlap the MMAs of tile j+1.
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -130,23 +200,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gbase = smem_raw + (base - raw);
-  const uint32_t bars = base + L::STAGES * L::STAGE;
-  // barriers: full[STAGES], empty[STAGES], tmem_full; then the TMEM address
+  float *epi_smem = reinterpret_cast<float *>(gbase + L::STAGES * L::STAGE);
+  const uint32_t bars = base + L::STAGES * L::STAGE + L::EPI_BYTES;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (L::STAGES + s); };
-  const uint32_t done_bar = bars + 8u * (2 * L::STAGES);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::STAGES * L::STAGE + 8 * (2 * L::STAGES + 1));
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * L::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * L::STAGES + 2 + a); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::STAGES * L::STAGE + L::EPI_BYTES +
+                                                     8 * (2 * L::STAGES + 4));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (g.K + BK - 1) / BK;
+  const int tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM - 1) / BM;
+  const int tiles = tiles_n * tiles_m;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    mbar_init(done_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 4);   // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -154,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(BN));
+                 "n"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -165,29 +241,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % L::STAGES;
-        const uint32_t ph = (kb / L::STAGES) & 1;
-        mbar_wait(empty_bar(s), ph ^ 1);
-        const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
         const int na = g.a_mn ? min(BM / 64, (g.M - m0 + 63) / 64) : 1;
         const int nb = g.b_mn ? min(BN / 64, (g.N - n0 + 63) / 64) : 1;
-        mbar_expect_tx(full_bar(s), (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
-                                        (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES));
-        const int k0 = kb * BK;
-        if (!g.a_mn) {
-          tma_load_2d(sa, &map_a, full_bar(s), k0, m0);
-        } else {
-          for (int j = 0; j < na; ++j)
-            tma_load_2d(sa + j * 64 * BK * 2, &map_a, full_bar(s), m0 + 64 * j, k0);
-        }
-        if (!g.b_mn) {
-          tma_load_2d(sb, &map_b, full_bar(s), k0, n0);
-        } else {
-          for (int j = 0; j < nb; ++j)
-            tma_load_2d(sb + j * 64 * BK * 2, &map_b, full_bar(s), n0 + 64 * j, k0);
+        const uint32_t bytes = (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
+                               (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % L::STAGES;
+          const uint32_t ph = (it / L::STAGES) & 1;
+          mbar_wait(empty_bar(s), ph ^ 1);
+          const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
+          mbar_expect_tx(full_bar(s), bytes);
+          const int k0 = kb * BK;
+          if (!g.a_mn) {
+            tma_load_2d(sa, &map_a, full_bar(s), k0, m0);
+          } else {
+            for (int j = 0; j < na; ++j)
+              tma_load_2d(sa + j * 64 * BK * 2, &map_a, full_bar(s), m0 + 64 * j, k0);
+          }
+          if (!g.b_mn) {
+            tma_load_2d(sb, &map_b, full_bar(s), k0, n0);
+          } else {
+            for (int j = 0; j < nb; ++j)
+              tma_load_2d(sb + j * 64 * BK * 2, &map_b, full_bar(s), n0 + 64 * j, k0);
+          }
         }
       }
     }
@@ -195,50 +276,76 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- MMA issuer
       const uint32_t idesc = instr_desc(BN, g.a_mn, g.b_mn);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % L::STAGES;
-        const uint32_t ph = (kb / L::STAGES) & 1;
-        mbar_wait(full_bar(s), ph);
+      int it = 0, j = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+        const int acc = j & 1;
+        mbar_wait(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % L::STAGES;
+          const uint32_t ph = (it / L::STAGES) & 1;
+          mbar_wait(full_bar(s), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          // K-major: +32 B per 16-element K step inside the 128B swizzle row;
-          // MN-major: +16 rows (2 KB) per K step, 64-element MN chunks 8 KB apart.
-          const uint64_t da = g.a_mn ? smem_desc(sa + kk * 2048, 64 * BK * 2, 1024)
-                                     : smem_desc(sa + kk * 32, 16, 1024);
-          const uint64_t db = g.b_mn ? smem_desc(sb + kk * 2048, 64 * BK * 2, 1024)
-                                     : smem_desc(sb + kk * 32, 16, 1024);
-          mma_bf16(tmem, da, db, idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major: +32 B per 16-element K step inside the 128B swizzle row;
+            // MN-major: +16 rows (2 KB) per K step, 64-element MN chunks 8 KB apart.
+            const uint64_t da = g.a_mn ? smem_desc(sa + kk * 2048, 64 * BK * 2, 1024)
+                                       : smem_desc(sa + kk * 32, 16, 1024);
+            const uint64_t db = g.b_mn ? smem_desc(sb + kk * 2048, 64 * BK * 2, 1024)
+                                       : smem_desc(sb + kk * 32, 16, 1024);
+            mma_bf16(d, da, db, idesc, (kb | kk) != 0);
+          }
+          mma_commit(empty_bar(s));
         }
-        mma_commit(empty_bar(s));
+        mma_commit(tfull_bar(acc));
       }
-      mma_commit(done_bar);
     }
   } else {
-    // ---------------- epilogue (warps 2..5)
-    mbar_wait(done_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---------------- epilogue (warps 2..5): TMEM -> regs -> smem -> coalesced rows
     const int q = warp % 4;               // TMEM lane quarter this warp may read
-    const int row = m0 + q * 32 + lane;
+    float *stage = epi_smem + (warp - 2) * 32 * L::EPI_LD;
+    int j = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      const int acc = j & 1;
+      mbar_wait(tfull_bar(acc), (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int ncols = min(BN, g.N - n0);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
-      if (row < g.M) {
+      for (int c = 0; c < ncols; c += 64) {
+        float v[32];
+        const uint32_t ta = tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c;
+        tmem_ld32(ta, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + c + j;
-          if (n < g.N) epi_store<__nv_bfloat16>(g, row, n, v[j]);
+        for (int i = 0; i < 32; ++i) stage[lane * L::EPI_LD + i] = v[i];
+        tmem_ld32(ta + 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[lane * L::EPI_LD + 32 + i] = v[i];
+        __syncwarp();
+        const int n = n0 + c + 2 * lane;
+        if (n < g.N) {
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            const int row = m0 + q * 32 + i;
+            if (row < g.M)
+              epi_store2(g, row, n, stage[i * L::EPI_LD + 2 * lane],
+                         stage[i * L::EPI_LD + 2 * lane + 1]);
+          }
         }
+        __syncwarp();
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar(acc)) : "memory");
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
   }
 }
 
@@ -289,7 +396,14 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = tiles < sms ? tiles : sms;
   gemm_tc_kernel<BN><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g);
   ++g_launches;
   return cudaGetLastError();
