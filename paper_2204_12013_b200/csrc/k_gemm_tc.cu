@@ -112,67 +112,63 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Pair epilogue: columns n, n+1 of row m (n even; N, ldc even in every use).
-__device__ __forceinline__ void epi_store2(const Gemm &g, int m, int n, float a0, float a1) {
-  const size_t idx = (size_t)m * g.ldc + n;
-  const bool two = n + 1 < g.N;
-  auto ld2 = [&](const void *p) -> float2 {
-    const __nv_bfloat16 *q = reinterpret_cast<const __nv_bfloat16 *>(p);
-    if (two) return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(q));
-    return make_float2(__bfloat162float(q[0]), 0.f);
-  };
-  auto st2 = [&](void *p, float x, float y) {
-    __nv_bfloat16 *q = reinterpret_cast<__nv_bfloat16 *>(p);
-    if (two)
-      *reinterpret_cast<__nv_bfloat162 *>(q) = __floats2bfloat162_rn(x, y);
-    else
-      q[0] = __float2bfloat16_rn(x);
-  };
-  __nv_bfloat16 *C = reinterpret_cast<__nv_bfloat16 *>(g.C);
-  switch (g.epi) {
-    case EPI_STORE: st2(C + idx, a0, a1); break;
-    case EPI_BIAS: {
-      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
-      st2(C + idx, a0 + b.x, a1 + b.y);
-      break;
-    }
-    case EPI_BIAS_RES: {
-      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
-      const float2 r = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.res) + idx);
-      st2(C + idx, a0 + b.x + r.x, a1 + b.y + r.y);
-      break;
-    }
-    case EPI_BIAS_GELU: {
-      const float2 b = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n);
+// Epilogue over one staged 32-row x 64-column chunk: lane l owns columns
+// n = n0 + 2l, n+1 of rows m0..m0+31 (all row operands are loaded before any
+// store so the 32 row loads are in flight together). N, ldc are even (checked
+// by gemm_tc_supported), so every pair is fully in or out.
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int ld_stage, int m0,
+                                          int n) {
+  if (n >= g.N) return;
+  const int rows = min(32, g.M - m0);
+  float2 b = make_float2(0.f, 0.f);
+  if (EPI == EPI_BIAS || EPI == EPI_BIAS_RES || EPI == EPI_BIAS_GELU)
+    b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(
+        reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n));
+  uint32_t pre[32];
+  float2 pref[32];
+  if (EPI == EPI_BIAS_RES || EPI == EPI_GELU_BWD) {
+    const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(
+        EPI == EPI_BIAS_RES ? g.res : g.aux);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      pre[i] = i < rows ? *reinterpret_cast<const uint32_t *>(src + (size_t)(m0 + i) * g.ldc + n)
+                        : 0u;
+  }
+  if (EPI == EPI_ACC_F32) {
+    const float *src = reinterpret_cast<const float *>(g.C);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      pref[i] = i < rows ? *reinterpret_cast<const float2 *>(src + (size_t)(m0 + i) * g.ldc + n)
+                         : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i >= rows) break;
+    const size_t idx = (size_t)(m0 + i) * g.ldc + n;
+    float a0 = stage[i * ld_stage + (n & 63)], a1 = stage[i * ld_stage + (n & 63) + 1];
+    __nv_bfloat162 *C = reinterpret_cast<__nv_bfloat162 *>(
+        reinterpret_cast<__nv_bfloat16 *>(g.C) + idx);
+    if (EPI == EPI_STORE) {
+      *C = __floats2bfloat162_rn(a0, a1);
+    } else if (EPI == EPI_BIAS) {
+      *C = __floats2bfloat162_rn(a0 + b.x, a1 + b.y);
+    } else if (EPI == EPI_BIAS_RES) {
+      const float2 r = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
+      *C = __floats2bfloat162_rn(a0 + b.x + r.x, a1 + b.y + r.y);
+    } else if (EPI == EPI_BIAS_GELU) {
       const float p0 = a0 + b.x, p1 = a1 + b.y;
-      st2(reinterpret_cast<__nv_bfloat16 *>(g.aux) + idx, p0, p1);
-      st2(C + idx, gelu_f(p0), gelu_f(p1));
-      break;
-    }
-    case EPI_GELU_BWD: {
-      const float2 p = ld2(reinterpret_cast<const __nv_bfloat16 *>(g.aux) + idx);
-      st2(C + idx, a0 * gelu_grad_f(p.x), a1 * gelu_grad_f(p.y));
-      break;
-    }
-    case EPI_ACC_F32: {
-      float *Cf = reinterpret_cast<float *>(g.C) + idx;
-      if (two) {
-        float2 c = *reinterpret_cast<float2 *>(Cf);
-        c.x += a0;
-        c.y += a1;
-        *reinterpret_cast<float2 *>(Cf) = c;
-      } else {
-        Cf[0] += a0;
-      }
-      break;
-    }
-    case EPI_STORE_F32: {
-      float *Cf = reinterpret_cast<float *>(g.C) + idx;
-      if (two)
-        *reinterpret_cast<float2 *>(Cf) = make_float2(a0, a1);
-      else
-        Cf[0] = a0;
-      break;
+      *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(g.aux) + idx) =
+          __floats2bfloat162_rn(p0, p1);
+      *C = __floats2bfloat162_rn(gelu_f(p0), gelu_f(p1));
+    } else if (EPI == EPI_GELU_BWD) {
+      const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
+      *C = __floats2bfloat162_rn(a0 * gelu_grad_f(p.x), a1 * gelu_grad_f(p.y));
+    } else if (EPI == EPI_ACC_F32) {
+      *reinterpret_cast<float2 *>(reinterpret_cast<float *>(g.C) + idx) =
+          make_float2(pref[i].x + a0, pref[i].y + a1);
+    } else {   // EPI_STORE_F32
+      *reinterpret_cast<float2 *>(reinterpret_cast<float *>(g.C) + idx) = make_float2(a0, a1);
     }
   }
 }
@@ -191,7 +187,7 @@ struct Smem {
 // Persistent: CTA b processes output tiles b, b + gridDim.x, ... (N-fastest
 // raster so consecutive CTAs share the A slab in L2). Two TMEM accumulators
 // (2 x BN columns) let the epilogue of tile j overlap the MMAs of tile j+1.
-template <int BN>
+template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, Gemm g) {
@@ -325,16 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) stage[lane * L::EPI_LD + 32 + i] = v[i];
         __syncwarp();
-        const int n = n0 + c + 2 * lane;
-        if (n < g.N) {
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            const int row = m0 + q * 32 + i;
-            if (row < g.M)
-              epi_store2(g, row, n, stage[i * L::EPI_LD + 2 * lane],
-                         stage[i * L::EPI_LD + 2 * lane + 1]);
-          }
-        }
+        epi_chunk<EPI>(g, stage, L::EPI_LD, m0 + q * 32, n0 + c + 2 * lane);
         __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -379,7 +366,7 @@ bool make_map(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, u
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int EPI>
 cudaError_t launch(const Gemm &g, cudaStream_t s) {
   CUtensorMap ma, mb;
   // K-major operand: tensor {K, rows}, box {64, tile rows}; MN-major: tensor {rows, K}, box {64, 64}
@@ -390,7 +377,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Smem<BN>::BYTES);
     if (e != cudaSuccess) return e;
@@ -404,7 +391,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = tiles < sms ? tiles : sms;
-  gemm_tc_kernel<BN><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g);
+  gemm_tc_kernel<BN, EPI><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -413,15 +400,29 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
 bool gemm_tc_supported(const Gemm &g) {
   if (g.M < 1 || g.N < 1 || g.K < 1) return false;
   if ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) return false;
-  if (g.lda % 8 || g.ldb % 8) return false;
+  if (g.lda % 8 || g.ldb % 8 || g.N % 2 || g.ldc % 2) return false;
+  if (g.epi < EPI_STORE || g.epi > EPI_STORE_F32) return false;
   // MN-major operands need at least one 64-wide box along M / N
   if ((g.a_mn && g.M < 64) || (g.b_mn && g.N < 64)) return false;
   return encode_fn() != nullptr;
 }
 
+template <int BN>
+cudaError_t launch_bn(const Gemm &g, cudaStream_t s) {
+  switch (g.epi) {
+    case EPI_STORE: return launch<BN, EPI_STORE>(g, s);
+    case EPI_BIAS: return launch<BN, EPI_BIAS>(g, s);
+    case EPI_BIAS_RES: return launch<BN, EPI_BIAS_RES>(g, s);
+    case EPI_BIAS_GELU: return launch<BN, EPI_BIAS_GELU>(g, s);
+    case EPI_GELU_BWD: return launch<BN, EPI_GELU_BWD>(g, s);
+    case EPI_ACC_F32: return launch<BN, EPI_ACC_F32>(g, s);
+    default: return launch<BN, EPI_STORE_F32>(g, s);
+  }
+}
+
 cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
-  if (g.N >= 256) return launch<256>(g, s);
-  return launch<128>(g, s);
+  if (g.N >= 256) return launch_bn<256>(g, s);
+  return launch_bn<128>(g, s);
 }
 
 }  // namespace k
