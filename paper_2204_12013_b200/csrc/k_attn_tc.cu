@@ -1,19 +1,24 @@
 // k_attn_tc.cu — bf16 flash attention forward / backward on tensor cores
 // (warp-level mma.sync m16n8k16, fp32 accumulation), head dim 32 or 64.
 //
-// Forward: one CTA = 64 query rows of one (sequence, head), 4 warps x 16 rows;
-// loop over 64-key blocks with an online softmax (P kept in registers as the
-// A operand of P.V), O and the log-sum-exp written at the end.
+// Tiles of 64 keys (or queries) are copied row-major into padded shared
+// memory with cp.async (double-buffered: the next tile streams in while the
+// current one is consumed); MMA operands are read with ldmatrix (.trans where
+// the operand is needed key-major), so no explicit transposes are stored.
+// Forward: one CTA = 128 query rows (8 warps x 16) of one (sequence, head),
+// online softmax in registers, P reused in registers as the A operand of P.V.
 // Backward, deterministic (no atomics): D_i = do_i.o_i;
-// kernel dQ: one CTA per 64 query rows loops over key blocks; kernel dK/dV:
-// one CTA per 64 keys loops over query blocks. P is recomputed from the LSE.
+// dQ pass: CTA per 128 query rows loops over key tiles; dK/dV pass: CTA per
+// 128 keys loops over query tiles. P is recomputed from the saved LSE.
 #include "k_common.cuh"
 
 namespace bb {
 namespace k {
 namespace {
 
-constexpr int BQ = 64, BKV = 64, NT = 128;
+constexpr int BR = 128;          // rows (queries or keys) per CTA, 16 per warp
+constexpr int BT = 64;           // streamed tile (keys or queries)
+constexpr int NW = BR / 16, NT = NW * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
@@ -30,43 +35,99 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t *>(&v);
 }
 
-__device__ __forceinline__ uint32_t ld32(const __nv_bfloat16 *p) {
-  return *reinterpret_cast<const uint32_t *>(p);
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void *p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void *p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
 }
 
-// A-operand fragments of a 16 x D row block (rows r0.., columns = head dims)
-// read straight from global memory (rows >= S give zeros).
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+template <int D> struct Tile { __nv_bfloat16 v[BT][D + 8]; };   // 16B-row padding: no ldsm conflicts
+
+// Async copy of a 64 x D row tile (rows r0.., stride ld elements) into smem;
+// rows >= S are zero-filled.
 template <int D>
-__device__ __forceinline__ void load_rows_frag(uint32_t (&f)[D / 16][4],
-                                               const __nv_bfloat16 *base, size_t ld, int r0,
-                                               int S, int g, int t) {
+__device__ __forceinline__ void tile_async(Tile<D> &t, const __nv_bfloat16 *base, size_t ld,
+                                           int r0, int S) {
+  constexpr int V8 = D / 8;
+  for (int i = threadIdx.x; i < BT * V8; i += NT) {
+    const int r = i / V8, c8 = (i % V8) * 8;
+    const bool ok = r0 + r < S;
+    cp_async16(&t.v[r][c8], base + (size_t)(ok ? r0 + r : 0) * ld + c8, ok);
+  }
+}
+
+// A-operand fragments of a warp's 16 x D row block read from global memory.
+template <int D>
+__device__ __forceinline__ void rows_frag(uint32_t (&f)[D / 16][4], const __nv_bfloat16 *base,
+                                          size_t ld, int r0, int S, int g, int t) {
 #pragma unroll
   for (int ks = 0; ks < D / 16; ++ks) {
     const int c = ks * 16 + 2 * t;
     const bool ok0 = r0 + g < S, ok1 = r0 + g + 8 < S;
-    f[ks][0] = ok0 ? ld32(base + (size_t)(r0 + g) * ld + c) : 0u;
-    f[ks][1] = ok1 ? ld32(base + (size_t)(r0 + g + 8) * ld + c) : 0u;
-    f[ks][2] = ok0 ? ld32(base + (size_t)(r0 + g) * ld + c + 8) : 0u;
-    f[ks][3] = ok1 ? ld32(base + (size_t)(r0 + g + 8) * ld + c + 8) : 0u;
+    const __nv_bfloat16 *p0 = base + (size_t)(r0 + g) * ld + c;
+    const __nv_bfloat16 *p1 = base + (size_t)(r0 + g + 8) * ld + c;
+    f[ks][0] = ok0 ? *reinterpret_cast<const uint32_t *>(p0) : 0u;
+    f[ks][1] = ok1 ? *reinterpret_cast<const uint32_t *>(p1) : 0u;
+    f[ks][2] = ok0 ? *reinterpret_cast<const uint32_t *>(p0 + 8) : 0u;
+    f[ks][3] = ok1 ? *reinterpret_cast<const uint32_t *>(p1 + 8) : 0u;
   }
 }
 
-// Copy a 64 x D tile (rows r0.., stride ld) into row-major smem [64][D+8]
-// and/or transposed smem [D][64+8]. Rows >= S are zero.
+// acc[16 x 64] += A[16 x D] . T^T where T is a 64 x D row tile (B = T rows as
+// columns: "S = Q K^T"). A given as D/16 fragments.
 template <int D>
-__device__ __forceinline__ void load_tile(__nv_bfloat16 (*rowm)[D + 8],
-                                          __nv_bfloat16 (*trans)[BKV + 8],
-                                          const __nv_bfloat16 *base, size_t ld, int r0, int S) {
-  constexpr int V8 = D / 8;
-  for (int i = threadIdx.x; i < 64 * V8; i += NT) {
-    const int r = i / V8, c8 = (i % V8) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r0 + r < S) v = *reinterpret_cast<const uint4 *>(base + (size_t)(r0 + r) * ld + c8);
-    if (rowm) *reinterpret_cast<uint4 *>(&rowm[r][c8]) = v;
-    if (trans) {
-      const __nv_bfloat16 *e = reinterpret_cast<const __nv_bfloat16 *>(&v);
+__device__ __forceinline__ void mma_abt(float (&acc)[8][4], const uint32_t (&a)[D / 16][4],
+                                        const Tile<D> &t, int lane) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) trans[c8 + j][r] = e[j];
+  for (int np = 0; np < 4; ++np) {          // pairs of 8-column groups
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      uint32_t r[4];
+      const int row = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+      const int col = ks * 16 + ((lane >> 3) & 1) * 8;
+      ldsm_x4(r, &t.v[row][col]);
+      mma16816(acc[2 * np], a[ks], r[0], r[1]);
+      mma16816(acc[2 * np + 1], a[ks], r[2], r[3]);
+    }
+  }
+}
+
+// acc[16 x D] += P[16 x 64] . T where T is a 64 x D row tile; P given as the
+// fp32 accumulator layout of a 16 x 64 block (converted to bf16 A fragments).
+template <int D>
+__device__ __forceinline__ void mma_pt(float (&acc)[D / 8][4], const float (&p)[8][4],
+                                       const Tile<D> &t, int lane) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const uint32_t a[4] = {pack_bf16(p[2 * kk][0], p[2 * kk][1]),
+                           pack_bf16(p[2 * kk][2], p[2 * kk][3]),
+                           pack_bf16(p[2 * kk + 1][0], p[2 * kk + 1][1]),
+                           pack_bf16(p[2 * kk + 1][2], p[2 * kk + 1][3])};
+#pragma unroll
+    for (int dp = 0; dp < D / 16; ++dp) {
+      uint32_t r[4];
+      const int row = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int col = dp * 16 + (lane >> 4) * 8;
+      ldsm_x4_t(r, &t.v[row][col]);
+      mma16816(acc[2 * dp], a, r[0], r[1]);
+      mma16816(acc[2 * dp + 1], a, r[2], r[3]);
     }
   }
 }
@@ -77,85 +138,81 @@ __global__ void __launch_bounds__(NT) fa_fwd_kernel(int S, int H, int nh, int ca
                                                     const __nv_bfloat16 *__restrict__ qkv,
                                                     __nv_bfloat16 *__restrict__ o,
                                                     float *__restrict__ lse) {
-  __shared__ __align__(16) __nv_bfloat16 Ks[BKV][D + 8];
-  __shared__ __align__(16) __nv_bfloat16 Vt[D][BKV + 8];
+  __shared__ __align__(128) Tile<D> Ks[2], Vs[2];
   const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, t = lane & 3;
   const size_t ld = 3 * (size_t)H;
   const __nv_bfloat16 *Q = qkv + (size_t)b * S * ld + h * D;
   const __nv_bfloat16 *K = Q + H, *V = Q + 2 * H;
-  const int q0 = qb * BQ + warp * 16;
+  const int q0 = qb * BR + warp * 16;
+  const int nkb_all = (S + BT - 1) / BT;
+  const int nkb = causal ? min(nkb_all, ((qb + 1) * BR + BT - 1) / BT) : nkb_all;
+  tile_async<D>(Ks[0], K, ld, 0, S);
+  tile_async<D>(Vs[0], V, ld, 0, S);
+  cp_commit();
   uint32_t qf[D / 16][4];
-  load_rows_frag<D>(qf, Q, ld, q0, S, g, t);
+  rows_frag<D>(qf, Q, ld, q0, S, g, t);
   const float sl2 = rsqrtf((float)D) * LOG2E;
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
   float acc[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  const int nkb_all = (S + BKV - 1) / BKV;
-  const int nkb = causal ? min(nkb_all, qb + 1) : nkb_all;
   for (int kb = 0; kb < nkb; ++kb) {
+    const int cur = kb & 1;
+    if (kb + 1 < nkb) {
+      tile_async<D>(Ks[cur ^ 1], K, ld, (kb + 1) * BT, S);
+      tile_async<D>(Vs[cur ^ 1], V, ld, (kb + 1) * BT, S);
+    }
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_tile<D>(Ks, nullptr, K, ld, kb * BKV, S);
-    load_tile<D>(nullptr, Vt, V, ld, kb * BKV, S);
-    __syncthreads();
-    float s[8][4];
+    const bool skip = causal && kb * BT > q0 + 15;   // whole tile above this warp's diagonal
+    if (!skip) {
+      float s[8][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+      for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      mma_abt<D>(s, qf, Ks[cur], lane);
+      float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        mma16816(s[nt], qf[ks], ld32(&Ks[nt * 8 + g][ks * 16 + 2 * t]),
-                 ld32(&Ks[nt * 8 + g][ks * 16 + 8 + 2 * t]));
-    }
-    float mx[2] = {-INFINITY, -INFINITY};
+      for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
+          const int row = q0 + g + (e >> 1) * 8;
+          float v = s[nt][e] * sl2;
+          if (key >= S || (causal && key > row)) v = -INFINITY;
+          s[nt][e] = v;
+          mx[e >> 1] = fmaxf(mx[e >> 1], v);
+        }
+      float corr[2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kb * BKV + nt * 8 + 2 * t + (e & 1);
-        const int row = q0 + g + (e >> 1) * 8;
-        float v = s[nt][e] * sl2;
-        if (key >= S || (causal && key > row)) v = -INFINITY;
-        s[nt][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
-      }
-    float corr[2], mnew[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-      mnew[r] = fmaxf(m[r], mx[r]);
-      corr[r] = mnew[r] == -INFINITY ? 1.f : exp2f(m[r] - mnew[r]);
-      m[r] = mnew[r];
-      l[r] *= corr[r];
-    }
-#pragma unroll
-    for (int i = 0; i < D / 8; ++i) {
-      acc[i][0] *= corr[0];
-      acc[i][1] *= corr[0];
-      acc[i][2] *= corr[1];
-      acc[i][3] *= corr[1];
-    }
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float mr = m[e >> 1];
-        const float p = mr == -INFINITY ? 0.f : exp2f(s[nt][e] - mr);
-        s[nt][e] = p;
-        l[e >> 1] += p;
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float mn = fmaxf(m[r], mx[r]);
+        corr[r] = mn == -INFINITY ? 1.f : exp2f(m[r] - mn);
+        m[r] = mn;
+        l[r] *= corr[r];
       }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      uint32_t a[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
-                       pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
-                       pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+      for (int i = 0; i < D / 8; ++i) {
+        acc[i][0] *= corr[0];
+        acc[i][1] *= corr[0];
+        acc[i][2] *= corr[1];
+        acc[i][3] *= corr[1];
+      }
 #pragma unroll
-      for (int dn = 0; dn < D / 8; ++dn)
-        mma16816(acc[dn], a, ld32(&Vt[dn * 8 + g][kk * 16 + 2 * t]),
-                 ld32(&Vt[dn * 8 + g][kk * 16 + 8 + 2 * t]));
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float mr = m[e >> 1];
+          const float p = mr == -INFINITY ? 0.f : exp2f(s[nt][e] - mr);
+          s[nt][e] = p;
+          l[e >> 1] += p;
+        }
+      mma_pt<D>(acc, s, Vs[cur], lane);
     }
+    __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -176,7 +233,7 @@ __global__ void __launch_bounds__(NT) fa_fwd_kernel(int S, int H, int nh, int ca
   }
 }
 
-// D_i = sum_d do[i,d] * o[i,d]; one warp per row.
+// D_i = sum_d do[i,d] * o[i,d]; one warp per (row, head).
 __global__ void fa_bwd_d_kernel(int R, int S, int H, int nh, const __nv_bfloat16 *__restrict__ o,
                                 const __nv_bfloat16 *__restrict__ dout, float *__restrict__ Dv) {
   const int row = blockIdx.x * 4 + threadIdx.x / 32;   // over B*S*nh
@@ -186,7 +243,11 @@ __global__ void fa_bwd_d_kernel(int R, int S, int H, int nh, const __nv_bfloat16
   const int d = H / nh;
   const size_t off = (size_t)r * H + h * d;
   float s = 0.f;
-  for (int c = lane; c < d; c += 32) s += __bfloat162float(o[off + c]) * __bfloat162float(dout[off + c]);
+  for (int c = 2 * lane; c < d; c += 64) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(o + off + c));
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(dout + off + c));
+    s += a.x * x.x + a.y * x.y;
+  }
   s = warp_sum(s);
   const int b = r / S, i = r % S;
   if (lane == 0) Dv[((size_t)b * nh + h) * S + i] = s;
@@ -200,69 +261,65 @@ __global__ void __launch_bounds__(NT) fa_bwd_dq_kernel(int S, int H, int nh, int
                                                        const float *__restrict__ lse,
                                                        const float *__restrict__ Dv,
                                                        __nv_bfloat16 *__restrict__ dqkv) {
-  __shared__ __align__(16) __nv_bfloat16 Ks[BKV][D + 8];
-  __shared__ __align__(16) __nv_bfloat16 Kt[D][BKV + 8];
-  __shared__ __align__(16) __nv_bfloat16 Vs[BKV][D + 8];
+  __shared__ __align__(128) Tile<D> Ks[2], Vs[2];
   const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, t = lane & 3;
   const size_t ld = 3 * (size_t)H;
   const __nv_bfloat16 *Q = qkv + (size_t)b * S * ld + h * D;
   const __nv_bfloat16 *K = Q + H, *V = Q + 2 * H;
   const __nv_bfloat16 *dO = dout + (size_t)b * S * H + h * D;
-  const int q0 = qb * BQ + warp * 16;
+  const int q0 = qb * BR + warp * 16;
+  const int nkb_all = (S + BT - 1) / BT;
+  const int nkb = causal ? min(nkb_all, ((qb + 1) * BR + BT - 1) / BT) : nkb_all;
+  tile_async<D>(Ks[0], K, ld, 0, S);
+  tile_async<D>(Vs[0], V, ld, 0, S);
+  cp_commit();
   uint32_t qf[D / 16][4], df[D / 16][4];
-  load_rows_frag<D>(qf, Q, ld, q0, S, g, t);
-  load_rows_frag<D>(df, dO, H, q0, S, g, t);
+  rows_frag<D>(qf, Q, ld, q0, S, g, t);
+  rows_frag<D>(df, dO, H, q0, S, g, t);
   const float scale = rsqrtf((float)D), sl2 = scale * LOG2E;
   float lrow[2], drow[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int row = q0 + g + r * 8;
-    const size_t ri = ((size_t)b * nh + h) * S + min(row, S - 1);
+    const int row = min(q0 + g + r * 8, S - 1);
+    const size_t ri = ((size_t)b * nh + h) * S + row;
     lrow[r] = lse[ri] * LOG2E;
     drow[r] = Dv[ri];
   }
   float acc[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  const int nkb_all = (S + BKV - 1) / BKV;
-  const int nkb = causal ? min(nkb_all, qb + 1) : nkb_all;
   for (int kb = 0; kb < nkb; ++kb) {
-    __syncthreads();
-    load_tile<D>(Ks, Kt, K, ld, kb * BKV, S);
-    load_tile<D>(Vs, nullptr, V, ld, kb * BKV, S);
-    __syncthreads();
-    float s[8][4], dp[8][4];
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) s[nt][e] = dp[nt][e] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        mma16816(s[nt], qf[ks], ld32(&Ks[nt * 8 + g][ks * 16 + 2 * t]),
-                 ld32(&Ks[nt * 8 + g][ks * 16 + 8 + 2 * t]));
-        mma16816(dp[nt], df[ks], ld32(&Vs[nt * 8 + g][ks * 16 + 2 * t]),
-                 ld32(&Vs[nt * 8 + g][ks * 16 + 8 + 2 * t]));
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int key = kb * BKV + nt * 8 + 2 * t + (e & 1);
-        const int row = q0 + g + (e >> 1) * 8;
-        float p = exp2f(s[nt][e] * sl2 - lrow[e >> 1]);
-        if (key >= S || row >= S || (causal && key > row)) p = 0.f;
-        s[nt][e] = p * (dp[nt][e] - drow[e >> 1]);   // dS
-      }
+    const int cur = kb & 1;
+    if (kb + 1 < nkb) {
+      tile_async<D>(Ks[cur ^ 1], K, ld, (kb + 1) * BT, S);
+      tile_async<D>(Vs[cur ^ 1], V, ld, (kb + 1) * BT, S);
     }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const bool skip = causal && kb * BT > q0 + 15;
+    if (!skip) {
+      float s[8][4], dp[8][4];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      uint32_t a[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]), pack_bf16(s[2 * kk][2], s[2 * kk][3]),
-                       pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
-                       pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int dn = 0; dn < D / 8; ++dn)
-        mma16816(acc[dn], a, ld32(&Kt[dn * 8 + g][kk * 16 + 2 * t]),
-                 ld32(&Kt[dn * 8 + g][kk * 16 + 8 + 2 * t]));
+        for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+      mma_abt<D>(s, qf, Ks[cur], lane);
+      mma_abt<D>(dp, df, Vs[cur], lane);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
+          const int row = q0 + g + (e >> 1) * 8;
+          float p = exp2f(s[nt][e] * sl2 - lrow[e >> 1]);
+          if (key >= S || row >= S || (causal && key > row)) p = 0.f;
+          s[nt][e] = p * (dp[nt][e] - drow[e >> 1]);   // dS
+        }
+      mma_pt<D>(acc, s, Ks[cur], lane);                // dQ += dS . K
     }
+    __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -284,79 +341,69 @@ __global__ void __launch_bounds__(NT) fa_bwd_dkv_kernel(int S, int H, int nh, in
                                                         const float *__restrict__ lse,
                                                         const float *__restrict__ Dv,
                                                         __nv_bfloat16 *__restrict__ dqkv) {
-  __shared__ __align__(16) __nv_bfloat16 Qs[BQ][D + 8];
-  __shared__ __align__(16) __nv_bfloat16 Qt[D][BQ + 8];
-  __shared__ __align__(16) __nv_bfloat16 Ds[BQ][D + 8];
-  __shared__ __align__(16) __nv_bfloat16 Dt[D][BQ + 8];
-  __shared__ float ls[BQ], dsv[BQ];
+  __shared__ __align__(128) Tile<D> Qs[2], Os[2];
+  __shared__ float ls[2][BT], dsv[2][BT];
   const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, t = lane & 3;
   const size_t ld = 3 * (size_t)H;
   const __nv_bfloat16 *Q = qkv + (size_t)b * S * ld + h * D;
   const __nv_bfloat16 *K = Q + H, *V = Q + 2 * H;
   const __nv_bfloat16 *dO = dout + (size_t)b * S * H + h * D;
-  const int k0 = kb * BKV + warp * 16;
+  const int k0 = kb * BR + warp * 16;
+  const int nqb = (S + BT - 1) / BT;
+  const int qb0 = causal ? (kb * BR) / BT : 0;
+  auto stage = [&](int buf, int qb) {
+    tile_async<D>(Qs[buf], Q, ld, qb * BT, S);
+    tile_async<D>(Os[buf], dO, H, qb * BT, S);
+    for (int i = threadIdx.x; i < BT; i += NT) {
+      const int q = min(qb * BT + i, S - 1);
+      const size_t ri = ((size_t)b * nh + h) * S + q;
+      ls[buf][i] = lse[ri] * LOG2E;
+      dsv[buf][i] = Dv[ri];
+    }
+  };
+  if (qb0 < nqb) stage(0, qb0);
+  cp_commit();
   uint32_t kf[D / 16][4], vf[D / 16][4];
-  load_rows_frag<D>(kf, K, ld, k0, S, g, t);
-  load_rows_frag<D>(vf, V, ld, k0, S, g, t);
+  rows_frag<D>(kf, K, ld, k0, S, g, t);
+  rows_frag<D>(vf, V, ld, k0, S, g, t);
   const float scale = rsqrtf((float)D), sl2 = scale * LOG2E;
   float dk[D / 8][4], dv[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
-  const int nqb = (S + BQ - 1) / BQ;
-  for (int qb = causal ? kb : 0; qb < nqb; ++qb) {
+  for (int qb = qb0; qb < nqb; ++qb) {
+    const int cur = (qb - qb0) & 1;
+    if (qb + 1 < nqb) stage(cur ^ 1, qb + 1);
+    cp_commit();
+    cp_wait<1>();
     __syncthreads();
-    load_tile<D>(Qs, Qt, Q, ld, qb * BQ, S);
-    load_tile<D>(Ds, Dt, dO, H, qb * BQ, S);
-    for (int i = threadIdx.x; i < BQ; i += NT) {
-      const int q = qb * BQ + i;
-      const size_t ri = ((size_t)b * nh + h) * S + min(q, S - 1);
-      ls[i] = lse[ri] * LOG2E;
-      dsv[i] = Dv[ri];
+    const bool skip = causal && qb * BT + BT - 1 < k0;   // tile entirely before these keys
+    if (!skip) {
+      float p[8][4], dp[8][4];   // transposed: rows = this warp's keys, cols = queries
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[i][e] = dp[i][e] = 0.f;
+      mma_abt<D>(p, kf, Qs[cur], lane);    // S^T = K Q^T
+      mma_abt<D>(dp, vf, Os[cur], lane);   // dP^T = V dO^T
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int qi = nt * 8 + 2 * t + (e & 1);
+          const int q = qb * BT + qi;
+          const int key = k0 + g + (e >> 1) * 8;
+          float pv = exp2f(p[nt][e] * sl2 - ls[cur][qi]);
+          if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
+          p[nt][e] = pv;
+          dp[nt][e] = pv * (dp[nt][e] - dsv[cur][qi]);   // dS^T
+        }
+      mma_pt<D>(dv, p, Os[cur], lane);    // dV += P^T dO
+      mma_pt<D>(dk, dp, Qs[cur], lane);   // dK += dS^T Q
     }
     __syncthreads();
-    float p[8][4], dp[8][4];   // transposed: rows = this warp's keys, cols = queries
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) p[nt][e] = dp[nt][e] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        mma16816(p[nt], kf[ks], ld32(&Qs[nt * 8 + g][ks * 16 + 2 * t]),
-                 ld32(&Qs[nt * 8 + g][ks * 16 + 8 + 2 * t]));
-        mma16816(dp[nt], vf[ks], ld32(&Ds[nt * 8 + g][ks * 16 + 2 * t]),
-                 ld32(&Ds[nt * 8 + g][ks * 16 + 8 + 2 * t]));
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int qi = nt * 8 + 2 * t + (e & 1);
-        const int q = qb * BQ + qi;
-        const int key = k0 + g + (e >> 1) * 8;
-        float pv = exp2f(p[nt][e] * sl2 - ls[qi]);
-        if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
-        p[nt][e] = pv;
-        dp[nt][e] = pv * (dp[nt][e] - dsv[qi]);   // dS^T
-      }
-    }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      uint32_t ap[4] = {pack_bf16(p[2 * kk][0], p[2 * kk][1]), pack_bf16(p[2 * kk][2], p[2 * kk][3]),
-                        pack_bf16(p[2 * kk + 1][0], p[2 * kk + 1][1]),
-                        pack_bf16(p[2 * kk + 1][2], p[2 * kk + 1][3])};
-      uint32_t as[4] = {pack_bf16(dp[2 * kk][0], dp[2 * kk][1]),
-                        pack_bf16(dp[2 * kk][2], dp[2 * kk][3]),
-                        pack_bf16(dp[2 * kk + 1][0], dp[2 * kk + 1][1]),
-                        pack_bf16(dp[2 * kk + 1][2], dp[2 * kk + 1][3])};
-#pragma unroll
-      for (int dn = 0; dn < D / 8; ++dn) {
-        mma16816(dv[dn], ap, ld32(&Dt[dn * 8 + g][kk * 16 + 2 * t]),
-                 ld32(&Dt[dn * 8 + g][kk * 16 + 8 + 2 * t]));
-        mma16816(dk[dn], as, ld32(&Qt[dn * 8 + g][kk * 16 + 2 * t]),
-                 ld32(&Qt[dn * 8 + g][kk * 16 + 8 + 2 * t]));
-      }
-    }
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -377,7 +424,7 @@ __global__ void __launch_bounds__(NT) fa_bwd_dkv_kernel(int S, int H, int nh, in
 template <int D>
 cudaError_t fwd_d(int B, int S, int H, int nh, bool causal, const void *qkv, void *o, float *lse,
                   cudaStream_t s) {
-  dim3 grid((S + BQ - 1) / BQ, nh, B);
+  dim3 grid((S + BR - 1) / BR, nh, B);
   fa_fwd_kernel<D><<<grid, NT, 0, s>>>(S, H, nh, causal, (const __nv_bfloat16 *)qkv,
                                        (__nv_bfloat16 *)o, lse);
   ++g_launches;
@@ -390,7 +437,7 @@ cudaError_t bwd_d(int B, int S, int H, int nh, bool causal, const void *qkv, con
   const int rows = B * S * nh;
   fa_bwd_d_kernel<<<(rows + 3) / 4, 128, 0, s>>>(B * S, S, H, nh, (const __nv_bfloat16 *)o,
                                                  (const __nv_bfloat16 *)dout, scratch);
-  dim3 grid((S + BQ - 1) / BQ, nh, B);
+  dim3 grid((S + BR - 1) / BR, nh, B);
   fa_bwd_dq_kernel<D><<<grid, NT, 0, s>>>(S, H, nh, causal, (const __nv_bfloat16 *)qkv,
                                           (const __nv_bfloat16 *)dout, lse, scratch,
                                           (__nv_bfloat16 *)dqkv);
