@@ -26,7 +26,8 @@ namespace k {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                 // 2 per TMEM lane quarter
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -112,41 +113,48 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Epilogue over one staged 32-row x 64-column chunk: lane l owns columns
-// n = n0 + 2l, n+1 of rows m0..m0+31 (all row operands are loaded before any
-// store so the 32 row loads are in flight together). N, ldc are even (checked
-// by gemm_tc_supported), so every pair is fully in or out.
+// Epilogue over one staged 32-row x 32-column chunk: lane l owns the column
+// pair n = n0 + 2(l % 16), n+1 of rows m0 + 2i + l/16 (i < 16), so each warp
+// store covers two 64-byte row segments. All row operands are loaded before
+// any store so the 16 row loads are in flight together. N, ldc are even
+// (gemm_tc_supported), so every pair is fully in or out.
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int ld_stage, int m0,
-                                          int n) {
+                                          int n0, int lane) {
+  const int n = n0 + 2 * (lane & 15);
   if (n >= g.N) return;
-  const int rows = min(32, g.M - m0);
+  const int rsub = lane >> 4;
   float2 b = make_float2(0.f, 0.f);
   if (EPI == EPI_BIAS || EPI == EPI_BIAS_RES || EPI == EPI_BIAS_GELU)
     b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(
         reinterpret_cast<const __nv_bfloat16 *>(g.bias) + n));
-  uint32_t pre[32];
-  float2 pref[32];
+  uint32_t pre[16];
+  float2 pref[16];
   if (EPI == EPI_BIAS_RES || EPI == EPI_GELU_BWD) {
     const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(
         EPI == EPI_BIAS_RES ? g.res : g.aux);
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      pre[i] = i < rows ? *reinterpret_cast<const uint32_t *>(src + (size_t)(m0 + i) * g.ldc + n)
-                        : 0u;
+    for (int i = 0; i < 16; ++i) {
+      const int row = m0 + 2 * i + rsub;
+      pre[i] = row < g.M ? *reinterpret_cast<const uint32_t *>(src + (size_t)row * g.ldc + n) : 0u;
+    }
   }
   if (EPI == EPI_ACC_F32) {
     const float *src = reinterpret_cast<const float *>(g.C);
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      pref[i] = i < rows ? *reinterpret_cast<const float2 *>(src + (size_t)(m0 + i) * g.ldc + n)
-                         : make_float2(0.f, 0.f);
+    for (int i = 0; i < 16; ++i) {
+      const int row = m0 + 2 * i + rsub;
+      pref[i] = row < g.M ? *reinterpret_cast<const float2 *>(src + (size_t)row * g.ldc + n)
+                          : make_float2(0.f, 0.f);
+    }
   }
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    if (i >= rows) break;
-    const size_t idx = (size_t)(m0 + i) * g.ldc + n;
-    float a0 = stage[i * ld_stage + (n & 63)], a1 = stage[i * ld_stage + (n & 63) + 1];
+  for (int i = 0; i < 16; ++i) {
+    const int r = 2 * i + rsub, row = m0 + r;
+    if (row >= g.M) break;
+    const size_t idx = (size_t)row * g.ldc + n;
+    const float a0 = stage[r * ld_stage + 2 * (lane & 15)];
+    const float a1 = stage[r * ld_stage + 2 * (lane & 15) + 1];
     __nv_bfloat162 *C = reinterpret_cast<__nv_bfloat162 *>(
         reinterpret_cast<__nv_bfloat16 *>(g.C) + idx);
     if (EPI == EPI_STORE) {
@@ -154,16 +162,16 @@ __device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int
     } else if (EPI == EPI_BIAS) {
       *C = __floats2bfloat162_rn(a0 + b.x, a1 + b.y);
     } else if (EPI == EPI_BIAS_RES) {
-      const float2 r = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
-      *C = __floats2bfloat162_rn(a0 + b.x + r.x, a1 + b.y + r.y);
+      const float2 rr = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
+      *C = __floats2bfloat162_rn(a0 + b.x + rr.x, a1 + b.y + rr.y);
     } else if (EPI == EPI_BIAS_GELU) {
       const float p0 = a0 + b.x, p1 = a1 + b.y;
       *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(g.aux) + idx) =
           __floats2bfloat162_rn(p0, p1);
-      *C = __floats2bfloat162_rn(gelu_f(p0), gelu_f(p1));
+      *C = __floats2bfloat162_rn(gelu_fast(p0), gelu_fast(p1));
     } else if (EPI == EPI_GELU_BWD) {
-      const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
-      *C = __floats2bfloat162_rn(a0 * gelu_grad_f(p.x), a1 * gelu_grad_f(p.y));
+      const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&pre[i]));
+      *C = __floats2bfloat162_rn(a0 * gelu_grad_fast(pp.x), a1 * gelu_grad_fast(pp.y));
     } else if (EPI == EPI_ACC_F32) {
       *reinterpret_cast<float2 *>(reinterpret_cast<float *>(g.C) + idx) =
           make_float2(pref[i].x + a0, pref[i].y + a1);
@@ -179,8 +187,8 @@ struct Smem {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int EPI_LD = 65;                       // floats per staged row (padded)
-  static constexpr int EPI_BYTES = 4 * 32 * EPI_LD * 4;   // 4 epilogue warps x 32 x 64 fp32
+  static constexpr int EPI_LD = 33;                       // floats per staged row (padded)
+  static constexpr int EPI_BYTES = kEpiWarps * 32 * EPI_LD * 4;   // per warp 32 x 32 fp32
   static constexpr int BYTES = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 4);   // one arrive per epilogue warp
+      mbar_init(tempty_bar(a), kEpiWarps);   // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- epilogue (warps 2..5): TMEM -> regs -> smem -> coalesced rows
     const int q = warp % 4;               // TMEM lane quarter this warp may read
+    const int half = (warp - 2) / 4;      // which half of the tile's columns
     float *stage = epi_smem + (warp - 2) * 32 * L::EPI_LD;
     int j = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
@@ -311,17 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int ncols = min(BN, g.N - n0);
 #pragma unroll 1
-      for (int c = 0; c < ncols; c += 64) {
+      for (int c = half * (BN / 2); c < min(ncols, (half + 1) * (BN / 2)); c += 32) {
         float v[32];
-        const uint32_t ta = tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c;
-        tmem_ld32(ta, v);
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) stage[lane * L::EPI_LD + i] = v[i];
-        tmem_ld32(ta + 32, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) stage[lane * L::EPI_LD + 32 + i] = v[i];
         __syncwarp();
-        epi_chunk<EPI>(g, stage, L::EPI_LD, m0 + q * 32, n0 + c + 2 * lane);
+        epi_chunk<EPI>(g, stage, L::EPI_LD, m0 + q * 32, n0 + c, lane);
         __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
