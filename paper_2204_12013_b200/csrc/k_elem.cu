@@ -101,6 +101,180 @@ __global__ void colreduce_final_kernel(int chunks, int N, const float *__restric
   out[n] += s;
 }
 
+// --------------------------------------- vectorized variants (H % 8 == 0)
+// 8 consecutive elements per access: 16 B of bf16 / 32 B of fp32.
+struct V8 { float v[8]; };
+__device__ __forceinline__ V8 ld8(const __nv_bfloat16 *p) {
+  const uint4 u = *reinterpret_cast<const uint4 *>(p);
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+  V8 r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    r.v[2 * i] = f.x;
+    r.v[2 * i + 1] = f.y;
+  }
+  return r;
+}
+__device__ __forceinline__ V8 ld8(const float *p) {
+  const float4 a = *reinterpret_cast<const float4 *>(p), b = *reinterpret_cast<const float4 *>(p + 4);
+  return V8{{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w}};
+}
+__device__ __forceinline__ void st8(__nv_bfloat16 *p, const V8 &x) {
+  uint4 u;
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(x.v[2 * i], x.v[2 * i + 1]);
+  *reinterpret_cast<uint4 *>(p) = u;
+}
+__device__ __forceinline__ void st8(float *p, const V8 &x) {
+  *reinterpret_cast<float4 *>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+  *reinterpret_cast<float4 *>(p + 4) = make_float4(x.v[4], x.v[5], x.v[6], x.v[7]);
+}
+
+constexpr int LN_MAXC = 8;   // chunks of 8 per lane: H <= 2048
+
+// One warp per row, the row kept in registers: a single HBM pass.
+template <typename T>
+__global__ void ln_fwd_vec_kernel(int R, int H, const T *__restrict__ x, const T *__restrict__ g,
+                                  const T *__restrict__ b, T *__restrict__ y,
+                                  float *__restrict__ mean, float *__restrict__ rstd) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const int nc = H / 8;
+  const T *xr = x + (size_t)row * H;
+  V8 v[LN_MAXC];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      v[c] = ld8(xr + 8 * ch);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[c].v[i];
+    }
+  }
+  const float mu = warp_sum(s) / H;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    if (lane + 32 * c < nc) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[c].v[i] - mu;
+        q += d * d;
+      }
+    }
+  }
+  const float rs = rsqrtf(warp_sum(q) / H + LN_EPS);
+  T *yr = y + (size_t)row * H;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      const V8 gg = ld8(g + 8 * ch), bb = ld8(b + 8 * ch);
+      V8 o;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = (v[c].v[i] - mu) * rs * gg.v[i] + bb.v[i];
+      st8(yr + 8 * ch, o);
+    }
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+template <typename T>
+__global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
+                                  const T *__restrict__ x, const float *__restrict__ mean,
+                                  const float *__restrict__ rstd, const T *__restrict__ g,
+                                  const float *__restrict__ dres32, const T *__restrict__ dresT,
+                                  T *__restrict__ dxT, float *__restrict__ dx32) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const int nc = H / 8;
+  const size_t off = (size_t)row * H;
+  const float mu = mean[row], rs = rstd[row];
+  V8 gd[LN_MAXC], xh[LN_MAXC];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      const V8 d = ld8(dy + off + 8 * ch), xx = ld8(x + off + 8 * ch), gg = ld8(g + 8 * ch);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        gd[c].v[i] = d.v[i] * gg.v[i];
+        xh[c].v[i] = (xx.v[i] - mu) * rs;
+        s1 += gd[c].v[i];
+        s2 += gd[c].v[i] * xh[c].v[i];
+      }
+    }
+  }
+  const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
+#pragma unroll
+  for (int c = 0; c < LN_MAXC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      V8 o;
+      V8 r{};
+      if (dres32) r = ld8(dres32 + off + 8 * ch);
+      else if (dresT) r = ld8(dresT + off + 8 * ch);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o.v[i] = rs * (gd[c].v[i] - m1 - xh[c].v[i] * m2) + r.v[i];
+      st8(dxT + off + 8 * ch, o);
+      if (dx32) st8(dx32 + off + 8 * ch, o);
+    }
+  }
+}
+
+// Column reduction, 8 columns per thread: block = 8 warps x 32 lanes covers
+// 256 columns x CRV_ROWS rows (warp w takes rows w, w+8, ...); the 8 warp
+// partials are added in a fixed order through shared memory.
+constexpr int CRV_ROWS = 256;
+template <typename TA, typename T>
+__global__ void __launch_bounds__(256) colreduce_vec_kernel(int mode, int R, int N,
+                                                            const TA *__restrict__ A,
+                                                            const T *__restrict__ X,
+                                                            const float *__restrict__ mean,
+                                                            const float *__restrict__ rstd,
+                                                            float *__restrict__ part) {
+  __shared__ float sh[8][256];   // 8 warps x 256 columns
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = (blockIdx.x * 32 + lane) * 8;
+  const int r0 = blockIdx.y * CRV_ROWS, r1 = min(R, r0 + CRV_ROWS);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (n < N) {
+    for (int r = r0 + warp; r < r1; r += 8) {
+      const size_t idx = (size_t)r * N + n;
+      const V8 a = ld8(A + idx);
+      if (mode == 1) {
+        const V8 xx = ld8(X + idx);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += a.v[i] * ((xx.v[i] - mu) * rs);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += a.v[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sh[warp][lane * 8 + i] = acc[i];
+  __syncthreads();
+  const int c = threadIdx.x;   // 256 columns of this block
+  const int nn = blockIdx.x * 256 + c;
+  if (nn < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += sh[w][c];
+    part[(size_t)blockIdx.y * N + nn] = s;
+  }
+}
+
 // -------------------------------------------------------------- embedding
 template <typename T>
 __global__ void embed_fwd_kernel(int R, int S, int H, const int32_t *__restrict__ tok,
@@ -259,7 +433,14 @@ template <typename T> static T *mp(void *p) { return reinterpret_cast<T *>(p); }
 cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
                           void *y, float *mean, float *rstd, cudaStream_t s) {
   const int grid = (R + 7) / 8;
-  if (bf16)
+  if (H % 8 == 0 && H <= 256 * LN_MAXC) {
+    if (bf16)
+      ln_fwd_vec_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(x),
+          cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(b), mp<__nv_bfloat16>(y), mean, rstd);
+    else
+      ln_fwd_vec_kernel<float><<<grid, 256, 0, s>>>(R, H, cp<float>(x), cp<float>(g),
+                                                    cp<float>(b), mp<float>(y), mean, rstd);
+  } else if (bf16)
     ln_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(x),
         cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(b), mp<__nv_bfloat16>(y), mean, rstd);
   else
@@ -274,7 +455,16 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
                              const float *dres32, const void *dresT, void *dxT, float *dx32,
                              cudaStream_t s) {
   const int grid = (R + 7) / 8;
-  if (bf16)
+  if (H % 8 == 0 && H <= 256 * LN_MAXC) {
+    if (bf16)
+      ln_bwd_vec_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, dy, cp<__nv_bfloat16>(x), mean,
+          rstd, cp<__nv_bfloat16>(g), dres32, cp<__nv_bfloat16>(dresT), mp<__nv_bfloat16>(dxT),
+          dx32);
+    else
+      ln_bwd_vec_kernel<float><<<grid, 256, 0, s>>>(R, H, dy, cp<float>(x), mean, rstd,
+                                                    cp<float>(g), dres32, cp<float>(dresT),
+                                                    mp<float>(dxT), dx32);
+  } else if (bf16)
     ln_bwd_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, dy, cp<__nv_bfloat16>(x), mean,
         rstd, cp<__nv_bfloat16>(g), dres32, cp<__nv_bfloat16>(dresT), mp<__nv_bfloat16>(dxT),
         dx32);
@@ -286,12 +476,28 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
 }
 
 size_t colreduce_partial_floats(int R, int N) {
-  return (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;
+  return (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;   // >= the vectorized kernel's need
 }
 
 cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void *A, const void *X,
                       const float *mean, const float *rstd, float *partial, float *out,
                       cudaStream_t s) {
+  if (N % 8 == 0) {
+    const int chunks = (R + CRV_ROWS - 1) / CRV_ROWS;
+    dim3 grid((N + 255) / 256, chunks);
+    if (bf16 && a_f32)
+      colreduce_vec_kernel<float, __nv_bfloat16><<<grid, 256, 0, s>>>(
+          mode, R, N, cp<float>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+    else if (bf16)
+      colreduce_vec_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
+          mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+    else
+      colreduce_vec_kernel<float, float><<<grid, 256, 0, s>>>(mode, R, N, cp<float>(A),
+                                                              cp<float>(X), mean, rstd, partial);
+    colreduce_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(chunks, N, partial, out);
+    g_launches += 2;
+    return cudaGetLastError();
+  }
   const int chunks = (R + CR_ROWS - 1) / CR_ROWS;
   dim3 grid((N + CR_COLS - 1) / CR_COLS, chunks);
   if (bf16 && a_f32)

@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "k_common.cuh"
@@ -144,7 +145,7 @@ __device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int row = m0 + 2 * i + rsub;
-      pref[i] = row < g.M ? *reinterpret_cast<const float2 *>(src + (size_t)row * g.ldc + n)
+      pref[i] = row < g.M ? __ldcg(reinterpret_cast<const float2 *>(src + (size_t)row * g.ldc + n))
                           : make_float2(0.f, 0.f);
     }
   }
@@ -198,7 +199,8 @@ struct Smem {
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, Gemm g) {
+                   const __grid_constant__ CUtensorMap map_b, Gemm g, int ksplit,
+                   int *__restrict__ flags, int epoch) {
   using L = Smem<BN>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -217,6 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nk = (g.K + BK - 1) / BK;
   const int tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM - 1) / BM;
   const int tiles = tiles_n * tiles_m;
+  // Work unit = (tile, K split). With ksplit > 1 (fp32-accumulating dW only)
+  // the splits of a tile add into C in ascending split order, serialised by a
+  // per-tile flag (epoch * 16 + split): deterministic, and deadlock-free since
+  // every CTA is resident and a unit only waits for a lower-numbered unit.
+  const int units = tiles * ksplit;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
@@ -246,7 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- TMA producer
       int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        const int tile = unit / ksplit, split = unit % ksplit;
+        const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
         const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nb = g.b_mn ? min(BN / 64, (g.N - n0 + 63) / 64) : 1;
         const uint32_t bytes = (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
                                (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
           mbar_wait(empty_bar(s), ph ^ 1);
@@ -281,12 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- MMA issuer
       const uint32_t idesc = instr_desc(BN, g.a_mn, g.b_mn);
       int it = 0, j = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+      for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++j) {
+        const int split = unit % ksplit;
+        const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
         const int acc = j & 1;
         mbar_wait(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
           mbar_wait(full_bar(s), ph);
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        : smem_desc(sa + kk * 32, 16, 1024);
             const uint64_t db = g.b_mn ? smem_desc(sb + kk * 2048, 64 * BK * 2, 1024)
                                        : smem_desc(sb + kk * 32, 16, 1024);
-            mma_bf16(d, da, db, idesc, (kb | kk) != 0);
+            mma_bf16(d, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(empty_bar(s));
         }
@@ -313,11 +324,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) / 4;      // which half of the tile's columns
     float *stage = epi_smem + (warp - 2) * 32 * L::EPI_LD;
     int j = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++j) {
+      const int tile = unit / ksplit, split = unit % ksplit;
       const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
       const int acc = j & 1;
       mbar_wait(tfull_bar(acc), (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (ksplit > 1 && split > 0) {
+        if (threadIdx.x == 64) {
+          const volatile int *f = flags + tile;
+          while (*f != epoch * 16 + split) __nanosleep(64);
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
       const int ncols = min(BN, g.N - n0);
 #pragma unroll 1
       for (int c = half * (BN / 2); c < min(ncols, (half + 1) * (BN / 2)); c += 32) {
@@ -331,6 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar(acc)) : "memory");
+      if (ksplit > 1) {
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (threadIdx.x == 64) *(volatile int *)(flags + tile) = epoch * 16 + split + 1;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -371,6 +396,27 @@ bool make_map(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, u
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Per-launch slice of a device flag ring for serialised split-K; every launch
+// gets a fresh epoch, so flags never need resetting.
+int *split_flags(int n, int *epoch) {
+  static std::mutex mu;
+  static int *ring = nullptr;
+  static int cursor = 0, ep = 0;
+  constexpr int kRing = 1 << 20;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ring) {
+    if (cudaMalloc(&ring, kRing * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(ring, 0, kRing * sizeof(int)) != cudaSuccess) return nullptr;
+  }
+  if (cursor + n > kRing) cursor = 0;
+  int *p = ring + cursor;
+  cursor += n;
+  ep = (ep + 1) & ((1 << 26) - 1);
+  if (ep == 0) ep = 1;
+  *epoch = ep;
+  return p;
+}
+
 template <int BN, int EPI>
 cudaError_t launch(const Gemm &g, cudaStream_t s) {
   CUtensorMap ma, mb;
@@ -395,8 +441,20 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int grid = tiles < sms ? tiles : sms;
-  gemm_tc_kernel<BN, EPI><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g);
+  // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU.
+  const int nk = (g.K + BK - 1) / BK;
+  int ksplit = 1;
+  if (EPI == EPI_ACC_F32 && tiles * 2 <= sms)
+    ksplit = std::max(1, std::min({sms / tiles, nk / 8, 8}));
+  int *flags = nullptr;
+  int epoch = 0;
+  if (ksplit > 1) {
+    flags = split_flags(tiles, &epoch);
+    if (!flags) ksplit = 1;
+  }
+  const int units = tiles * ksplit;
+  const int grid = units < sms ? units : sms;
+  gemm_tc_kernel<BN, EPI><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g, ksplit, flags, epoch);
   ++g_launches;
   return cudaGetLastError();
 }

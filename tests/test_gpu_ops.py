@@ -27,7 +27,8 @@ def rnd(*shape, scale=1.0):
 
 
 GEMM_SHAPES = [(64, 64, 64), (200, 136, 72), (256, 512, 128), (1000, 328, 520), (128, 2304, 768),
-               (130, 50304 // 64, 64), (8, 24, 16), (384, 640, 1000)]
+               (130, 50304 // 64, 64), (8, 24, 16), (384, 640, 1000), (256, 512, 4096),
+               (136, 264, 8200)]
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
