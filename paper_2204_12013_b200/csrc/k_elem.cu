@@ -132,10 +132,12 @@ __device__ __forceinline__ void st8(float *p, const V8 &x) {
   *reinterpret_cast<float4 *>(p + 4) = make_float4(x.v[4], x.v[5], x.v[6], x.v[7]);
 }
 
-constexpr int LN_MAXC = 8;   // chunks of 8 per lane: H <= 2048
+constexpr int LN_MAXC_MAX = 8;   // chunks of 8 per lane: H <= 2048
 
 // One warp per row, the row kept in registers: a single HBM pass.
-template <typename T>
+// LN_MAXC = chunks of 8 elements per lane (compile-time so the row stays in
+// registers; the smallest that covers H keeps occupancy high).
+template <typename T, int LN_MAXC>
 __global__ void ln_fwd_vec_kernel(int R, int H, const T *__restrict__ x, const T *__restrict__ g,
                                   const T *__restrict__ b, T *__restrict__ y,
                                   float *__restrict__ mean, float *__restrict__ rstd) {
@@ -186,7 +188,7 @@ __global__ void ln_fwd_vec_kernel(int R, int H, const T *__restrict__ x, const T
   }
 }
 
-template <typename T>
+template <typename T, int LN_MAXC>
 __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
                                   const T *__restrict__ x, const float *__restrict__ mean,
                                   const float *__restrict__ rstd, const T *__restrict__ g,
@@ -234,7 +236,7 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
 // Column reduction, 8 columns per thread: block = 8 warps x 32 lanes covers
 // 256 columns x CRV_ROWS rows (warp w takes rows w, w+8, ...); the 8 warp
 // partials are added in a fixed order through shared memory.
-constexpr int CRV_ROWS = 256;
+constexpr int CRV_ROWS = 64;
 template <typename TA, typename T>
 __global__ void __launch_bounds__(256) colreduce_vec_kernel(int mode, int R, int N,
                                                             const TA *__restrict__ A,
@@ -433,13 +435,21 @@ template <typename T> static T *mp(void *p) { return reinterpret_cast<T *>(p); }
 cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
                           void *y, float *mean, float *rstd, cudaStream_t s) {
   const int grid = (R + 7) / 8;
-  if (H % 8 == 0 && H <= 256 * LN_MAXC) {
-    if (bf16)
-      ln_fwd_vec_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(x),
-          cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(b), mp<__nv_bfloat16>(y), mean, rstd);
-    else
-      ln_fwd_vec_kernel<float><<<grid, 256, 0, s>>>(R, H, cp<float>(x), cp<float>(g),
-                                                    cp<float>(b), mp<float>(y), mean, rstd);
+  if (H % 8 == 0 && H <= 256 * LN_MAXC_MAX) {
+#define BB_LNF(T, C)                                                                          \
+  ln_fwd_vec_kernel<T, C><<<grid, 256, 0, s>>>(R, H, cp<T>(x), cp<T>(g), cp<T>(b), mp<T>(y), \
+                                               mean, rstd)
+    const int need = (H / 8 + 31) / 32;
+    if (bf16) {
+      if (need <= 2) BB_LNF(__nv_bfloat16, 2);
+      else if (need <= 4) BB_LNF(__nv_bfloat16, 4);
+      else BB_LNF(__nv_bfloat16, 8);
+    } else {
+      if (need <= 2) BB_LNF(float, 2);
+      else if (need <= 4) BB_LNF(float, 4);
+      else BB_LNF(float, 8);
+    }
+#undef BB_LNF
   } else if (bf16)
     ln_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, cp<__nv_bfloat16>(x),
         cp<__nv_bfloat16>(g), cp<__nv_bfloat16>(b), mp<__nv_bfloat16>(y), mean, rstd);
@@ -455,15 +465,21 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
                              const float *dres32, const void *dresT, void *dxT, float *dx32,
                              cudaStream_t s) {
   const int grid = (R + 7) / 8;
-  if (H % 8 == 0 && H <= 256 * LN_MAXC) {
-    if (bf16)
-      ln_bwd_vec_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, dy, cp<__nv_bfloat16>(x), mean,
-          rstd, cp<__nv_bfloat16>(g), dres32, cp<__nv_bfloat16>(dresT), mp<__nv_bfloat16>(dxT),
-          dx32);
-    else
-      ln_bwd_vec_kernel<float><<<grid, 256, 0, s>>>(R, H, dy, cp<float>(x), mean, rstd,
-                                                    cp<float>(g), dres32, cp<float>(dresT),
-                                                    mp<float>(dxT), dx32);
+  if (H % 8 == 0 && H <= 256 * LN_MAXC_MAX) {
+#define BB_LNB(T, C)                                                                          \
+  ln_bwd_vec_kernel<T, C><<<grid, 256, 0, s>>>(R, H, dy, cp<T>(x), mean, rstd, cp<T>(g),     \
+                                               dres32, cp<T>(dresT), mp<T>(dxT), dx32)
+    const int need = (H / 8 + 31) / 32;
+    if (bf16) {
+      if (need <= 2) BB_LNB(__nv_bfloat16, 2);
+      else if (need <= 4) BB_LNB(__nv_bfloat16, 4);
+      else BB_LNB(__nv_bfloat16, 8);
+    } else {
+      if (need <= 2) BB_LNB(float, 2);
+      else if (need <= 4) BB_LNB(float, 4);
+      else BB_LNB(float, 8);
+    }
+#undef BB_LNB
   } else if (bf16)
     ln_bwd_dx_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(R, H, dy, cp<__nv_bfloat16>(x), mean,
         rstd, cp<__nv_bfloat16>(g), dres32, cp<__nv_bfloat16>(dresT), mp<__nv_bfloat16>(dxT),
