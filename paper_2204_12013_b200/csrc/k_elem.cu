@@ -92,13 +92,26 @@ __global__ void colreduce_partial_kernel(int mode, int R, int N, const TA *__res
   part[(size_t)blockIdx.y * N + n] = s;
 }
 
-__global__ void colreduce_final_kernel(int chunks, int N, const float *__restrict__ part,
-                                       float *__restrict__ out) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+// out[n] += sum_c part[c][n]: block = 32 columns x 8 warps; warp w adds
+// chunks w, w+8, ... (lane = column, coalesced), then the 8 warp sums are
+// added in a fixed order.
+__global__ void __launch_bounds__(256) colreduce_final_kernel(int chunks, int N,
+                                                              const float *__restrict__ part,
+                                                              float *__restrict__ out) {
+  __shared__ float sh[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int c = 0; c < chunks; ++c) s += part[(size_t)c * N + n];
-  out[n] += s;
+  if (n < N)
+    for (int c = warp; c < chunks; c += 8) s += part[(size_t)c * N + n];
+  sh[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += sh[w][lane];
+    out[n] += t;
+  }
 }
 
 // --------------------------------------- vectorized variants (H % 8 == 0)
@@ -510,7 +523,7 @@ cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void 
     else
       colreduce_vec_kernel<float, float><<<grid, 256, 0, s>>>(mode, R, N, cp<float>(A),
                                                               cp<float>(X), mean, rstd, partial);
-    colreduce_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(chunks, N, partial, out);
+    colreduce_final_kernel<<<(N + 31) / 32, 256, 0, s>>>(chunks, N, partial, out);
     g_launches += 2;
     return cudaGetLastError();
   }
@@ -525,7 +538,7 @@ cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void 
   else
     colreduce_partial_kernel<float, float><<<grid, CR_COLS, 0, s>>>(
         mode, R, N, cp<float>(A), cp<float>(X), mean, rstd, partial);
-  colreduce_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(chunks, N, partial, out);
+  colreduce_final_kernel<<<(N + 31) / 32, 256, 0, s>>>(chunks, N, partial, out);
   g_launches += 2;
   return cudaGetLastError();
 }

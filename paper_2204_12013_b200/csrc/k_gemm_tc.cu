@@ -483,9 +483,11 @@ cudaError_t launch_bn(const Gemm &g, cudaStream_t s) {
   }
 }
 
-// Tile width: the fewest persistent rounds, a 128-wide tile costing ~0.55 of
-// a 256-wide one (same A slab, half the B slab and MMA time).
+// Tile width: 256 whenever N allows (measured best for the forward / dX
+// shapes); for fp32-accumulating dW GEMMs the fewest persistent rounds, a
+// 128-wide tile costing ~0.55 of a 256-wide one.
 cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
+  if (g.epi != EPI_ACC_F32) return g.N >= 256 ? launch_bn<256>(g, s) : launch_bn<128>(g, s);
   static int sms = 0;
   if (!sms) {
     int dev = 0;
