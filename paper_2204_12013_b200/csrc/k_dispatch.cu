@@ -17,9 +17,16 @@ cudaError_t attention_tc_bwd(int B, int S, int H, int nh, bool causal, const voi
                              const void *o, const float *lse, const void *dout, void *dqkv,
                              float *scratch, cudaStream_t s);
 
-// bf16: tensor-core flash attention (head dim 32/64); fp32 check mode: SIMT.
+bool attention_umma_supported(int B, int S, int H, int nh);
+cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const void *qkv, void *o,
+                               float *lse, cudaStream_t s);
+
+// bf16: tcgen05 flash attention forward (head dim 64), else the mma.sync
+// kernels (head dim 32/64); fp32 check mode: SIMT.
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s) {
+  if (bf16 && attention_umma_supported(B, S, H, nh))
+    return attention_umma_fwd(B, S, H, nh, causal, qkv, o, lse, s);
   if (bf16 && attention_tc_supported(H, nh))
     return attention_tc_fwd(B, S, H, nh, causal, qkv, o, lse, s);
   return attention_simt_fwd(bf16, B, S, H, nh, causal, qkv, o, lse, s);
