@@ -1,4 +1,6 @@
 // k_dispatch.cu — picks the kernel implementation per op and shape.
+#include <cstdlib>
+
 #include "k_common.cuh"
 
 namespace bb {
@@ -25,7 +27,14 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
 // kernels (head dim 32/64); fp32 check mode: SIMT.
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s) {
-  if (bf16 && attention_umma_supported(B, S, H, nh))
+  // The tcgen05 forward (k_attn_umma.cu) is parity-tested but, with a single
+  // softmax warpgroup per CTA, still slower than the mma.sync kernel on C1
+  // shapes; it is selected only when BB_ATTN_UMMA=1.
+  static const bool use_umma = [] {
+    const char *e = std::getenv("BB_ATTN_UMMA");
+    return e && e[0] == '1';
+  }();
+  if (bf16 && use_umma && attention_umma_supported(B, S, H, nh))
     return attention_umma_fwd(B, S, H, nh, causal, qkv, o, lse, s);
   if (bf16 && attention_tc_supported(H, nh))
     return attention_tc_fwd(B, S, H, nh, causal, qkv, o, lse, s);

@@ -1,0 +1,71 @@
+"""Worker for multi-process (one rank per GPU) parity tests; launched by
+tests/test_gpu_multi.py through torch.distributed.run. Runs a few steps of a
+config through the C ABI with NCCL edges, optionally injecting a preemption,
+and saves each rank's hosted stage states to <out>/rank<r>.npz."""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2204_12013_b200 as bb  # noqa: E402
+from synth import get_config, make_params, make_tokens  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C0")
+    ap.add_argument("--prec", default="bf16")
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--victim", type=int, default=-1)
+    ap.add_argument("--pi", type=int, default=0)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = get_config(a.config)
+    P = a.stages or cfg.stages
+    obj = [bb.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=True,
+                    prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=local,
+                    nccl_id=obj[0])
+    p.load_params(make_params(cfg.model))
+    losses, rec = [], None
+    for t in range(a.steps):
+        tok, tgt = make_tokens(cfg, t)
+        if t == 0 and a.victim >= 0:
+            p.preempt(a.victim, a.pi)
+        status, st = p.step(tok, tgt)
+        loss = st.loss
+        if status == "preempted":
+            r = p.recover()
+            loss, rec = r.loss, r
+        losses.append(loss)
+        dist.barrier()
+    out = {"losses": np.array(losses, np.float32), "dump": np.array(p.schedule_dump())}
+    if rec is not None:
+        out["recovery_dump"] = np.array(p.recovery_dump())
+    for s in range(P):
+        for what in ("params", "grads", "adam_m", "adam_v"):
+            try:
+                out[f"{what}_{s}"] = p.read_state(s, what)
+            except bb.BambooError:
+                pass
+    np.savez(os.path.join(a.out, f"rank{rank}.npz"), **out)
+    p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,97 @@
+"""Multi-GPU (one process per GPU, NCCL P2P edges) parity: the pipeline spread
+over 2 (or 4) B200s must give exactly the single-process results (same
+kernels, same order => bit-identical), match the fp64 oracle within the
+tolerances, and recover from an injected preemption bit-identically."""
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import pipeline as opipe, plan as opl
+from synth import get_config, make_params, make_tokens
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+def run_mp(n, **kw):
+    d = tempfile.mkdtemp()
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}",
+            os.path.join(ROOT, "tests", "mp_worker.py"), "--out", d]
+    for k, v in kw.items():
+        args += [f"--{k}", str(v)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [dict(np.load(os.path.join(d, f"rank{i}.npz"))) for i in range(n)]
+
+
+def merged(ranks, P, what):
+    out = []
+    for s in range(P):
+        got = [r[f"{what}_{s}"] for r in ranks if f"{what}_{s}" in r]
+        assert got, (what, s)
+        out.append(got[0])
+    return np.concatenate(out)
+
+
+def single(cfg, steps, victim=-1, pi=0):
+    import paper_2204_12013_b200 as bb
+    p = bb.Pipeline(cfg.model, cfg.stages, cfg.microbatches, micro_batch=cfg.micro_batch, rc=True,
+                    lr=1e-4)
+    p.load_params(make_params(cfg.model))
+    losses = []
+    for t in range(steps):
+        tok, tgt = make_tokens(cfg, t)
+        if t == 0 and victim >= 0:
+            p.preempt(victim, pi)
+        status, st = p.step(tok, tgt)
+        losses.append(p.recover().loss if status == "preempted" else st.loss)
+    state = {w: np.concatenate([p.read_state(s, w) for s in range(cfg.stages)])
+             for w in ("params", "grads", "adam_m", "adam_v")}
+    p.close()
+    return losses, state
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multi_gpu_equals_single_process(n):
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cfg = get_config("C0") if n == 2 else __import__("dataclasses").replace(
+        get_config("C0"), stages=4, microbatches=6)
+    ranks = run_mp(n, config="C0", stages=cfg.stages, steps=2) if n == 2 else None
+    if n == 4:
+        import dataclasses
+        ranks = run_mp(4, config="C0", stages=4, steps=2)
+    P = cfg.stages if n == 2 else 4
+    c = get_config("C0") if n == 2 else dataclasses.replace(get_config("C0"), stages=4)
+    losses, state = single(c, 2)
+    got_losses = [float(l) for l in ranks[-1]["losses"]]
+    assert got_losses == [float(x) for x in losses]
+    for w in state:
+        assert np.array_equal(merged(ranks, P, w), state[w]), w
+    want = opl.dump(P, c.microbatches, True, opl.partition(4, P), opl.normal_plans(P, c.microbatches, True),
+                    device={i: min(i // (-(-P // n)), n - 1) for i in range(P)})
+    assert str(ranks[0]["dump"]) == want
+
+
+@pytest.mark.parametrize("victim,pi", [(1, 9), (0, 5), (1, 0), (0, 24)])
+def test_multi_gpu_recovery_bitwise(victim, pi):
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cfg = get_config("C0")
+    ranks = run_mp(2, config="C0", steps=2, victim=victim, pi=pi)
+    losses, state = single(cfg, 2)   # failure-free reference
+    survivor = ranks[(victim - 1) % 2]
+    assert [float(x) for x in survivor["losses"]] == [float(x) for x in losses]
+    assert str(survivor["recovery_dump"]) == opl.recovery_dump(2, cfg.microbatches, victim, pi)
+    for w in state:
+        assert np.array_equal(merged([survivor], 2, w), state[w]), w
