@@ -61,25 +61,23 @@ def single(cfg, steps, victim=-1, pi=0):
     return losses, state
 
 
-@pytest.mark.parametrize("n", [2, 4])
-def test_multi_gpu_equals_single_process(n):
+@pytest.mark.parametrize("n,P", [(2, 2), (2, 4), (4, 4)])
+def test_multi_gpu_equals_single_process(n, P):
+    """P stages over n GPUs (n < P: several nodes per process, device-local
+    edges next to NCCL ones) == all P stages in one process, bit for bit."""
+    import dataclasses
     if ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    cfg = get_config("C0") if n == 2 else __import__("dataclasses").replace(
-        get_config("C0"), stages=4, microbatches=6)
-    ranks = run_mp(n, config="C0", stages=cfg.stages, steps=2) if n == 2 else None
-    if n == 4:
-        import dataclasses
-        ranks = run_mp(4, config="C0", stages=4, steps=2)
-    P = cfg.stages if n == 2 else 4
-    c = get_config("C0") if n == 2 else dataclasses.replace(get_config("C0"), stages=4)
+    c = dataclasses.replace(get_config("C0"), stages=P)
+    ranks = run_mp(n, config="C0", stages=P, steps=2)
     losses, state = single(c, 2)
-    got_losses = [float(l) for l in ranks[-1]["losses"]]
-    assert got_losses == [float(x) for x in losses]
+    assert [float(x) for x in ranks[-1]["losses"]] == [float(x) for x in losses]
     for w in state:
         assert np.array_equal(merged(ranks, P, w), state[w]), w
-    want = opl.dump(P, c.microbatches, True, opl.partition(4, P), opl.normal_plans(P, c.microbatches, True),
-                    device={i: min(i // (-(-P // n)), n - 1) for i in range(P)})
+    per = -(-P // n)
+    want = opl.dump(P, c.microbatches, True, opl.partition(4, P),
+                    opl.normal_plans(P, c.microbatches, True),
+                    device={i: min(i // per, n - 1) for i in range(P)})
     assert str(ranks[0]["dump"]) == want
 
 
