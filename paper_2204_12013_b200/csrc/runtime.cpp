@@ -9,6 +9,8 @@
 #include <cstring>
 #include <numeric>
 #include <set>
+#include <cstdio>
+#include <cstdlib>
 #include <sstream>
 
 namespace bb {
@@ -467,8 +469,19 @@ struct Phase {
   int victim = -1;
 };
 
+bool debug_on() {
+  static const bool on = [] {
+    const char *e = std::getenv("BB_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Execute one instruction of node nd; false = blocked on a local message.
 bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
+  if (debug_on())
+    std::fprintf(stderr, "[bb rank %d node %d] %s mb=%d peer=%d stage=%d\n", c.o.world_rank, nd.n,
+                 kind_name(ins.kind), ins.mb, ins.peer, ins.stage);
   const Dims &d = c.d;
   const int P = d.P, M = d.M, k = ins.mb, X = ins.stage;
   switch (ins.kind) {
@@ -831,6 +844,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       if (!c.o.nccl_id) throw RtError{BB_E_INVAL, "nccl_id required for world_size > 1"};
       ncclUniqueId id;
       std::memcpy(&id, c.o.nccl_id, sizeof(id));
+      if (debug_on()) std::fprintf(stderr, "[bb rank %d] ncclCommInitRank\n", c.o.world_rank);
       NK(ncclCommInitRank(&c.world, c.o.world_size, id, c.o.world_rank));
       std::set<std::tuple<int, int, int>> want;
       auto add = [&](int a, int b, int kind) {
@@ -872,6 +886,8 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           }
         }
         ncclComm_t nc = nullptr;
+        if (debug_on())
+          std::fprintf(stderr, "[bb rank %d] split color %d key %d\n", c.o.world_rank, color, key);
         NK(ncclCommSplit(c.world, color, key, &nc, nullptr));
         if (mine) {
           EdgeComm ed;
