@@ -901,6 +901,24 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         color_base += (int)round.size();
         todo = rest;
       }
+      // NCCL connects P2P channels lazily on the first send/recv of a
+      // communicator and blocks the calling thread until the peer connects
+      // on the same communicator. Connect every edge now, in one global
+      // order (deadlock-free: the smallest edge anybody waits on is always
+      // reached by both endpoints), so no step ever blocks in a connect.
+      float *ping = (float *)dmalloc(sizeof(float));
+      CK(cudaMemset(ping, 0, sizeof(float)));
+      for (auto &e : want) {
+        auto it = c.edges.find(e);
+        if (it == c.edges.end()) continue;
+        EdgeComm &ed = it->second;
+        if (c.node_rank[ed.src] == c.o.world_rank)
+          NK(ncclSend(ping, 1, ncclFloat32, 1, ed.comm, ed.stream));
+        else
+          NK(ncclRecv(ping, 1, ncclFloat32, 0, ed.comm, ed.stream));
+        CK(cudaStreamSynchronize(ed.stream));
+      }
+      CK(cudaFree(ping));
     }
     CK(cudaDeviceSynchronize());
     return BB_OK;
