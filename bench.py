@@ -19,6 +19,11 @@ barriers, max over ranks; `e2e` = the same through bb_step with host buffers
 import argparse
 import json
 import os
+
+# Every node has a main + FRC stream and every NCCL edge its own stream:
+# give each its own hardware queue (the default 8 would serialise unrelated
+# streams behind spinning P2P kernels). Must precede CUDA initialisation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -17,7 +17,10 @@
  * exchange activations, gradients and replica gradients with NCCL P2P over
  * NVLink on 2-rank communicators, one per (src node, dst node, message kind)
  * edge, created inside bb_init from the 128-byte ncclUniqueId the caller
- * broadcasts (bb_nccl_unique_id on rank 0).
+ * broadcasts (bb_nccl_unique_id on rank 0). Each node uses two streams and
+ * each edge one, so processes should set CUDA_DEVICE_MAX_CONNECTIONS=32 before
+ * creating their CUDA context (otherwise unrelated streams share hardware
+ * queues and can serialise behind spinning P2P kernels).
  *
  * Conventions for every entry point:
  *  - Returns bb_status (0 = BB_OK). No exception, exit() or abort() crosses

@@ -1,4 +1,9 @@
 import os
+
+# Every node has a main + FRC stream and every NCCL edge its own stream:
+# give each its own hardware queue (the default 8 would serialise unrelated
+# streams behind spinning P2P kernels). Must precede CUDA initialisation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -4,6 +4,11 @@ config through the C ABI with NCCL edges, optionally injecting a preemption,
 and saves each rank's hosted stage states to <out>/rank<r>.npz."""
 import argparse
 import os
+
+# Every node has a main + FRC stream and every NCCL edge its own stream:
+# give each its own hardware queue (the default 8 would serialise unrelated
+# streams behind spinning P2P kernels). Must precede CUDA initialisation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import numpy as np

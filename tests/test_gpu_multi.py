@@ -29,7 +29,7 @@ def run_mp(n, **kw):
             os.path.join(ROOT, "tests", "mp_worker.py"), "--out", d]
     for k, v in kw.items():
         args += [f"--{k}", str(v)]
-    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(args, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return [dict(np.load(os.path.join(d, f"rank{i}.npz"))) for i in range(n)]
 

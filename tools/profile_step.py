@@ -1,5 +1,10 @@
 """One warm-up + one profiled step of a config on cuda:0 (for ncu launch lists)."""
 import argparse, os, sys
+
+# Every node has a main + FRC stream and every NCCL edge its own stream:
+# give each its own hardware queue (the default 8 would serialise unrelated
+# streams behind spinning P2P kernels). Must precede CUDA initialisation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2204_12013_b200 as bb
 from synth import get_config, make_params, make_tokens
