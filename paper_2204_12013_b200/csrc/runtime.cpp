@@ -10,6 +10,7 @@
 #include <numeric>
 #include <set>
 #include <cstdio>
+#include <ctime>
 #include <cstdlib>
 #include <sstream>
 
@@ -572,6 +573,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         wait_ev(ed.stream, pl.ev);
         NK(ncclSend(pl.p, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 1, ed.comm,
                     ed.stream));
+        ++ed.issued;
       }
       return true;
     }
@@ -592,6 +594,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
                                          : arena_alloc(nd, msg_bytes(c, m.kind, m.stage));
         NK(ncclRecv(dp, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 0, ed.comm,
                     ed.stream));
+        ++ed.issued;
         got = {dp, record(nd, ed.stream)};
       }
       if (ins.kind == RECV_ACT)
@@ -649,7 +652,31 @@ void run(Ctx &c, const Plans &lists, const std::map<int, int> *lim, const Phase 
   }
 }
 
+void debug_wait(Ctx &c, bool comm_too) {
+  // BB_DEBUG: poll instead of blocking and report the streams still busy
+  for (int iter = 0;; ++iter) {
+    bool busy = false;
+    std::ostringstream o;
+    for (auto &kv : c.nodes) {
+      if (cudaStreamQuery(kv.second.main) == cudaErrorNotReady) { busy = true; o << " main" << kv.first; }
+      if (cudaStreamQuery(kv.second.frc) == cudaErrorNotReady) { busy = true; o << " frc" << kv.first; }
+    }
+    if (comm_too)
+      for (auto &kv : c.edges)
+        if (cudaStreamQuery(kv.second.stream) == cudaErrorNotReady) {
+          busy = true;
+          o << " edge" << std::get<0>(kv.first) << "->" << std::get<1>(kv.first) << "k" << std::get<2>(kv.first)
+            << "(ops " << kv.second.issued << ")";
+        }
+    if (!busy) return;
+    if (iter % 50 == 49) std::fprintf(stderr, "[bb rank %d] busy:%s\n", c.o.world_rank, o.str().c_str());
+    struct timespec ts{0, 100000000};
+    nanosleep(&ts, nullptr);
+  }
+}
+
 void sync_all(Ctx &c, bool comm_too) {
+  if (debug_on()) debug_wait(c, comm_too);
   for (auto &kv : c.nodes) {
     CK(cudaStreamSynchronize(kv.second.main));
     CK(cudaStreamSynchronize(kv.second.frc));

@@ -92,6 +92,7 @@ struct EdgeComm {
   int src = -1, dst = -1, kind = -1;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  long issued = 0;   // ops enqueued (debug)
 };
 
 struct ProfRec {
