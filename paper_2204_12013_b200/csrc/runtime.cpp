@@ -13,6 +13,7 @@
 #include <ctime>
 #include <cstdlib>
 #include <sstream>
+#include <thread>
 
 namespace bb {
 
@@ -451,10 +452,6 @@ size_t msg_count(const Ctx &c, MsgKind kind, int stage) {
 size_t msg_bytes(const Ctx &c, MsgKind kind, int stage) {
   return msg_count(c, kind, stage) * (kind == MSG_GRADSUM ? sizeof(float) : c.act_bytes);
 }
-ncclDataType_t msg_type(const Ctx &c, MsgKind kind) {
-  if (kind == MSG_GRADSUM || !c.bf16) return ncclFloat32;
-  return ncclBfloat16;
-}
 
 Key payload_key(const Instr &ins) {
   switch (ins.kind) {
@@ -569,11 +566,14 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         CK(cudaMemcpyAsync(dp, pl.p, bytes, cudaMemcpyDeviceToDevice, nd.main));
         c.mail[ck].push_back({dp, record(nd, nd.main)});
       } else {
-        EdgeComm &ed = c.edges.at(std::make_tuple(nd.n, ins.peer, (int)m.kind));
-        wait_ev(ed.stream, pl.ev);
-        NK(ncclSend(pl.p, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 1, ed.comm,
-                    ed.stream));
-        ++ed.issued;
+        XEdge &e = c.x.edges.at(std::make_tuple(nd.n, ins.peer, (int)m.kind));
+        const int slot = (int)(e.sent % (uint64_t)e.cap);
+        if (bytes > e.slot_bytes) throw RtError{BB_E_STATE, "message larger than its slot"};
+        char *dst = e.peer_base + e.recv_off + (size_t)slot * e.slot_bytes;
+        wait_ev(e.stream, pl.ev);
+        CK(cudaMemcpyAsync(dst, pl.p, bytes, cudaMemcpyDeviceToDevice, e.stream));
+        CK(cudaEventRecord(e.ev[slot], e.stream));
+        c.x.post(e);
       }
       return true;
     }
@@ -589,13 +589,19 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         got = it->second.front();
         it->second.pop_front();
       } else {
-        EdgeComm &ed = c.edges.at(std::make_tuple(ins.peer, nd.n, (int)m.kind));
-        void *dp = m.kind == MSG_GRADSUM ? (void *)nd.copies.at(X).grad
-                                         : arena_alloc(nd, msg_bytes(c, m.kind, m.stage));
-        NK(ncclRecv(dp, msg_count(c, m.kind, m.stage), msg_type(c, m.kind), 0, ed.comm,
-                    ed.stream));
-        ++ed.issued;
-        got = {dp, record(nd, ed.stream)};
+        XEdge &e = c.x.edges.at(std::make_tuple(ins.peer, nd.n, (int)m.kind));
+        if (!c.x.available(e)) return false;       // the sender has not posted it yet
+        const int slot = (int)(e.consumed % (uint64_t)e.cap);
+        ++e.consumed;
+        char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
+        if (m.kind == MSG_GRADSUM) {
+          wait_ev(nd.main, e.rev[slot]);
+          CK(cudaMemcpyAsync(nd.copies.at(X).grad, src, msg_bytes(c, m.kind, m.stage),
+                             cudaMemcpyDeviceToDevice, nd.main));
+          got = {nd.copies.at(X).grad, record(nd, nd.main)};
+        } else {
+          got = {src, e.rev[slot]};
+        }
       }
       if (ins.kind == RECV_ACT)
         nd.store[{K_ACT, X, k}] = got;
@@ -626,18 +632,33 @@ void run(Ctx &c, const Plans &lists, const std::map<int, int> *lim, const Phase 
   std::map<int, size_t> pc;
   for (auto &kv : c.nodes)
     if (kv.second.alive && lists.count(kv.first)) pc[kv.first] = 0;
-  bool progress = true;
-  while (progress) {
-    progress = false;
+  const double t_start = now_ms();
+  for (;;) {
+    bool progress = false, pending = false;
     for (auto &kv : pc) {
       Node &nd = c.nodes.at(kv.first);
       const auto &seq = lists.at(kv.first);
       size_t cap = seq.size();
       if (lim) cap = std::min(cap, (size_t)lim->at(kv.first));
+      if (kv.second < cap) pending = true;
       while (kv.second < cap && exec(c, nd, seq[kv.second], ph)) {
+        if (debug_on()) {
+          cudaEvent_t e1, e2;
+          cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+          cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
+          cudaEventRecord(e1, nd.main);
+          cudaEventRecord(e2, nd.frc);
+          c.dbg.push_back({nd.n, (int)kv.second, seq[kv.second], e1, e2});
+        }
         ++kv.second;
         progress = true;
       }
+    }
+    if (!pending) break;
+    if (!progress) {
+      // waiting for a peer rank's message (or a genuine local deadlock)
+      if (c.o.world_size == 1 || now_ms() - t_start > 300000.0) break;
+      std::this_thread::yield();
     }
   }
   for (auto &kv : pc) {
@@ -662,14 +683,25 @@ void debug_wait(Ctx &c, bool comm_too) {
       if (cudaStreamQuery(kv.second.frc) == cudaErrorNotReady) { busy = true; o << " frc" << kv.first; }
     }
     if (comm_too)
-      for (auto &kv : c.edges)
-        if (cudaStreamQuery(kv.second.stream) == cudaErrorNotReady) {
+      for (auto &kv : c.x.edges)
+        if (kv.second.stream && cudaStreamQuery(kv.second.stream) == cudaErrorNotReady) {
           busy = true;
-          o << " edge" << std::get<0>(kv.first) << "->" << std::get<1>(kv.first) << "k" << std::get<2>(kv.first)
-            << "(ops " << kv.second.issued << ")";
+          o << " edge" << std::get<0>(kv.first) << "->" << std::get<1>(kv.first) << "k"
+            << std::get<2>(kv.first) << "(sent " << kv.second.sent << ")";
         }
     if (!busy) return;
-    if (iter % 50 == 49) std::fprintf(stderr, "[bb rank %d] busy:%s\n", c.o.world_rank, o.str().c_str());
+    if (iter % 50 == 49) {
+      std::fprintf(stderr, "[bb rank %d] busy:%s\n", c.o.world_rank, o.str().c_str());
+      std::map<int, int> shown;
+      for (auto &d : c.dbg) {
+        const bool m_ok = cudaEventQuery(d.main_ev) == cudaSuccess;
+        const bool f_ok = cudaEventQuery(d.frc_ev) == cudaSuccess;
+        if ((!m_ok || !f_ok) && shown[d.node]++ < 2)
+          std::fprintf(stderr, "[bb rank %d] node %d first pending #%d %s mb=%d peer=%d stage=%d main=%d frc=%d\n",
+                       c.o.world_rank, d.node, d.idx, kind_name(d.ins.kind), d.ins.mb, d.ins.peer,
+                       d.ins.stage, m_ok, f_ok);
+      }
+    }
     struct timespec ts{0, 100000000};
     nanosleep(&ts, nullptr);
   }
@@ -682,7 +714,8 @@ void sync_all(Ctx &c, bool comm_too) {
     CK(cudaStreamSynchronize(kv.second.frc));
   }
   if (comm_too)
-    for (auto &kv : c.edges) CK(cudaStreamSynchronize(kv.second.stream));
+    for (auto &kv : c.x.edges)
+      if (kv.second.stream) CK(cudaStreamSynchronize(kv.second.stream));
 }
 
 void begin_step(Ctx &c) {
@@ -828,7 +861,9 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       Node &nd = c.nodes[n];
       nd.n = n;
       CK(cudaStreamCreateWithPriority(&nd.main, cudaStreamNonBlocking, hi_prio));
-      CK(cudaStreamCreateWithPriority(&nd.frc, cudaStreamNonBlocking, lo_prio));
+      const char *fp = std::getenv("BB_FRC_PRIO");   // debug: 0 = same priority as main
+      CK(cudaStreamCreateWithPriority(&nd.frc, cudaStreamNonBlocking,
+                                      (fp && fp[0] == '0') ? hi_prio : lo_prio));
       CK(cudaEventCreate(&nd.t0));
       CK(cudaEventCreate(&nd.t1));
       std::vector<std::pair<int, bool>> hosted{{n, false}};
@@ -864,9 +899,9 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.d_tgt = (int32_t *)dmalloc((size_t)M * R * 4);
       nd.d_csr = (int32_t *)dmalloc((size_t)M * c.csr_stride * 4);
     }
-    // NCCL edges: one 2-rank communicator per (src node, dst node, kind) whose
-    // endpoints live on different ranks; ring distance <= 2 covers the normal
-    // pipeline, the replica ring and the failover skip edges.
+    // Cross-rank edges: one per (src node, dst node, kind) whose endpoints
+    // live on different ranks; ring distance <= 2 covers the normal pipeline,
+    // the replica ring and the failover skip edges (xport.h).
     if (c.o.world_size > 1) {
       if (!c.o.nccl_id) throw RtError{BB_E_INVAL, "nccl_id required for world_size > 1"};
       ncclUniqueId id;
@@ -886,66 +921,14 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         add(a, a - 2, MSG_GRAD);
         add(a, a - 1, MSG_GRADSUM);
       }
-      std::vector<std::tuple<int, int, int>> todo(want.begin(), want.end());
-      int color_base = 0;
-      while (!todo.empty()) {
-        // one round = a matching over ranks
-        std::set<int> busy;
-        std::vector<std::tuple<int, int, int>> round, rest;
-        for (auto &e : todo) {
-          const int ra = c.node_rank[std::get<0>(e)], rb = c.node_rank[std::get<1>(e)];
-          if (busy.count(ra) || busy.count(rb)) {
-            rest.push_back(e);
-            continue;
-          }
-          busy.insert(ra);
-          busy.insert(rb);
-          round.push_back(e);
-        }
-        int color = NCCL_SPLIT_NOCOLOR, key = 0;
-        const std::tuple<int, int, int> *mine = nullptr;
-        for (size_t i = 0; i < round.size(); ++i) {
-          const int ra = c.node_rank[std::get<0>(round[i])], rb = c.node_rank[std::get<1>(round[i])];
-          if (ra == c.o.world_rank || rb == c.o.world_rank) {
-            color = color_base + (int)i;
-            key = ra == c.o.world_rank ? 0 : 1;
-            mine = &round[i];
-          }
-        }
-        ncclComm_t nc = nullptr;
-        if (debug_on())
-          std::fprintf(stderr, "[bb rank %d] split color %d key %d\n", c.o.world_rank, color, key);
-        NK(ncclCommSplit(c.world, color, key, &nc, nullptr));
-        if (mine) {
-          EdgeComm ed;
-          ed.src = std::get<0>(*mine);
-          ed.dst = std::get<1>(*mine);
-          ed.kind = std::get<2>(*mine);
-          ed.comm = nc;
-          CK(cudaStreamCreateWithPriority(&ed.stream, cudaStreamNonBlocking, hi_prio));
-          c.edges[*mine] = ed;
-        }
-        color_base += (int)round.size();
-        todo = rest;
-      }
-      // NCCL connects P2P channels lazily on the first send/recv of a
-      // communicator and blocks the calling thread until the peer connects
-      // on the same communicator. Connect every edge now, in one global
-      // order (deadlock-free: the smallest edge anybody waits on is always
-      // reached by both endpoints), so no step ever blocks in a connect.
-      float *ping = (float *)dmalloc(sizeof(float));
-      CK(cudaMemset(ping, 0, sizeof(float)));
-      for (auto &e : want) {
-        auto it = c.edges.find(e);
-        if (it == c.edges.end()) continue;
-        EdgeComm &ed = it->second;
-        if (c.node_rank[ed.src] == c.o.world_rank)
-          NK(ncclSend(ping, 1, ncclFloat32, 1, ed.comm, ed.stream));
-        else
-          NK(ncclRecv(ping, 1, ncclFloat32, 0, ed.comm, ed.stream));
-        CK(cudaStreamSynchronize(ed.stream));
-      }
-      CK(cudaFree(ping));
+      size_t gmax = 0;
+      for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
+      const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float)};
+      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4};
+      const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
+      const std::string xe = xport_init(c.x, c.world, c.o.world_rank, c.o.world_size, wl,
+                                        c.node_rank, slot_bytes, caps, c.o.nccl_id, hi_prio);
+      if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
     }
     CK(cudaDeviceSynchronize());
     return BB_OK;
@@ -986,6 +969,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     if ((tok == nullptr) != (tgt == nullptr)) throw RtError{BB_E_INVAL, "null tokens/targets"};
     if (!tok && !c.resident) throw RtError{BB_E_STATE, "no resident inputs (bb_stage_inputs)"};
     CK(cudaSetDevice(c.o.device));
+    c.x.barrier();   // every rank finished the previous step: receive slots are free
     begin_step(c);
     c.resident_step = tok == nullptr;
     if (tok) {
@@ -1023,7 +1007,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     ph.drop_to_victim = true;
     ph.victim = v;
     run(c, c.plans, &c.cut.pcs, ph);
-    sync_all(c, false);   // pending sends wait for the continuation's receives
+    sync_all(c, true);
     c.interrupted = true;
     if (st) {
       st->loss = NAN;
@@ -1203,8 +1187,7 @@ bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n) {
 
 void rt_destroy(Ctx &c) {
   cudaDeviceSynchronize();
-  for (auto &kv : c.edges)
-    if (kv.second.comm) ncclCommDestroy(kv.second.comm);
+  xport_destroy(c.x);
   if (c.world) ncclCommDestroy(c.world);
   for (auto &kv : c.nodes) {
     Node &nd = kv.second;

@@ -7,7 +7,8 @@
 // (own stage + the successor's replica with Adam state), saved-set
 // slot pools (1F1B stash; full FRC retention, P:524 / Q10), a per-step arena
 // for activations and input-gradients (retained for a lazy-BRC resend, Q3) and
-// a backward scratch. Nodes on other ranks are reached over NCCL P2P edges.
+// a backward scratch. Nodes on other ranks are reached through xport.h
+// (copy-engine writes into the peer's HBM + IPC events; NCCL bootstraps).
 #pragma once
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -19,6 +20,7 @@
 #include "bamboo.h"
 #include "kernels.h"
 #include "plan.h"
+#include "xport.h"
 
 namespace bb {
 
@@ -88,20 +90,20 @@ struct Node {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 
-struct EdgeComm {
-  int src = -1, dst = -1, kind = -1;
-  ncclComm_t comm = nullptr;
-  cudaStream_t stream = nullptr;
-  long issued = 0;   // ops enqueued (debug)
-};
-
 struct ProfRec {
   int cls;
   cudaEvent_t a, b;
   double work;
 };
 
+struct DbgRec {
+  int node, idx;
+  Instr ins;
+  cudaEvent_t main_ev, frc_ev;
+};
+
 struct Ctx {
+  std::vector<DbgRec> dbg;
   Dims d{};
   bb_opts o{};
   bool bf16 = true;
@@ -116,8 +118,8 @@ struct Ctx {
   bool fatal = false;
   std::vector<int> node_rank, node_device;
   std::map<int, Node> nodes;          // local nodes only
-  std::map<std::tuple<int, int, int>, EdgeComm> edges;
-  ncclComm_t world = nullptr;
+  Xport x;                            // cross-rank transport (IPC + copy engines)
+  ncclComm_t world = nullptr;         // bootstrap only
   // local mailboxes (per (src node, dst node, kind))
   std::map<ChanKey, std::deque<Entry>> mail;
   // injection / recovery state

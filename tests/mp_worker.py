@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--pi", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--rc", type=int, default=1)
     a = ap.parse_args()
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -41,7 +42,7 @@ def main():
     P = a.stages or cfg.stages
     obj = [bb.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=True,
+    p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=bool(a.rc),
                     prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=local,
                     nccl_id=obj[0])
     p.load_params(make_params(cfg.model))
