@@ -186,17 +186,17 @@ def run_ours(args, rank, ws, local):
     P = max(cfg.stages, ws)
     M, mb = cfg.microbatches, cfg.micro_batch
     samples = M * mb
-    nccl_id = bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
+    def fresh_id():   # every communicator needs its own unique id
+        return bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
     flat = make_params(m)
     tok, tgt = make_tokens(cfg, 0)
     host_batches = [make_tokens(cfg, s) for s in range(1, 3)]
-    common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
-                  nccl_id=nccl_id)
+    common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local)
 
     results = {}
     for rc in (False, True):
         log(rank, f"init rc={rc} P={P} M={M} mb={mb}")
-        pipe = bb.Pipeline(m, P, M, rc=rc, profile=rc, **common)
+        pipe = bb.Pipeline(m, P, M, rc=rc, nccl_id=fresh_id(), **common)
         pipe.load_params(flat)
         pipe.stage_inputs(tok, tgt)
         for i in range(args.warmup):
@@ -209,13 +209,12 @@ def run_ours(args, rank, ws, local):
             clocks.start()
         ms, launches, _, _ = timed(pipe, args.steps, ws)
         clk = clocks.stop() if rc else None
-        kstats = pipe.kernel_stats() if rc else None
         # end to end through the public call with host buffers
         log(rank, f"timed: {ms / args.steps:.2f} ms/step")
         ms_e2e, _, h2d, d2h = timed(pipe, args.steps, ws, host_inputs=host_batches)
         log(rank, f"e2e: {ms_e2e / args.steps:.2f} ms/step")
         pipe.stage_inputs(tok, tgt)
-        results[rc] = dict(ms=ms / args.steps, launches=launches, clocks=clk, kstats=kstats,
+        results[rc] = dict(ms=ms / args.steps, launches=launches, clocks=clk,
                            e2e_ms=ms_e2e / args.steps, h2d=h2d / args.steps, d2h=d2h / args.steps)
         if rc:
             # recovery latency: preempt the middle node in its backward phase
@@ -242,10 +241,24 @@ def run_ours(args, rank, ws, local):
         del pipe
         torch.cuda.empty_cache()
 
+    # Per-kernel device times: the same step (RC on) re-run with every local
+    # node on one serialised stream, each kernel bracketed by CUDA events on
+    # that stream (concurrent streams would double-count overlapped time).
+    log(rank, "profiled (serialised) steps for per-kernel times")
+    pipe = bb.Pipeline(m, P, M, rc=True, profile=True, nccl_id=fresh_id(), **common)
+    pipe.load_params(flat)
+    pipe.stage_inputs(tok, tgt)
+    for _ in range(2):
+        _, st_prof = pipe.step()
+    ks = pipe.kernel_stats()
+    prof_step_ms = allreduce_max(st_prof.device_ms, ws)
+    pipe.close()
+    del pipe
+    torch.cuda.empty_cache()
+
     on, off = results[True], results[False]
     value = samples / (on["ms"] / 1e3)
     pk = peaks()
-    ks = on["kstats"] or {}
     gemm_ms = sum(ks[k][1] for k in ks if k.startswith("gemm"))
     gemm_flop = sum(ks[k][2] for k in ks if k.startswith("gemm"))
     gemm_n = sum(ks[k][0] for k in ks if k.startswith("gemm"))
@@ -261,7 +274,9 @@ def run_ours(args, rank, ws, local):
             "peak": pk.get("bf16_tflops_sustained", 1377.6), "unit": "TFLOP/s",
             "frac": round(achieved / pk.get("bf16_tflops_sustained", 1377.6), 4),
             "traffic": None, "kernel": "gemm_tc (tcgen05 bf16, all GEMM launches of the step)",
-            "launches_per_step": gemm_n / args.steps,
+            "launches_per_step": gemm_n,
+            "timing": "CUDA events around every GEMM launch of one full step (RC on), all "
+                      "local nodes serialised on one stream; sum of 2MNK over sum of durations",
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
     ncu = os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")
     if os.path.exists(ncu):
@@ -291,7 +306,8 @@ def run_ours(args, rank, ws, local):
                 "h2d_bytes_per_step": int(on["h2d"]), "d2h_bytes_per_step": int(on["d2h"])},
         "gpu_launches": int(launches),
         "clocks": on["clocks"],
-        "kernel_ms_per_step": {k: round(v[1] / args.steps, 3) for k, v in ks.items()},
+        "kernel_ms_per_step": {k: round(v[1], 3) for k, v in ks.items()},
+        "serialised_step_ms": round(prof_step_ms, 2),
     }
     if args.cpu_baseline and ws >= 1:
         log(rank, "cpu baseline (oracle)")

@@ -81,7 +81,9 @@ typedef struct {
   const int *node_rank;         /* [stages] process rank hosting node n; NULL = contiguous
                                    blocks of ceil(stages/world_size) nodes per rank        */
   const void *nccl_id;          /* 128-byte ncclUniqueId (same on all ranks) or NULL       */
-  int profile;                  /* 1 = time every GEMM launch with CUDA events            */
+  int profile;                  /* 1 = time every kernel class with CUDA events; the local
+                                   nodes then share ONE serialised stream (no FRC overlap),
+                                   so use it for per-kernel timing, not for throughput    */
 } bb_opts;
 
 typedef struct {

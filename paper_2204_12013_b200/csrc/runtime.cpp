@@ -860,10 +860,15 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       if (c.node_rank[n] != c.o.world_rank) continue;
       Node &nd = c.nodes[n];
       nd.n = n;
-      CK(cudaStreamCreateWithPriority(&nd.main, cudaStreamNonBlocking, hi_prio));
-      const char *fp = std::getenv("BB_FRC_PRIO");   // debug: 0 = same priority as main
-      CK(cudaStreamCreateWithPriority(&nd.frc, cudaStreamNonBlocking,
-                                      (fp && fp[0] == '0') ? hi_prio : lo_prio));
+      if (c.o.profile) {
+        // profiling: every local node issues into one serialised stream so
+        // each kernel's CUDA-event time is its own (no cross-stream overlap)
+        if (!c.serial) CK(cudaStreamCreateWithPriority(&c.serial, cudaStreamNonBlocking, hi_prio));
+        nd.main = nd.frc = c.serial;
+      } else {
+        CK(cudaStreamCreateWithPriority(&nd.main, cudaStreamNonBlocking, hi_prio));
+        CK(cudaStreamCreateWithPriority(&nd.frc, cudaStreamNonBlocking, lo_prio));
+      }
       CK(cudaEventCreate(&nd.t0));
       CK(cudaEventCreate(&nd.t1));
       std::vector<std::pair<int, bool>> hosted{{n, false}};
@@ -1216,10 +1221,13 @@ void rt_destroy(Ctx &c) {
     for (auto e : nd.evpool) cudaEventDestroy(e);
     cudaEventDestroy(nd.t0);
     cudaEventDestroy(nd.t1);
-    cudaStreamDestroy(nd.main);
-    cudaStreamDestroy(nd.frc);
+    if (!c.serial) {
+      cudaStreamDestroy(nd.main);
+      cudaStreamDestroy(nd.frc);
+    }
   }
   for (auto e : c.prof_pool) cudaEventDestroy(e);
+  if (c.serial) cudaStreamDestroy(c.serial);
   if (c.h_tok) cudaFreeHost(c.h_tok);
   if (c.h_tgt) cudaFreeHost(c.h_tgt);
   if (c.h_csr) cudaFreeHost(c.h_csr);

@@ -120,6 +120,7 @@ struct Ctx {
   std::map<int, Node> nodes;          // local nodes only
   Xport x;                            // cross-rank transport (IPC + copy engines)
   ncclComm_t world = nullptr;         // bootstrap only
+  cudaStream_t serial = nullptr;      // profile mode: the one stream of all local nodes
   // local mailboxes (per (src node, dst node, kind))
   std::map<ChanKey, std::deque<Entry>> mail;
   // injection / recovery state
