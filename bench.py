@@ -267,6 +267,8 @@ def run_ours(args, rank, ws, local):
     gemm_flop_all = allreduce_sum(gemm_flop, ws)
     achieved = gemm_flop_all / (gemm_ms_all / 1e3) / 1e12 if gemm_ms_all > 0 else 0.0
     launches = allreduce_sum(on["launches"], ws)
+    on["h2d"] = allreduce_sum(on["h2d"], ws)
+    on["d2h"] = allreduce_sum(on["d2h"], ws)
     rec = results.get("recovery", {})
     if rank != 0:
         return
@@ -309,7 +311,7 @@ def run_ours(args, rank, ws, local):
         "kernel_ms_per_step": {k: round(v[1], 3) for k, v in ks.items()},
         "serialised_step_ms": round(prof_step_ms, 2),
     }
-    if args.cpu_baseline and ws >= 1:
+    if args.cpu_baseline and ws == 1:   # the oracle leg runs on rank 0 at N=1 only
         log(rank, "cpu baseline (oracle)")
         line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     print(json.dumps(line), flush=True)
