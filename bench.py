@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 
 from synth import get_config, make_params, make_tokens  # noqa: E402
 
+MODEL_NAMES = {"C0": "tiny", "C1": "GPT-2 small", "C2": "BERT-large", "C3": "GPT-2 XL"}
 BASELINE_METRIC = "samples/sec at 1/2/4/8 B200 with RC vs no-RC; RC overhead %; recovery ms"
 
 
@@ -293,8 +294,9 @@ def run_ours(args, rank, ws, local):
         "warmup": args.warmup, "ms_per_step": round(on["ms"], 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded tokens, random-init weights)",
-        "config": {"workload": f"{cfg.name}: GPT-2 small 12L H768 S1024, {P} stages, M={M}, "
-                               f"mb={mb}, EFLB (eager FRC, lazy BRC)",
+        "config": {"workload": f"{cfg.name}: {MODEL_NAMES.get(cfg.name, cfg.name)} {m.n_layer}L "
+                               f"H{m.d_model} S{m.seq_len} {'causal' if m.causal else 'bidirectional'}, "
+                               f"{P} stages, M={M}, mb={mb}, EFLB (eager FRC, lazy BRC)",
                    "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
                    "seq_len": m.seq_len, "parallelism": f"pp{P} on {ws} GPU(s)",
                    "l2": "working set (weights, stash, FRC retention) >> 126 MB L2"},
