@@ -90,51 +90,60 @@ __device__ __forceinline__ void rows_frag(uint32_t (&f)[D / 16][4], const __nv_b
   }
 }
 
-// acc[16 x 64] += A[16 x D] . T^T where T is a 64 x D row tile (B = T rows as
-// columns: "S = Q K^T"). A given as D/16 fragments.
-template <int D>
-__device__ __forceinline__ void mma_abt(float (&acc)[8][4], const uint32_t (&a)[D / 16][4],
-                                        const Tile<D> &t, int lane) {
+// acc[16 x 8*NG] += A[16 x D] . T^T where T is a (8*NG) x D row tile starting at
+// row r0 of `t` (B = T rows as columns: "S = Q K^T"). A given as D/16
+// fragments. K-step outer, column groups inner: consecutive MMAs feed
+// independent accumulators, and each K step's B fragments are loaded first.
+template <int D, int NG = 8>
+__device__ __forceinline__ void mma_abt(float (&acc)[NG][4], const uint32_t (&a)[D / 16][4],
+                                        const Tile<D> &t, int lane, int r0 = 0) {
 #pragma unroll
-  for (int np = 0; np < 4; ++np) {          // pairs of 8-column groups
+  for (int ks = 0; ks < D / 16; ++ks) {
+    uint32_t r[NG / 2][4];
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      uint32_t r[4];
-      const int row = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+    for (int np = 0; np < NG / 2; ++np) {
+      const int row = r0 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
       const int col = ks * 16 + ((lane >> 3) & 1) * 8;
-      ldsm_x4(r, &t.v[row][col]);
-      mma16816(acc[2 * np], a[ks], r[0], r[1]);
-      mma16816(acc[2 * np + 1], a[ks], r[2], r[3]);
+      ldsm_x4(r[np], &t.v[row][col]);
+    }
+#pragma unroll
+    for (int np = 0; np < NG / 2; ++np) {
+      mma16816(acc[2 * np], a[ks], r[np][0], r[np][1]);
+      mma16816(acc[2 * np + 1], a[ks], r[np][2], r[np][3]);
     }
   }
 }
 
-// acc[16 x D] += P[16 x 64] . T where T is a 64 x D row tile; P given as the
-// fp32 accumulator layout of a 16 x 64 block (converted to bf16 A fragments).
-template <int D>
-__device__ __forceinline__ void mma_pt(float (&acc)[D / 8][4], const float (&p)[8][4],
-                                       const Tile<D> &t, int lane) {
+// acc[16 x D] += P[16 x 16*KK] . T where T is a (16*KK) x D row tile starting
+// at row r0 of `t`; P given as the fp32 accumulator layout of a 16 x (16*KK)
+// block (converted to bf16 A fragments).
+template <int D, int KK = 4>
+__device__ __forceinline__ void mma_pt(float (&acc)[D / 8][4], const float (&p)[2 * KK][4],
+                                       const Tile<D> &t, int lane, int r0 = 0) {
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
+  for (int kk = 0; kk < KK; ++kk) {
     const uint32_t a[4] = {pack_bf16(p[2 * kk][0], p[2 * kk][1]),
                            pack_bf16(p[2 * kk][2], p[2 * kk][3]),
                            pack_bf16(p[2 * kk + 1][0], p[2 * kk + 1][1]),
                            pack_bf16(p[2 * kk + 1][2], p[2 * kk + 1][3])};
+    uint32_t r[D / 16][4];
 #pragma unroll
     for (int dp = 0; dp < D / 16; ++dp) {
-      uint32_t r[4];
-      const int row = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int row = r0 + kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
       const int col = dp * 16 + (lane >> 4) * 8;
-      ldsm_x4_t(r, &t.v[row][col]);
-      mma16816(acc[2 * dp], a, r[0], r[1]);
-      mma16816(acc[2 * dp + 1], a, r[2], r[3]);
+      ldsm_x4_t(r[dp], &t.v[row][col]);
+    }
+#pragma unroll
+    for (int dp = 0; dp < D / 16; ++dp) {
+      mma16816(acc[2 * dp], a, r[dp][0], r[dp][1]);
+      mma16816(acc[2 * dp + 1], a, r[dp][2], r[dp][3]);
     }
   }
 }
 
 // ------------------------------------------------------------------ forward
 template <int D>
-__global__ void __launch_bounds__(NT) fa_fwd_kernel(int S, int H, int nh, int causal,
+__global__ void __launch_bounds__(NT, 2) fa_fwd_kernel(int S, int H, int nh, int causal,
                                                     const __nv_bfloat16 *__restrict__ qkv,
                                                     __nv_bfloat16 *__restrict__ o,
                                                     float *__restrict__ lse) {
@@ -255,7 +264,7 @@ __global__ void fa_bwd_d_kernel(int R, int S, int H, int nh, const __nv_bfloat16
 
 // ------------------------------------------------------------ backward: dQ
 template <int D>
-__global__ void __launch_bounds__(NT) fa_bwd_dq_kernel(int S, int H, int nh, int causal,
+__global__ void __launch_bounds__(NT, 2) fa_bwd_dq_kernel(int S, int H, int nh, int causal,
                                                        const __nv_bfloat16 *__restrict__ qkv,
                                                        const __nv_bfloat16 *__restrict__ dout,
                                                        const float *__restrict__ lse,
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(NT) fa_bwd_dq_kernel(int S, int H, int nh, int
 
 // --------------------------------------------------------- backward: dK, dV
 template <int D>
-__global__ void __launch_bounds__(NT) fa_bwd_dkv_kernel(int S, int H, int nh, int causal,
+__global__ void __launch_bounds__(NT, 2) fa_bwd_dkv_kernel(int S, int H, int nh, int causal,
                                                         const __nv_bfloat16 *__restrict__ qkv,
                                                         const __nv_bfloat16 *__restrict__ dout,
                                                         const float *__restrict__ lse,
@@ -381,27 +390,31 @@ __global__ void __launch_bounds__(NT) fa_bwd_dkv_kernel(int S, int H, int nh, in
     __syncthreads();
     const bool skip = causal && qb * BT + BT - 1 < k0;   // tile entirely before these keys
     if (!skip) {
-      float p[8][4], dp[8][4];   // transposed: rows = this warp's keys, cols = queries
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int hq = 0; hq < 2; ++hq) {     // two 32-query halves (register budget)
+        if (causal && qb * BT + hq * 32 + 31 < k0) continue;
+        float p[4][4], dp[4][4];   // transposed: rows = this warp's keys, cols = queries
 #pragma unroll
-        for (int e = 0; e < 4; ++e) p[i][e] = dp[i][e] = 0.f;
-      mma_abt<D>(p, kf, Qs[cur], lane);    // S^T = K Q^T
-      mma_abt<D>(dp, vf, Os[cur], lane);   // dP^T = V dO^T
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+          for (int e = 0; e < 4; ++e) p[i][e] = dp[i][e] = 0.f;
+        mma_abt<D, 4>(p, kf, Qs[cur], lane, hq * 32);    // S^T = K Q^T
+        mma_abt<D, 4>(dp, vf, Os[cur], lane, hq * 32);   // dP^T = V dO^T
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int qi = nt * 8 + 2 * t + (e & 1);
-          const int q = qb * BT + qi;
-          const int key = k0 + g + (e >> 1) * 8;
-          float pv = exp2f(p[nt][e] * sl2 - ls[cur][qi]);
-          if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
-          p[nt][e] = pv;
-          dp[nt][e] = pv * (dp[nt][e] - dsv[cur][qi]);   // dS^T
-        }
-      mma_pt<D>(dv, p, Os[cur], lane);    // dV += P^T dO
-      mma_pt<D>(dk, dp, Qs[cur], lane);   // dK += dS^T Q
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int qi = hq * 32 + nt * 8 + 2 * t + (e & 1);
+            const int q = qb * BT + qi;
+            const int key = k0 + g + (e >> 1) * 8;
+            float pv = exp2f(p[nt][e] * sl2 - ls[cur][qi]);
+            if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
+            p[nt][e] = pv;
+            dp[nt][e] = pv * (dp[nt][e] - dsv[cur][qi]);   // dS^T
+          }
+        mma_pt<D, 2>(dv, p, Os[cur], lane, hq * 32);    // dV += P^T dO
+        mma_pt<D, 2>(dk, dp, Qs[cur], lane, hq * 32);   // dK += dS^T Q
+      }
     }
     __syncthreads();
   }
