@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbamboo.so")
+LIB_PATH = os.environ.get("BB_LIB", os.path.join(_HERE, "libbamboo.so"))   # BB_LIB: A/B builds
 
 BB_OK, BB_E_INVAL, BB_E_CUDA, BB_E_NCCL, BB_E_OOM = 0, -1, -2, -3, -4
 BB_E_PREEMPTED, BB_E_FATAL, BB_E_STATE, BB_E_UNSUPPORTED = -5, -6, -7, -8

@@ -181,25 +181,30 @@ __global__ void __launch_bounds__(NT, 2) fa_fwd_kernel(int S, int H, int nh, int
 #pragma unroll
       for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
       mma_abt<D>(s, qf, Ks[cur], lane);
+      // scores stay unscaled; masks only on the diagonal / tail tiles
+      if (kb * BT + BT > S || (causal && kb * BT + BT - 1 > q0)) {
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
+            const int row = q0 + g + (e >> 1) * 8;
+            if (key >= S || (causal && key > row)) s[nt][e] = -INFINITY;
+          }
+      }
       float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
-          const int row = q0 + g + (e >> 1) * 8;
-          float v = s[nt][e] * sl2;
-          if (key >= S || (causal && key > row)) v = -INFINITY;
-          s[nt][e] = v;
-          mx[e >> 1] = fmaxf(mx[e >> 1], v);
-        }
-      float corr[2];
+        for (int e = 0; e < 4; ++e) mx[e >> 1] = fmaxf(mx[e >> 1], s[nt][e]);
+      float corr[2], ms[2];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
         mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
         const float mn = fmaxf(m[r], mx[r]);
-        corr[r] = mn == -INFINITY ? 1.f : exp2f(m[r] - mn);
+        corr[r] = mn == -INFINITY ? 1.f : exp2f((m[r] - mn) * sl2);
+        ms[r] = mn == -INFINITY ? 0.f : mn * sl2;
         m[r] = mn;
         l[r] *= corr[r];
       }
@@ -214,8 +219,7 @@ __global__ void __launch_bounds__(NT, 2) fa_fwd_kernel(int S, int H, int nh, int
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float mr = m[e >> 1];
-          const float p = mr == -INFINITY ? 0.f : exp2f(s[nt][e] - mr);
+          const float p = exp2f(fmaf(s[nt][e], sl2, -ms[e >> 1]));   // -inf -> 0
           s[nt][e] = p;
           l[e >> 1] += p;
         }
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(NT, 2) fa_fwd_kernel(int S, int H, int nh, int
     for (int dn = 0; dn < D / 8; ++dn)
       *reinterpret_cast<uint32_t *>(orow + dn * 8 + 2 * t) =
           pack_bf16(acc[dn][2 * r] * inv, acc[dn][2 * r + 1] * inv);
-    if (t == 0) lse[((size_t)b * nh + h) * S + row] = (m[r] + log2f(l[r])) / LOG2E;
+    if (t == 0) lse[((size_t)b * nh + h) * S + row] = (m[r] * sl2 + log2f(l[r])) / LOG2E;
   }
 }
 
@@ -316,14 +320,17 @@ __global__ void __launch_bounds__(NT, 2) fa_bwd_dq_kernel(int S, int H, int nh, 
         for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
       mma_abt<D>(s, qf, Ks[cur], lane);
       mma_abt<D>(dp, df, Vs[cur], lane);
+      const bool mask = kb * BT + BT > S || q0 + 16 > S || (causal && kb * BT + BT - 1 > q0);
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
-          const int row = q0 + g + (e >> 1) * 8;
-          float p = exp2f(s[nt][e] * sl2 - lrow[e >> 1]);
-          if (key >= S || row >= S || (causal && key > row)) p = 0.f;
+          float p = exp2f(fmaf(s[nt][e], sl2, -lrow[e >> 1]));
+          if (mask) {
+            const int key = kb * BT + nt * 8 + 2 * t + (e & 1);
+            const int row = q0 + g + (e >> 1) * 8;
+            if (key >= S || row >= S || (causal && key > row)) p = 0.f;
+          }
           s[nt][e] = p * (dp[nt][e] - drow[e >> 1]);   // dS
         }
       mma_pt<D>(acc, s, Ks[cur], lane);                // dQ += dS . K
@@ -400,15 +407,19 @@ __global__ void __launch_bounds__(NT, 2) fa_bwd_dkv_kernel(int S, int H, int nh,
           for (int e = 0; e < 4; ++e) p[i][e] = dp[i][e] = 0.f;
         mma_abt<D, 4>(p, kf, Qs[cur], lane, hq * 32);    // S^T = K Q^T
         mma_abt<D, 4>(dp, vf, Os[cur], lane, hq * 32);   // dP^T = V dO^T
+        const int qlo = qb * BT + hq * 32;
+        const bool mask = qlo + 32 > S || k0 + 16 > S || (causal && k0 + 15 > qlo);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int qi = hq * 32 + nt * 8 + 2 * t + (e & 1);
-            const int q = qb * BT + qi;
-            const int key = k0 + g + (e >> 1) * 8;
-            float pv = exp2f(p[nt][e] * sl2 - ls[cur][qi]);
-            if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
+            float pv = exp2f(fmaf(p[nt][e], sl2, -ls[cur][qi]));
+            if (mask) {
+              const int q = qb * BT + qi;
+              const int key = k0 + g + (e >> 1) * 8;
+              if (q >= S || key >= S || (causal && key > q)) pv = 0.f;
+            }
             p[nt][e] = pv;
             dp[nt][e] = pv * (dp[nt][e] - dsv[cur][qi]);   // dS^T
           }
