@@ -155,6 +155,16 @@ bb_status bb_preempt(void *ctx, int stage, int at_instr);
  * victim's memory). r may be NULL. */
 bb_status bb_recover(void *ctx, bb_recovery_stats *r);
 
+/* Reconfigure back to full depth at a step boundary after a recovery
+ * (SURVEY.md §8(f)-1): the preempted node returns on its rank,
+ * receives its stage's parameters and Adam state from the shadow and its
+ * successor's (for its replica) from the successor; the shadow's copy
+ * becomes a replica again and the normal plans (with full protection)
+ * resume, so later preemptions are recoverable again. Called on every rank.
+ * BB_E_STATE unless the pipeline is in failover mode with no pending
+ * recovery. */
+bb_status bb_rejoin(void *ctx);
+
 enum { BB_STATE_PARAMS = 0, BB_STATE_GRADS = 1, BB_STATE_ADAM_M = 2, BB_STATE_ADAM_V = 3 };
 /* Copy stage `stage`'s fp32 state (what = BB_STATE_*) into host[n], n = the
  * stage's parameter count. replica = 0 reads the copy the stage runs on

@@ -245,6 +245,35 @@ class Pipeline:
         self.interrupted = None
         return self._end_step(), info
 
+    def rejoin(self):
+        """The preempted node returns at a step boundary (reconfiguration back
+        to full depth): it receives its stage's
+        parameters and Adam state from the shadow and its successor's (for its
+        replica) from the successor, reusing existing state as much as
+        possible; the shadow's copy becomes a replica again and the
+        normal plans resume. Values are unchanged by construction."""
+        if self.mode != "failover" or self.interrupted is not None:
+            raise RuntimeError("rejoin needs a recovered failover pipeline")
+        P, v = self.P, self.victim
+        u, w = (v - 1) % P, (v + 1) % P
+        node = self.nodes[v]
+        node.copies = {}
+        src = self.nodes[u].copies[v]
+        node.copies[v] = {k: (val.copy() if isinstance(val, np.ndarray) else val)
+                          for k, val in src.items()}
+        node.copies[v]["role"] = "primary"
+        sw = self.nodes[w].copies[w]
+        node.copies[w] = {k: (val.copy() if isinstance(val, np.ndarray) else val)
+                          for k, val in sw.items()}
+        node.copies[w]["role"] = "replica"
+        src["role"] = "replica"
+        self.dead.discard(v)
+        self.host[v] = v
+        self.mode = "normal"
+        self.victim = None
+        self.replica_on = {s: (s - 1) % P for s in range(P)}
+        self.plans = pl.normal_plans(P, self.M, self.rc)
+
     def dump(self):
         host, rep = (self.host, self.replica_on)
         mode = self.mode

@@ -22,7 +22,7 @@ STATE = {"params": 0, "grads": 1, "adam_m": 2, "adam_v": 3}
 
 EXPORTED = ["bb_default_opts", "bb_nccl_unique_id", "bb_init", "bb_load_params", "bb_step",
             "bb_stage_inputs",
-            "bb_preempt", "bb_recover", "bb_read_state", "bb_stage_params", "bb_schedule_dump",
+            "bb_preempt", "bb_recover", "bb_rejoin", "bb_read_state", "bb_stage_params", "bb_schedule_dump",
             "bb_recovery_dump", "bb_kernel_stats", "bb_plan_dump", "bb_last_error", "bb_destroy",
             "bb_op_gemm", "bb_op_attention_fwd", "bb_op_attention_bwd", "bb_op_layernorm_fwd",
             "bb_op_layernorm_bwd", "bb_op_cross_entropy", "bb_op_adam"]
@@ -88,6 +88,7 @@ def lib():
         _lib.bb_preempt.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         _lib.bb_stage_inputs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib.bb_recover.argtypes = [ctypes.c_void_p, ctypes.POINTER(BBRecoveryStats)]
+        _lib.bb_rejoin.argtypes = [ctypes.c_void_p]
         _lib.bb_read_state.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_void_p, ctypes.c_size_t]
         _lib.bb_stage_params.argtypes = [ctypes.c_void_p, ctypes.c_int,
@@ -243,6 +244,9 @@ class Pipeline:
         r = BBRecoveryStats()
         self._check(lib().bb_recover(self._h, ctypes.byref(r)), "bb_recover")
         return r
+
+    def rejoin(self):
+        self._check(lib().bb_rejoin(self._h), "bb_rejoin")
 
     def stage_params(self, stage):
         off, cnt = ctypes.c_size_t(), ctypes.c_size_t()

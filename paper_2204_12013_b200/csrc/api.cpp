@@ -85,6 +85,11 @@ bb_status bb_recover(void *ctx, bb_recovery_stats *r) {
   return bb::rt_recover(*static_cast<Ctx *>(ctx), r);
 }
 
+bb_status bb_rejoin(void *ctx) {
+  if (!ctx) return BB_E_INVAL;
+  return bb::rt_rejoin(*static_cast<Ctx *>(ctx));
+}
+
 bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n) {
   if (!ctx || !host) return BB_E_INVAL;
   return bb::rt_read_state(*static_cast<Ctx *>(ctx), stage, replica, what, host, n);

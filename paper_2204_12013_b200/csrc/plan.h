@@ -37,7 +37,7 @@ struct Instr {
   int stage;  // logical stage the node acts for, -1 = none
 };
 
-enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2 };
+enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2, MSG_STATE = 3 /* rejoin only */ };
 struct Msg {
   MsgKind kind;
   int mb;

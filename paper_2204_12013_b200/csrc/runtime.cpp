@@ -925,11 +925,14 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         if (a > 0) add(a, a - 1, MSG_GRAD);
         add(a, a - 2, MSG_GRAD);
         add(a, a - 1, MSG_GRADSUM);
+        add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
+        add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
       }
       size_t gmax = 0;
       for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
-      const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float)};
-      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4};
+      const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float),
+                                           3 * gmax * sizeof(float)};
+      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, 2};
       const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
       const std::string xe = xport_init(c.x, c.world, c.o.world_rank, c.o.world_size, wl,
                                         c.node_rank, slot_bytes, caps, c.o.nccl_id, hi_prio);
@@ -984,6 +987,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     if (!c.armed) {
       run(c, c.plans, nullptr, Phase{});
       sync_all(c, true);
+      ++c.steps_done;
       if (st) st->loss = read_loss(c);
       finish_stats(c, st, t0);
       return BB_OK;
@@ -1120,6 +1124,7 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
     c.failover = true;
     c.victim = v;
     c.interrupted = false;
+    ++c.steps_done;
     if (r) {
       r->victim = v;
       r->shadow = u;
@@ -1135,6 +1140,87 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
   } catch (const RtError &e) {
     c.err = e.msg;
     c.fatal = e.st != BB_E_INVAL;
+    return e.st;
+  }
+}
+
+// Reconfiguration back to full depth: the
+// returning node v receives its stage (params + Adam state) from the shadow
+// and its successor's stage (for its replica) from the successor; the
+// shadow's promoted copy becomes a replica again; normal plans resume.
+bb_status rt_rejoin(Ctx &c) {
+  try {
+    if (c.fatal) return BB_E_FATAL;
+    if (!c.failover || c.interrupted) throw RtError{BB_E_STATE, "rejoin needs a recovered failover pipeline"};
+    CK(cudaSetDevice(c.o.device));
+    c.x.barrier();
+    const int P = c.d.P, v = c.victim, u = (v - 1 + P) % P, w = (v + 1) % P;
+    auto parts = [&](Copy &cp) {
+      return std::vector<float *>{cp.master, cp.m, cp.v};
+    };
+    // senders
+    for (auto pr : std::vector<std::pair<int, int>>{{u, v}, {w, w}}) {
+      const int from = pr.first, X = pr.second;
+      if (!c.nodes.count(from)) continue;
+      Node &src = c.nodes.at(from);
+      Copy &cp = src.copies.at(X);
+      const size_t n = c.stages[X].pcount;
+      if (is_local(c, v)) {
+        Copy &dc = c.nodes.at(v).copies.at(X);
+        auto sp = parts(cp), dp = parts(dc);
+        for (int i = 0; i < 3; ++i)
+          CK(cudaMemcpyAsync(dp[i], sp[i], n * 4, cudaMemcpyDeviceToDevice, src.main));
+      } else {
+        XEdge &e = c.x.edges.at(std::make_tuple(from, v, (int)MSG_STATE));
+        const int slot = (int)(e.sent % (uint64_t)e.cap);
+        char *dst = e.peer_base + e.recv_off + (size_t)slot * e.slot_bytes;
+        wait_ev(e.stream, record(src, src.main));
+        auto sp = parts(cp);
+        for (int i = 0; i < 3; ++i)
+          CK(cudaMemcpyAsync(dst + (size_t)i * n * 4, sp[i], n * 4, cudaMemcpyDeviceToDevice, e.stream));
+        CK(cudaEventRecord(e.ev[slot], e.stream));
+        c.x.post(e);
+      }
+    }
+    sync_all(c, true);
+    // the returning node
+    if (c.nodes.count(v)) {
+      Node &nd = c.nodes.at(v);
+      for (auto pr : std::vector<std::pair<int, int>>{{u, v}, {w, w}}) {
+        const int from = pr.first, X = pr.second;
+        Copy &dc = nd.copies.at(X);
+        const size_t n = c.stages[X].pcount;
+        if (!is_local(c, from)) {
+          XEdge &e = c.x.edges.at(std::make_tuple(from, v, (int)MSG_STATE));
+          const double t0 = now_ms();
+          while (!c.x.available(e)) {
+            if (now_ms() - t0 > 300000.0) throw RtError{BB_E_STATE, "rejoin: state never arrived"};
+            std::this_thread::yield();
+          }
+          const int slot = (int)(e.consumed % (uint64_t)e.cap);
+          ++e.consumed;
+          const char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
+          wait_ev(nd.main, e.rev[slot]);
+          auto dp = parts(dc);
+          for (int i = 0; i < 3; ++i)
+            CK(cudaMemcpyAsync(dp[i], src + (size_t)i * n * 4, n * 4, cudaMemcpyDeviceToDevice, nd.main));
+        }
+        if (c.bf16) CK(k::cast_f32_to_bf16(n, dc.master, dc.work, nd.main));
+        CK(cudaMemsetAsync(dc.grad, 0, n * 4, nd.main));
+        dc.t = (int)c.steps_done;
+        dc.replica = X != v;
+      }
+      nd.alive = true;
+    }
+    if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = true;
+    sync_all(c, true);
+    c.topo = normal_topology(P, true);
+    c.plans = normal_plans(P, c.d.M, true);
+    c.failover = false;
+    c.victim = -1;
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
     return e.st;
   }
 }

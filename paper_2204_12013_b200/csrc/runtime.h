@@ -136,6 +136,7 @@ struct Ctx {
   int32_t *h_tok = nullptr, *h_tgt = nullptr, *h_csr = nullptr;
   std::vector<int> csr_U;
   size_t csr_stride = 0;
+  long long steps_done = 0;     // completed steps (identical on every rank)
   bool resident = false;        // inputs staged on every local node's device (bb_stage_inputs)
   bool resident_step = false;   // this step reuses the resident inputs (no H2D)
   std::string err;
@@ -154,6 +155,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
 bb_status rt_stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt);
 bb_status rt_preempt(Ctx &c, int stage, int at_instr);
 bb_status rt_recover(Ctx &c, bb_recovery_stats *r);
+bb_status rt_rejoin(Ctx &c);
 bb_status rt_read_state(Ctx &c, int stage, int replica, int what, float *host, size_t n);
 std::string rt_dump(const Ctx &c);
 void rt_destroy(Ctx &c);

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--out", required=True)
     ap.add_argument("--rc", type=int, default=1)
+    ap.add_argument("--events", default="", help="t:v:pi or t:rejoin, comma separated")
     a = ap.parse_args()
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -47,10 +48,19 @@ def main():
                     nccl_id=obj[0])
     p.load_params(make_params(cfg.model))
     losses, rec = [], None
+    events = {}
+    for e in filter(None, a.events.split(",")):
+        f = e.split(":")
+        events[int(f[0])] = "rejoin" if f[1] == "rejoin" else (int(f[1]), int(f[2]))
+    if a.victim >= 0:
+        events[0] = (a.victim, a.pi)
     for t in range(a.steps):
         tok, tgt = make_tokens(cfg, t)
-        if t == 0 and a.victim >= 0:
-            p.preempt(a.victim, a.pi)
+        ev = events.get(t)
+        if ev == "rejoin":
+            p.rejoin()
+        elif ev is not None:
+            p.preempt(*ev)
         status, st = p.step(tok, tgt)
         loss = st.loss
         if status == "preempted":

@@ -93,3 +93,18 @@ def test_multi_gpu_recovery_bitwise(victim, pi):
     assert str(survivor["recovery_dump"]) == opl.recovery_dump(2, cfg.microbatches, victim, pi)
     for w in state:
         assert np.array_equal(merged([survivor], 2, w), state[w]), w
+
+
+def test_multi_gpu_rejoin_sequence_bitwise():
+    """Two ranks, four nodes: preempt node 2 (cross-rank shadow), rejoin, then
+    preempt node 1, rejoin: every step equals the failure-free single-process
+    run bit for bit."""
+    import dataclasses
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    c = dataclasses.replace(get_config("C0"), stages=4)
+    ranks = run_mp(2, config="C0", stages=4, steps=6, events="0:2:13,2:rejoin,3:1:20,5:rejoin")
+    losses, state = single(c, 6)
+    assert [float(x) for x in ranks[-1]["losses"]] == [float(x) for x in losses]
+    for w in state:
+        assert np.array_equal(merged(ranks, 4, w), state[w]), w

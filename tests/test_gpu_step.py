@@ -174,3 +174,32 @@ def test_depth_reduced_c1_width_parity():
     g = _flat_state(p, cfg.stages, "grads")
     check_tensors(ref.lay, 0, ref.lay.total, g, ref.full_grads(), 1e-2, "grad")
     p.close()
+
+
+def test_c0_rejoin_and_repeated_preemptions_bitwise():
+    """C4-style sequence on the GPU: preempt, failover steps, rejoin,
+    preempt another node, rejoin... == failure-free run, bit for bit; the
+    dumps after a rejoin are the normal plans again."""
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    _, ref, _ = _run(cfg, flat, 6)
+    p = _gpu(cfg, flat, "bf16")
+    events = {0: (1, 9), 2: "rejoin", 3: (0, 17), 5: "rejoin"}
+    for t in range(6):
+        tok, tgt = make_tokens(cfg, t)
+        ev = events.get(t)
+        if ev == "rejoin":
+            p.rejoin()
+        elif ev is not None:
+            p.preempt(*ev)
+        status, st = p.step(tok, tgt)
+        loss = p.recover().loss if status == "preempted" else st.loss
+        assert loss == ref[t][0], t
+        for w in ("params", "grads", "adam_m", "adam_v"):
+            assert np.array_equal(_flat_state(p, cfg.stages, w), ref[t][1][w]), (t, w)
+    want = opl.dump(cfg.stages, cfg.microbatches, True, opl.partition(4, 2),
+                    opl.normal_plans(cfg.stages, cfg.microbatches, True))
+    assert p.schedule_dump() == want
+    for s in range(cfg.stages):   # protection restored: replica == primary again
+        assert np.array_equal(p.read_state(s, "params"), p.read_state(s, "params", replica=True))
+    p.close()

@@ -170,3 +170,33 @@ def test_no_rc_preemption_is_fatal():
     pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=False)
     with pytest.raises(pl.Fatal):
         pp.preempt(1, 3)
+
+
+def test_rejoin_and_repeated_preemptions_exact():
+    """C4-style run: preempt, run on the failover plan, rejoin,
+    preempt another node, ... equals the failure-free run exactly."""
+    r = random.Random(5)
+    for P, M in ((2, 4), (3, 3), (4, 5)):
+        cfg = tiny(P, M)
+        flat = make_params(cfg.model)
+        _, ref = _run(cfg, flat, 7)
+        pp = pipeline.Pipeline(cfg, flat, rc=True)
+        plans = pl.normal_plans(P, M, True)
+        events = {0: (r.randrange(P),), 2: "rejoin", 3: (r.randrange(P),), 5: "rejoin"}
+        for t in range(7):
+            tok, tgt = make_tokens(cfg, t)
+            ev = events.get(t)
+            if ev == "rejoin":
+                pp.rejoin()
+                assert pp.mode == "normal"
+            elif ev is not None:
+                v = ev[0]
+                pp.preempt(v, r.randint(0, len(plans[v])))
+            status, val = pp.step(tok, tgt)
+            if status == "preempted":
+                val, _ = pp.recover()
+            _same((val, pp.full_grads(), pp.full_params(), *pp.full_adam()), ref[t])
+        # after a rejoin the replicas are exact again
+        for s in range(P):
+            for key in ("p", "m", "v"):
+                assert np.array_equal(pp.nodes[s].copies[s][key], pp.nodes[(s - 1) % P].copies[s][key])
