@@ -182,7 +182,7 @@ def test_c0_rejoin_and_repeated_preemptions_bitwise():
     dumps after a rejoin are the normal plans again."""
     cfg = get_config("C0")
     flat = make_params(cfg.model)
-    _, ref, _ = _run(cfg, flat, 6)
+    _, ref, _ = _run(cfg, flat, "bf16", 6)
     p = _gpu(cfg, flat, "bf16")
     events = {0: (1, 9), 2: "rejoin", 3: (0, 17), 5: "rejoin"}
     for t in range(6):
