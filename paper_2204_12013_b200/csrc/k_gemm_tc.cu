@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "k_common.cuh"
@@ -421,6 +422,12 @@ cudaError_t launch_bn(const Gemm &g, cudaStream_t s) {
 // shapes); for fp32-accumulating dW GEMMs the fewest persistent rounds, a
 // 128-wide tile costing ~0.55 of a 256-wide one.
 cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
+  static const int force_bn = [] {   // experiments: BB_GEMM_BN=128|256
+    const char *e = std::getenv("BB_GEMM_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_bn == 128) return launch_bn<128>(g, s);
+  if (force_bn == 256 && g.N >= 256) return launch_bn<256>(g, s);
   if (g.epi != EPI_ACC_F32) return g.N >= 256 ? launch_bn<256>(g, s) : launch_bn<128>(g, s);
   static int sms = 0;
   if (!sms) {
