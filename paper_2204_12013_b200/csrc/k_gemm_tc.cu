@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "k_common.cuh"
@@ -34,14 +35,14 @@ constexpr int kEpiWarps = 8;                 // 2 per TMEM lane quarter
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 // Instruction descriptor: bf16 x bf16 -> f32, M = 128, N = BN.
-__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn, int m) {
   return (1u << 4)                    // D format f32
          | (1u << 7)                  // A bf16
          | (1u << 10)                 // B bf16
          | ((a_mn ? 1u : 0u) << 15)   // A major
          | ((b_mn ? 1u : 0u) << 16)   // B major
          | ((uint32_t)(n >> 3) << 17) // N / 8
-         | ((uint32_t)(BM >> 4) << 24);
+         | ((uint32_t)(m >> 4) << 24);
 }
 
 // Epilogue over one staged 32-row x 32-column chunk: lane l owns the column
@@ -112,26 +113,43 @@ __device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int
   }
 }
 
-template <int BN>
+// Per-CTA shared memory: a ring of (A, B) K-slabs as deep as fits, the
+// epilogue staging and the barriers. With CG = 2 a CTA holds its 128 rows of
+// A and half (BN / 2 rows) of B.
+template <int BN, int CG>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
   static constexpr int EPI_LD = 33;                       // floats per staged row (padded)
   static constexpr int EPI_BYTES = kEpiWarps * 32 * EPI_LD * 4;   // per warp 32 x 32 fp32
+  static constexpr int kMaxSmem = 232448;                 // 227 KB opt-in per CTA
+  static constexpr int FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
   static constexpr int BYTES = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// Persistent: CTA b processes output tiles b, b + gridDim.x, ... (N-fastest
-// raster so consecutive CTAs share the A slab in L2). Two TMEM accumulators
-// (2 x BN columns) let the epilogue of tile j overlap the MMAs of tile j+1.
-template <int BN, int EPI>
+// Persistent: CTA b (CTA pair b with CG = 2) processes output tiles b,
+// b + grid, ... (N-fastest raster so consecutive CTAs share the A slab in
+// L2). Two TMEM accumulators (2 x BN columns) let the epilogue of tile j
+// overlap the MMAs of tile j+1.
+//
+// CG = 2 (cluster of two CTAs on one TPC, tcgen05 cta_group::2): the pair
+// computes a 256 x BN tile with M = 256 MMAs issued by CTA 0. CTA r loads
+// rows m0 + 128 r of A and rows n0 + r BN/2 of B into its own smem; both
+// CTAs' TMA complete on CTA 0's `full` barrier (count 2: one arrive +
+// expect_tx per CTA); the MMA commit multicasts `empty` / `tfull` to both
+// CTAs; CTA r's epilogue reads its TMEM (= tile rows 128 r ..) and arrives
+// on CTA 0's `tempty` (count 2 x kEpiWarps). Each SM fetches 32 KB per
+// K slab instead of 48 KB for the same 128 x 256 x 64 MMA work: the mainloop
+// is bound by L2 -> SM bandwidth, not by the tensor pipe.
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, Gemm g, int ksplit,
                    int *__restrict__ flags, int epoch) {
-  using L = Smem<BN>;
+  using L = Smem<BN, CG>;
+  constexpr int BNH = BN / CG;                     // B rows held by this CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -146,33 +164,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      8 * (2 * L::STAGES + 4));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int pid = CG == 2 ? (int)cluster_id_x() : blockIdx.x;
+  const int npid = CG == 2 ? (int)nclusters_x() : gridDim.x;
   const int nk = (g.K + BK - 1) / BK;
-  const int tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM - 1) / BM;
+  const int tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM * CG - 1) / (BM * CG);
   const int tiles = tiles_n * tiles_m;
   // Work unit = (tile, K split). With ksplit > 1 (fp32-accumulating dW only)
   // the splits of a tile add into C in ascending split order, serialised by a
-  // per-tile flag (epoch * 16 + split): deterministic, and deadlock-free since
-  // every CTA is resident and a unit only waits for a lower-numbered unit.
+  // per-(tile, CTA) flag (epoch * 16 + split): deterministic, and deadlock-free
+  // since every CTA is resident and a unit only waits for a lower-numbered unit.
   const int units = tiles * ksplit;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
-      mbar_init(full_bar(s), 1);
+      mbar_init(full_bar(s), CG);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), kEpiWarps);   // one arrive per epilogue warp
+      mbar_init(tempty_bar(a), CG * kEpiWarps);   // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
+  if (CG == 2) cluster_sync();          // peer barriers initialised before any remote arrive
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -181,16 +210,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (both CTAs of a pair)
       int it = 0;
-      for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+      for (int unit = pid; unit < units; unit += npid) {
         const int tile = unit / ksplit, split = unit % ksplit;
         const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
-        const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+        const int m0 = (tile / tiles_n) * BM * CG + rank * BM;
+        const int nb0 = (tile % tiles_n) * BN + rank * BNH;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
-        const int na = g.a_mn ? min(BM / 64, (g.M - m0 + 63) / 64) : 1;
-        const int nb = g.b_mn ? min(BN / 64, (g.N - n0 + 63) / 64) : 1;
+        const int na = g.a_mn ? max(0, min(BM / 64, (g.M - m0 + 63) / 64)) : 1;
+        const int nb = g.b_mn ? max(0, min(BNH / 64, (g.N - nb0 + 63) / 64)) : 1;
         const uint32_t bytes = (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
                                (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -198,39 +228,58 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (it / L::STAGES) & 1;
           mbar_wait(empty_bar(s), ph ^ 1);
           const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
-          mbar_expect_tx(full_bar(s), bytes);
           const int k0 = kb * BK;
-          if (!g.a_mn) {
-            tma_load_2d(sa, &map_a, full_bar(s), k0, m0);
+          if (CG == 1) {
+            mbar_expect_tx(full_bar(s), bytes);
+            if (!g.a_mn) {
+              tma_load_2d(sa, &map_a, full_bar(s), k0, m0);
+            } else {
+              for (int j = 0; j < na; ++j)
+                tma_load_2d(sa + j * 64 * BK * 2, &map_a, full_bar(s), m0 + 64 * j, k0);
+            }
+            if (!g.b_mn) {
+              tma_load_2d(sb, &map_b, full_bar(s), k0, nb0);
+            } else {
+              for (int j = 0; j < nb; ++j)
+                tma_load_2d(sb + j * 64 * BK * 2, &map_b, full_bar(s), nb0 + 64 * j, k0);
+            }
           } else {
-            for (int j = 0; j < na; ++j)
-              tma_load_2d(sa + j * 64 * BK * 2, &map_a, full_bar(s), m0 + 64 * j, k0);
-          }
-          if (!g.b_mn) {
-            tma_load_2d(sb, &map_b, full_bar(s), k0, n0);
-          } else {
-            for (int j = 0; j < nb; ++j)
-              tma_load_2d(sb + j * 64 * BK * 2, &map_b, full_bar(s), n0 + 64 * j, k0);
+            const uint32_t fb = mapa(full_bar(s), 0);
+            mbar_arrive_expect_tx_cluster(fb, bytes);
+            if (!g.a_mn) {
+              tma_load_2d_pair(sa, &map_a, fb, k0, m0);
+            } else {
+              for (int j = 0; j < na; ++j)
+                tma_load_2d_pair(sa + j * 64 * BK * 2, &map_a, fb, m0 + 64 * j, k0);
+            }
+            if (!g.b_mn) {
+              tma_load_2d_pair(sb, &map_b, fb, k0, nb0);
+            } else {
+              for (int j = 0; j < nb; ++j)
+                tma_load_2d_pair(sb + j * 64 * BK * 2, &map_b, fb, nb0 + 64 * j, k0);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      const uint32_t idesc = instr_desc(BN, g.a_mn, g.b_mn);
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (CTA 0 of a pair)
+      const uint32_t idesc = instr_desc(BN, g.a_mn, g.b_mn, BM * CG);
       int it = 0, j = 0;
-      for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++j) {
+      for (int unit = pid; unit < units; unit += npid, ++j) {
         const int split = unit % ksplit;
         const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
         const int acc = j & 1;
-        mbar_wait(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
+        if (CG == 2) mbar_wait_cluster(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
+        else mbar_wait(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
-          mbar_wait(full_bar(s), ph);
+          if (CG == 2) mbar_wait_cluster(full_bar(s), ph);
+          else mbar_wait(full_bar(s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
 #pragma unroll
@@ -241,34 +290,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                                        : smem_desc(sa + kk * 32, 16, 1024);
             const uint64_t db = g.b_mn ? smem_desc(sb + kk * 2048, 64 * BK * 2, 1024)
                                        : smem_desc(sb + kk * 32, 16, 1024);
-            mma_bf16(d, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            if (CG == 2) mma_bf16_pair(d, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else mma_bf16(d, da, db, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(empty_bar(s));
+          if (CG == 2) mma_commit_pair(empty_bar(s), 3);
+          else mma_commit(empty_bar(s));
         }
-        mma_commit(tfull_bar(acc));
+        if (CG == 2) mma_commit_pair(tfull_bar(acc), 3);
+        else mma_commit(tfull_bar(acc));
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5): TMEM -> regs -> smem -> coalesced rows
+    // ---------------- epilogue (warps 2..9): TMEM -> regs -> smem -> coalesced rows
     const int q = warp % 4;               // TMEM lane quarter this warp may read
     const int half = (warp - 2) / 4;      // which half of the tile's columns
     float *stage = epi_smem + (warp - 2) * 32 * L::EPI_LD;
+    const uint32_t my_tempty0 = CG == 2 ? mapa(tempty_bar(0), 0) : tempty_bar(0);
     int j = 0;
-    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++j) {
+    for (int unit = pid; unit < units; unit += npid, ++j) {
       const int tile = unit / ksplit, split = unit % ksplit;
-      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      const int m0 = (tile / tiles_n) * BM * CG + rank * BM, n0 = (tile % tiles_n) * BN;
+      const int fl = tile * CG + rank;
       const int acc = j & 1;
       mbar_wait(tfull_bar(acc), (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (ksplit > 1 && split > 0) {
         if (threadIdx.x == 64) {
-          const volatile int *f = flags + tile;
+          const volatile int *f = flags + fl;
           while (*f != epoch * 16 + split) __nanosleep(64);
           __threadfence();
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
-      const int ncols = min(BN, g.N - n0);
+      const int ncols = m0 < g.M ? min(BN, g.N - n0) : 0;
 #pragma unroll 1
       for (int c = half * (BN / 2); c < min(ncols, (half + 1) * (BN / 2)); c += 32) {
         float v[32];
@@ -280,19 +334,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_bar(acc)) : "memory");
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(my_tempty0 + 8u * acc);
+        else mbar_arrive(tempty_bar(acc));
+      }
       if (ksplit > 1) {
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (threadIdx.x == 64) *(volatile int *)(flags + tile) = epoch * 16 + split + 1;
+        if (threadIdx.x == 64) *(volatile int *)(flags + fl) = epoch * 16 + split + 1;
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CG == 2) cluster_sync();          // peer MMAs / remote arrives done before dealloc / exit
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
   }
 }
 
@@ -347,44 +408,69 @@ int *split_flags(int n, int *epoch) {
   return p;
 }
 
-template <int BN, int EPI>
-cudaError_t launch(const Gemm &g, cudaStream_t s) {
-  CUtensorMap ma, mb;
-  // K-major operand: tensor {K, rows}, box {64, tile rows}; MN-major: tensor {rows, K}, box {64, 64}
-  const bool ok_a = g.a_mn ? make_map(&ma, g.A, g.M, g.K, g.lda, BK)
-                           : make_map(&ma, g.A, g.K, g.M, g.lda, BM);
-  const bool ok_b = g.b_mn ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK)
-                           : make_map(&mb, g.B, g.K, g.N, g.ldb, BN);
-  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<BN>::BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
+int num_sms() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  return sms;
+}
+
+template <int BN, int EPI, int CG>
+cudaError_t launch(const Gemm &g, cudaStream_t s) {
+  constexpr int BNH = BN / CG;
+  CUtensorMap ma, mb;
+  // K-major operand: tensor {K, rows}, box {64, tile rows}; MN-major: tensor {rows, K}, box {64, 64}
+  const bool ok_a = g.a_mn ? make_map(&ma, g.A, g.M, g.K, g.lda, BK)
+                           : make_map(&ma, g.A, g.K, g.M, g.lda, BM);
+  const bool ok_b = g.b_mn ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK)
+                           : make_map(&mb, g.B, g.K, g.N, g.ldb, BNH);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Smem<BN, CG>::BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM * CG - 1) / (BM * CG));
+  const int slots = num_sms() / CG;            // resident CTAs (pairs)
   // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU.
   const int nk = (g.K + BK - 1) / BK;
   int ksplit = 1;
-  if (EPI == EPI_ACC_F32 && tiles * 2 <= sms)
-    ksplit = std::max(1, std::min({sms / tiles, nk / 8, 8}));
+  if (EPI == EPI_ACC_F32 && tiles * 2 <= slots)
+    ksplit = std::max(1, std::min({slots / tiles, nk / 8, 8}));
   int *flags = nullptr;
   int epoch = 0;
   if (ksplit > 1) {
-    flags = split_flags(tiles, &epoch);
+    flags = split_flags(tiles * CG, &epoch);
     if (!flags) ksplit = 1;
   }
   const int units = tiles * ksplit;
-  const int grid = units < sms ? units : sms;
-  gemm_tc_kernel<BN, EPI><<<grid, kThreads, Smem<BN>::BYTES, s>>>(ma, mb, g, ksplit, flags, epoch);
+  const int grid = (units < slots ? units : slots) * CG;
+  if (CG == 1) {
+    gemm_tc_kernel<BN, EPI, CG><<<grid, kThreads, Smem<BN, CG>::BYTES, s>>>(ma, mb, g, ksplit,
+                                                                             flags, epoch);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Smem<BN, CG>::BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CG>, ma, mb, g, ksplit, flags,
+                                       epoch);
+    if (e != cudaSuccess) return e;
+  }
   ++g_launches;
   return cudaGetLastError();
 }
@@ -405,41 +491,44 @@ bool gemm_tc_supported(const Gemm &g) {
   return encode_fn() != nullptr;
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t launch_bn(const Gemm &g, cudaStream_t s) {
   switch (g.epi) {
-    case EPI_STORE: return launch<BN, EPI_STORE>(g, s);
-    case EPI_BIAS: return launch<BN, EPI_BIAS>(g, s);
-    case EPI_BIAS_RES: return launch<BN, EPI_BIAS_RES>(g, s);
-    case EPI_BIAS_GELU: return launch<BN, EPI_BIAS_GELU>(g, s);
-    case EPI_GELU_BWD: return launch<BN, EPI_GELU_BWD>(g, s);
-    case EPI_ACC_F32: return launch<BN, EPI_ACC_F32>(g, s);
-    default: return launch<BN, EPI_STORE_F32>(g, s);
+    case EPI_STORE: return launch<BN, EPI_STORE, CG>(g, s);
+    case EPI_BIAS: return launch<BN, EPI_BIAS, CG>(g, s);
+    case EPI_BIAS_RES: return launch<BN, EPI_BIAS_RES, CG>(g, s);
+    case EPI_BIAS_GELU: return launch<BN, EPI_BIAS_GELU, CG>(g, s);
+    case EPI_GELU_BWD: return launch<BN, EPI_GELU_BWD, CG>(g, s);
+    case EPI_ACC_F32: return launch<BN, EPI_ACC_F32, CG>(g, s);
+    default: return launch<BN, EPI_STORE_F32, CG>(g, s);
   }
 }
 
-// Tile width: 256 whenever N allows (measured best for the forward / dX
-// shapes); for fp32-accumulating dW GEMMs the fewest persistent rounds, a
-// 128-wide tile costing ~0.55 of a 256-wide one.
+// Tile choice. Default: 256 x 256 tiles on CTA pairs whenever N >= 256 (the
+// mainloop is L2-bandwidth bound, so halving each SM's operand traffic is
+// what raises the tensor-pipe duty cycle); 128 x 128 single-CTA tiles for
+// narrow N. BB_GEMM_TILE=pair|256|128 forces one kind (experiments / tests).
 cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
-  static const int force_bn = [] {   // experiments: BB_GEMM_BN=128|256
-    const char *e = std::getenv("BB_GEMM_BN");
-    return e ? std::atoi(e) : 0;
+  static const int force = [] {
+    const char *e = std::getenv("BB_GEMM_TILE");
+    if (!e) return 0;
+    if (!std::strcmp(e, "pair")) return 2;
+    if (!std::strcmp(e, "256")) return 256;
+    if (!std::strcmp(e, "128")) return 128;
+    return 0;
   }();
-  if (force_bn == 128) return launch_bn<128>(g, s);
-  if (force_bn == 256 && g.N >= 256) return launch_bn<256>(g, s);
-  if (g.epi != EPI_ACC_F32) return g.N >= 256 ? launch_bn<256>(g, s) : launch_bn<128>(g, s);
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  if (force == 128 || g.N < 256) return launch_bn<128, 1>(g, s);
+  if (force == 256) return launch_bn<256, 1>(g, s);
+  if (force == 2) return launch_bn<256, 2>(g, s);
+  if (g.epi != EPI_ACC_F32) return launch_bn<256, 2>(g, s);
+  // fp32-accumulating dW: the fewest persistent rounds (a 128-wide tile costs
+  // ~0.55 of a 256-wide one on one SM; a pair tile ~ one 256-wide round).
+  const int sms = num_sms();
   const long tm = (g.M + BM - 1) / BM;
   const long t256 = tm * ((g.N + 255) / 256), t128 = tm * ((g.N + 127) / 128);
   const double c256 = (double)((t256 + sms - 1) / sms), c128 = 0.55 * ((t128 + sms - 1) / sms);
-  if (g.N >= 256 && c256 <= c128) return launch_bn<256>(g, s);
-  return launch_bn<128>(g, s);
+  if (c256 <= c128) return launch_bn<256, 2>(g, s);
+  return launch_bn<128, 1>(g, s);
 }
 
 }  // namespace k

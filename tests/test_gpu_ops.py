@@ -1,6 +1,10 @@
 """Per-kernel GPU parity through the C ABI's single-op entry points, against
 the oracle's fp64 ops on the same (bf16-representable) inputs. Shapes span
 several tiles plus ragged tails, every operand layout and epilogue."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -55,9 +59,11 @@ def test_gemm_layouts(prec, impl, layout, shape):
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 6])
-def test_gemm_epilogues(prec, epi):
+@pytest.mark.parametrize("M,N,K", [(300, 200, 136), (300, 520, 136), (130, 768, 200)])
+def test_gemm_epilogues(prec, epi, M, N, K):
+    """N >= 256 runs on CTA pairs (256 x 256 tiles): ragged M leaves the
+    second CTA of the last pair partly or wholly past M."""
     import paper_2204_12013_b200 as bb
-    M, N, K = 300, 200, 136
     A, B = rnd(M, K), rnd(N, K)
     bias, res, aux = rnd(N), rnd(M, N), rnd(M, N)
     D = om.linear_fwd(A, B)
@@ -88,6 +94,18 @@ def test_gemm_epilogues(prec, epi):
         assert np.abs(host(C) - want).max() <= tol * np.abs(want).max()
         if want_aux is not None:
             assert np.abs(host(dAux) - want_aux).max() <= tol * np.abs(want_aux).max()
+
+
+@pytest.mark.skipif(os.environ.get("BB_GEMM_TILE") is not None, reason="already forced")
+@pytest.mark.parametrize("tile", ["256", "128"])
+def test_gemm_forced_single_cta_tiles(tile):
+    """The single-CTA 128 x 256 / 128 x 128 kernels (BB_GEMM_TILE) stay
+    correct: rerun the layout and epilogue tests with the tile forced."""
+    env = dict(os.environ, BB_GEMM_TILE=tile)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "test_gemm_layouts or test_gemm_epilogues"], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
