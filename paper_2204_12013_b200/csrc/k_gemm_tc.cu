@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -116,17 +117,20 @@ __device__ __forceinline__ void epi_chunk(const Gemm &g, const float *stage, int
 // Per-CTA shared memory: a ring of (A, B) K-slabs as deep as fits, the
 // epilogue staging and the barriers. With CG = 2 a CTA holds its 128 rows of
 // A and half (BN / 2 rows) of B.
-template <int BN, int CG>
+template <int BN, int CG, bool TE>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int EPI_LD = 33;                       // floats per staged row (padded)
-  static constexpr int EPI_BYTES = kEpiWarps * 32 * EPI_LD * 4;   // per warp 32 x 32 fp32
+  // TE: two 32-row x 128-byte (SW128) boxes per epilogue warp; else the
+  // padded fp32 staging of one 32 x 32 chunk per warp.
+  static constexpr int EPI_BYTES = TE ? kEpiWarps * 2 * 4096 : kEpiWarps * 32 * EPI_LD * 4;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int kMaxSmem = 232448;                 // 227 KB opt-in per CTA
-  static constexpr int FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE;
+  static constexpr int FIT = (kMaxSmem - EPI_BYTES - 1024 - BAR_BYTES) / STAGE;
   static constexpr int STAGES = FIT > 8 ? 8 : FIT;
-  static constexpr int BYTES = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int BYTES = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + BAR_BYTES;
 };
 
 // Persistent: CTA b (CTA pair b with CG = 2) processes output tiles b,
@@ -137,18 +141,20 @@ struct Smem {
 // CG = 2 (cluster of two CTAs on one TPC, tcgen05 cta_group::2): the pair
 // computes a 256 x BN tile with M = 256 MMAs issued by CTA 0. CTA r loads
 // rows m0 + 128 r of A and rows n0 + r BN/2 of B into its own smem; both
-// CTAs' TMA complete on CTA 0's `full` barrier (count 2: one arrive +
-// expect_tx per CTA); the MMA commit multicasts `empty` / `tfull` to both
+// CTAs' TMA complete on CTA 0's `full` barrier (one arrive + expect_tx for
+// both, armed by CTA 0); the MMA commit multicasts `empty` / `tfull` to both
 // CTAs; CTA r's epilogue reads its TMEM (= tile rows 128 r ..) and arrives
 // on CTA 0's `tempty` (count 2 x kEpiWarps). Each SM fetches 32 KB per
 // K slab instead of 48 KB for the same 128 x 256 x 64 MMA work: the mainloop
 // is bound by L2 -> SM bandwidth, not by the tensor pipe.
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, bool TE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, Gemm g, int ksplit,
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c,
+                   const __grid_constant__ CUtensorMap map_x, Gemm g, int ksplit,
                    int *__restrict__ flags, int epoch) {
-  using L = Smem<BN, CG>;
+  using L = Smem<BN, CG, TE>;
   constexpr int BNH = BN / CG;                     // B rows held by this CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -160,8 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto empty_bar = [&](int s) { return bars + 8u * (L::STAGES + s); };
   auto tfull_bar = [&](int a) { return bars + 8u * (2 * L::STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (2 * L::STAGES + 2 + a); };
+  auto in_bar = [&](int w, int b) { return bars + 8u * (2 * L::STAGES + 4 + 2 * w + b); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::STAGES * L::STAGE + L::EPI_BYTES +
-                                                     8 * (2 * L::STAGES + 4));
+                                                     8 * (2 * L::STAGES + 4 + 2 * kEpiWarps));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -178,13 +185,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
-      mbar_init(full_bar(s), CG);
+      mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), CG * kEpiWarps);   // one arrive per epilogue warp
     }
+    if (TE)
+      for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(in_bar(w / 2, w % 2), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -219,10 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nb0 = (tile % tiles_n) * BN + rank * BNH;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
-        const int na = g.a_mn ? max(0, min(BM / 64, (g.M - m0 + 63) / 64)) : 1;
-        const int nb = g.b_mn ? max(0, min(BNH / 64, (g.N - nb0 + 63) / 64)) : 1;
-        const uint32_t bytes = (g.a_mn ? na * 64 * BK * 2 : L::A_BYTES) +
-                               (g.b_mn ? nb * 64 * BK * 2 : L::B_BYTES);
+        auto n_boxes_a = [&](int r) { return max(0, min(BM / 64, (g.M - (m0 + (r - rank) * BM) + 63) / 64)); };
+        auto n_boxes_b = [&](int r) { return max(0, min(BNH / 64, (g.N - (nb0 + (r - rank) * BNH) + 63) / 64)); };
+        auto bytes_of = [&](int r) {
+          return (uint32_t)((g.a_mn ? n_boxes_a(r) * 64 * BK * 2 : L::A_BYTES) +
+                            (g.b_mn ? n_boxes_b(r) * 64 * BK * 2 : L::B_BYTES));
+        };
+        const int na = g.a_mn ? n_boxes_a(rank) : 1;
+        const int nb = g.b_mn ? n_boxes_b(rank) : 1;
+        // CTA 0 arms its full barrier for both CTAs' bytes (one arrive); the
+        // peer's loads only complete_tx on it (a remote arrive per slab would
+        // serialise the peer's producer behind a cluster-scope release).
+        const uint32_t bytes = CG == 1 ? bytes_of(0) : bytes_of(0) + bytes_of(1);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
@@ -245,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             const uint32_t fb = mapa(full_bar(s), 0);
-            mbar_arrive_expect_tx_cluster(fb, bytes);
+            if (rank == 0) mbar_expect_tx(full_bar(s), bytes);
             if (!g.a_mn) {
               tma_load_2d_pair(sa, &map_a, fb, k0, m0);
             } else {
@@ -278,8 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
-          if (CG == 2) mbar_wait_cluster(full_bar(s), ph);
-          else mbar_wait(full_bar(s), ph);
+          mbar_wait(full_bar(s), ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
 #pragma unroll
@@ -300,8 +316,179 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mma_commit(tfull_bar(acc));
       }
     }
+  } else if (TE) {
+    // ---------------- epilogue, TMA flavour (warps 2..9). Warp w owns tile rows
+    // 32 (w % 4).. (its TMEM lane quarter) and one half of the columns, in
+    // chunks of 128 bytes per row (64 bf16 / 32 fp32 columns): tcgen05.ld ->
+    // fused math -> 128B-swizzled smem box -> one TMA store (or TMA fp32
+    // add-reduction for EPI_ACC_F32). Row operands (residual / GELU input) are
+    // TMA-loaded into the same box ahead of use, the first chunk's while the
+    // tile's MMAs still run. Two boxes per warp alternate so the store of one
+    // chunk overlaps the math of the next. TMA clips rows / columns past M / N.
+    constexpr bool F32OUT = EPI == EPI_ACC_F32 || EPI == EPI_STORE_F32;
+    constexpr int CW = F32OUT ? 32 : 64;
+    constexpr bool HAS_IN = EPI == EPI_BIAS_RES || EPI == EPI_GELU_BWD;
+    constexpr bool HAS_BIAS = EPI == EPI_BIAS || EPI == EPI_BIAS_RES || EPI == EPI_BIAS_GELU;
+    constexpr int NCH = (BN / 2) / CW;
+    const int q = warp % 4, half = (warp - 2) / 4, ew = warp - 2;
+    const uint32_t box0 = base + L::STAGES * L::STAGE + ew * 8192;
+    const uint32_t rowoff = lane * 128;
+    const uint32_t my_tempty0 = CG == 2 ? mapa(tempty_bar(0), 0) : tempty_bar(0);
+    uint32_t inph = 0;                    // parity bit per box of in_bar
+    int bsel = 0;
+    int j = 0;
+    for (int unit = pid; unit < units; unit += npid, ++j) {
+      const int tile = unit / ksplit, split = unit % ksplit;
+      const int m0 = (tile / tiles_n) * BM * CG + rank * BM, n0 = (tile % tiles_n) * BN;
+      const int fl = tile * CG + rank;
+      const int acc = j & 1;
+      const int mr = m0 + q * 32;                         // this warp's first row
+      const int nw = n0 + half * (BN / 2);                // this warp's first column
+      const bool live = mr < g.M && nw < g.N;
+      if (HAS_IN && live && lane == 0) {                  // prefetch chunk 0's row operand
+        bulk_wait_read<0>();
+        mbar_expect_tx(in_bar(ew, bsel), 4096);
+        tma_load_2d(box0 + bsel * 4096, &map_x, in_bar(ew, bsel), nw, mr);
+      }
+      mbar_wait(tfull_bar(acc), (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (ksplit > 1 && split > 0) {
+        if (threadIdx.x == 64) {
+          const volatile int *f = flags + fl;
+          while (*f != epoch * 16 + split) __nanosleep(64);
+          __threadfence();
+          asm volatile("fence.proxy.async;" ::: "memory");
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int n = nw + ch * CW;
+        const bool go = live && n < g.N;
+        const int b = bsel;
+        if (go) {
+          if (lane == 0) {
+            if (HAS_IN) {
+              if (ch + 1 < NCH && n + CW < g.N) {         // prefetch the next chunk's operand
+                bulk_wait_read<0>();
+                mbar_expect_tx(in_bar(ew, b ^ 1), 4096);
+                tma_load_2d(box0 + (b ^ 1) * 4096, &map_x, in_bar(ew, b ^ 1), n + CW, mr);
+              }
+            } else if (EPI == EPI_BIAS_GELU) {
+              bulk_wait_read<0>();                        // both boxes are written below
+            } else {
+              bulk_wait_read<1>();                        // box b's previous store has read it
+            }
+          }
+          __syncwarp();
+        }
+        uint32_t r0[32], r1[32];
+        if (go) {
+          const uint32_t t = tmem + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2) + ch * CW;
+          tmem_ld32_nowait(t, r0);
+          if (!F32OUT) tmem_ld32_nowait(t + 32, r1);
+          tmem_wait_ld();
+          tmem_pin(r0);
+          if (!F32OUT) tmem_pin(r1);
+        }
+        if (ch == NCH - 1 || !go) {
+          // all TMEM reads of this accumulator done: release it to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        }
+        if (!go) break;
+        if (HAS_IN) {
+          mbar_wait(in_bar(ew, b), (inph >> b) & 1);
+          inph ^= 1u << b;
+        }
+        const uint32_t box = box0 + b * 4096;
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {               // 16-byte chunk of this lane's row
+          const uint32_t addr = box + rowoff + ((c16 ^ (lane & 7)) << 4);
+          if (F32OUT) {
+            st_shared_v4(addr, r0[4 * c16], r0[4 * c16 + 1], r0[4 * c16 + 2], r0[4 * c16 + 3]);
+          } else {
+            float x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              x[i] = __uint_as_float(c16 < 4 ? r0[8 * c16 + i] : r1[8 * (c16 - 4) + i]);
+            if (HAS_BIAS) {
+              const int nb = n + 8 * c16;
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                float2 bv = make_float2(0.f, 0.f);
+                if (nb + i < g.N)
+                  bv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(
+                      reinterpret_cast<const __nv_bfloat16 *>(g.bias) + nb + i));
+                x[i] += bv.x;
+                x[i + 1] += bv.y;
+              }
+            }
+            uint32_t o[4];
+            if (HAS_IN) {
+              const uint4 in = ld_shared_v4(addr);
+              const uint32_t iw[4] = {in.x, in.y, in.z, in.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&iw[i]));
+                float y0, y1;
+                if (EPI == EPI_BIAS_RES) {
+                  y0 = x[2 * i] + p.x;
+                  y1 = x[2 * i + 1] + p.y;
+                } else {
+                  y0 = x[2 * i] * gelu_grad_fast(p.x);
+                  y1 = x[2 * i + 1] * gelu_grad_fast(p.y);
+                }
+                __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
+                o[i] = *reinterpret_cast<uint32_t *>(&h);
+              }
+            } else if (EPI == EPI_BIAS_GELU) {
+              uint32_t pa[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                __nv_bfloat162 hp = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+                pa[i] = *reinterpret_cast<uint32_t *>(&hp);
+                __nv_bfloat162 h = __floats2bfloat162_rn(gelu_fast(x[2 * i]), gelu_fast(x[2 * i + 1]));
+                o[i] = *reinterpret_cast<uint32_t *>(&h);
+              }
+              st_shared_v4(box0 + (b ^ 1) * 4096 + rowoff + ((c16 ^ (lane & 7)) << 4), pa[0], pa[1],
+                           pa[2], pa[3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+                o[i] = *reinterpret_cast<uint32_t *>(&h);
+              }
+            }
+            st_shared_v4(addr, o[0], o[1], o[2], o[3]);
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (EPI == EPI_ACC_F32) tma_reduce_add_2d(&map_c, box, n, mr);
+          else tma_store_2d(&map_c, box, n, mr);
+          if (EPI == EPI_BIAS_GELU) tma_store_2d(&map_x, box0 + (b ^ 1) * 4096, n, mr);
+          bulk_commit();
+        }
+        bsel ^= 1;
+      }
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(my_tempty0 + 8u * acc);
+        else mbar_arrive(tempty_bar(acc));
+      }
+      if (ksplit > 1) {
+        if (lane == 0) {
+          bulk_wait<0>();                                 // this warp's adds are performed
+          asm volatile("fence.proxy.async;" ::: "memory");
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (threadIdx.x == 64) *(volatile int *)(flags + fl) = epoch * 16 + split + 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();                        // smem boxes read before exit
   } else {
-    // ---------------- epilogue (warps 2..9): TMEM -> regs -> smem -> coalesced rows
+    // ---------------- epilogue, LSU flavour (warps 2..9): TMEM -> regs -> smem -> coalesced rows
     const int q = warp % 4;               // TMEM lane quarter this warp may read
     const int half = (warp - 2) / 4;      // which half of the tile's columns
     float *stage = epi_smem + (warp - 2) * 32 * L::EPI_LD;
@@ -387,6 +574,23 @@ bool make_map(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, u
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Epilogue box map: {inner, outer} elements of `es` bytes, row pitch ld
+// elements, box {128 / es, 32}, 128B swizzle (the epilogue's smem box layout).
+bool make_epi_map(CUtensorMap *m, const void *ptr, bool f32, uint64_t inner, uint64_t outer,
+                  uint64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
+  cuuint32_t el[2] = {1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void *>(ptr), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Per-launch slice of a device flag ring for serialised split-K; every launch
 // gets a fresh epoch, so flags never need resetting.
 int *split_flags(int n, int *epoch) {
@@ -418,26 +622,64 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int EPI, int CG>
+template <int BN, int EPI, int CG, bool TE>
 cudaError_t launch(const Gemm &g, cudaStream_t s) {
   constexpr int BNH = BN / CG;
-  CUtensorMap ma, mb;
+  using L = Smem<BN, CG, TE>;
+  auto kern = gemm_tc_kernel<BN, EPI, CG, TE>;
+  CUtensorMap ma, mb, mc, mx;
   // K-major operand: tensor {K, rows}, box {64, tile rows}; MN-major: tensor {rows, K}, box {64, 64}
   const bool ok_a = g.a_mn ? make_map(&ma, g.A, g.M, g.K, g.lda, BK)
                            : make_map(&ma, g.A, g.K, g.M, g.lda, BM);
   const bool ok_b = g.b_mn ? make_map(&mb, g.B, g.N, g.K, g.ldb, BK)
                            : make_map(&mb, g.B, g.K, g.N, g.ldb, BNH);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  constexpr bool F32OUT = EPI == EPI_ACC_F32 || EPI == EPI_STORE_F32;
+  if (TE) {
+    if (!make_epi_map(&mc, g.C, F32OUT, g.N, g.M, g.ldc)) return cudaErrorInvalidValue;
+    const void *x = EPI == EPI_BIAS_RES ? g.res : g.aux;
+    if (EPI == EPI_BIAS_RES || EPI == EPI_GELU_BWD || EPI == EPI_BIAS_GELU) {
+      if (!make_epi_map(&mx, x, false, g.N, g.M, g.ldc)) return cudaErrorInvalidValue;
+    } else {
+      mx = mc;
+    }
+  } else {
+    mc = ma;
+    mx = ma;
+  }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CG>,
+    cudaError_t e = cudaFuncSetAttribute(kern,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Smem<BN, CG>::BYTES);
+                                         L::BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((g.N + BN - 1) / BN) * ((g.M + BM * CG - 1) / (BM * CG));
-  const int slots = num_sms() / CG;            // resident CTAs (pairs)
+  // Resident CTAs (pairs): a pair needs both SMs of one TPC free, and not
+  // every TPC has two usable SMs, so ask the occupancy calculator.
+  static int slots = 0;
+  if (!slots) {
+    slots = num_sms() / CG;
+    if (CG > 1) {
+      cudaLaunchConfig_t oc = {};
+      oc.gridDim = dim3(CG * slots);
+      oc.blockDim = dim3(kThreads);
+      oc.dynamicSmemBytes = L::BYTES;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = CG;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      oc.attrs = &at;
+      oc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &oc) == cudaSuccess &&
+          n > 0)
+        slots = std::min(slots, n);
+      if (std::getenv("BB_DEBUG")) fprintf(stderr, "[bb] gemm pair slots %d\n", slots);
+    }
+  }
   // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU.
   const int nk = (g.K + BK - 1) / BK;
   int ksplit = 1;
@@ -452,13 +694,12 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
   const int units = tiles * ksplit;
   const int grid = (units < slots ? units : slots) * CG;
   if (CG == 1) {
-    gemm_tc_kernel<BN, EPI, CG><<<grid, kThreads, Smem<BN, CG>::BYTES, s>>>(ma, mb, g, ksplit,
-                                                                             flags, epoch);
+    kern<<<grid, kThreads, L::BYTES, s>>>(ma, mb, mc, mx, g, ksplit, flags, epoch);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Smem<BN, CG>::BYTES;
+    cfg.dynamicSmemBytes = L::BYTES;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -467,8 +708,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CG>, ma, mb, g, ksplit, flags,
-                                       epoch);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g, ksplit, flags, epoch);
     if (e != cudaSuccess) return e;
   }
   ++g_launches;
@@ -491,23 +731,37 @@ bool gemm_tc_supported(const Gemm &g) {
   return encode_fn() != nullptr;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool TE>
 cudaError_t launch_bn(const Gemm &g, cudaStream_t s) {
   switch (g.epi) {
-    case EPI_STORE: return launch<BN, EPI_STORE, CG>(g, s);
-    case EPI_BIAS: return launch<BN, EPI_BIAS, CG>(g, s);
-    case EPI_BIAS_RES: return launch<BN, EPI_BIAS_RES, CG>(g, s);
-    case EPI_BIAS_GELU: return launch<BN, EPI_BIAS_GELU, CG>(g, s);
-    case EPI_GELU_BWD: return launch<BN, EPI_GELU_BWD, CG>(g, s);
-    case EPI_ACC_F32: return launch<BN, EPI_ACC_F32, CG>(g, s);
-    default: return launch<BN, EPI_STORE_F32, CG>(g, s);
+    case EPI_STORE: return launch<BN, EPI_STORE, CG, TE>(g, s);
+    case EPI_BIAS: return launch<BN, EPI_BIAS, CG, TE>(g, s);
+    case EPI_BIAS_RES: return launch<BN, EPI_BIAS_RES, CG, TE>(g, s);
+    case EPI_BIAS_GELU: return launch<BN, EPI_BIAS_GELU, CG, TE>(g, s);
+    case EPI_GELU_BWD: return launch<BN, EPI_GELU_BWD, CG, TE>(g, s);
+    case EPI_ACC_F32: return launch<BN, EPI_ACC_F32, CG, TE>(g, s);
+    default: return launch<BN, EPI_STORE_F32, CG, TE>(g, s);
   }
 }
 
-// Tile choice. Default: 256 x 256 tiles on CTA pairs whenever N >= 256 (the
-// mainloop is L2-bandwidth bound, so halving each SM's operand traffic is
-// what raises the tensor-pipe duty cycle); 128 x 128 single-CTA tiles for
-// narrow N. BB_GEMM_TILE=pair|256|128 forces one kind (experiments / tests).
+// The TMA epilogue needs 16-byte aligned C / residual / aux bases and row
+// pitches (tensor-map rules); anything else takes the LSU epilogue.
+bool tma_epilogue_ok(const Gemm &g) {
+  const bool f32 = g.epi == EPI_ACC_F32 || g.epi == EPI_STORE_F32;
+  const uintptr_t mask = reinterpret_cast<uintptr_t>(g.C) |
+                         (g.epi == EPI_BIAS_RES ? reinterpret_cast<uintptr_t>(g.res) : 0) |
+                         (g.epi == EPI_BIAS_GELU || g.epi == EPI_GELU_BWD
+                              ? reinterpret_cast<uintptr_t>(g.aux) : 0);
+  if (mask & 15) return false;
+  return ((size_t)g.ldc * (f32 ? 4 : 2)) % 16 == 0;
+}
+
+// Tile choice. Default: 256 x 256 tiles on CTA pairs with the TMA epilogue
+// whenever N >= 256 and the epilogue operands are 16-byte aligned (the
+// mainloop is L2 / smem bandwidth bound, so halving each SM's operand
+// traffic is what raises the tensor-pipe duty cycle); otherwise single-CTA
+// 128 x 256 / 128 x 128 tiles. BB_GEMM_TILE=pair|256|128 and BB_GEMM_EPI=lsu
+// force a kind (experiments / tests).
 cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
   static const int force = [] {
     const char *e = std::getenv("BB_GEMM_TILE");
@@ -517,18 +771,24 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     if (!std::strcmp(e, "128")) return 128;
     return 0;
   }();
-  if (force == 128 || g.N < 256) return launch_bn<128, 1>(g, s);
-  if (force == 256) return launch_bn<256, 1>(g, s);
-  if (force == 2) return launch_bn<256, 2>(g, s);
-  if (g.epi != EPI_ACC_F32) return launch_bn<256, 2>(g, s);
+  static const bool lsu = [] {
+    const char *e = std::getenv("BB_GEMM_EPI");
+    return e && !std::strcmp(e, "lsu");
+  }();
+  const bool te = !lsu && tma_epilogue_ok(g);
+  if (force == 128 || g.N < 256)
+    return te ? launch_bn<128, 1, true>(g, s) : launch_bn<128, 1, false>(g, s);
+  if (force == 256) return te ? launch_bn<256, 1, true>(g, s) : launch_bn<256, 1, false>(g, s);
+  if (!te) return launch_bn<256, 1, false>(g, s);
+  if (force == 2 || g.epi != EPI_ACC_F32) return launch_bn<256, 2, true>(g, s);
   // fp32-accumulating dW: the fewest persistent rounds (a 128-wide tile costs
   // ~0.55 of a 256-wide one on one SM; a pair tile ~ one 256-wide round).
   const int sms = num_sms();
   const long tm = (g.M + BM - 1) / BM;
   const long t256 = tm * ((g.N + 255) / 256), t128 = tm * ((g.N + 127) / 128);
   const double c256 = (double)((t256 + sms - 1) / sms), c128 = 0.55 * ((t128 + sms - 1) / sms);
-  if (c256 <= c128) return launch_bn<256, 2>(g, s);
-  return launch_bn<128, 1>(g, s);
+  if (c256 <= c128) return launch_bn<256, 2, true>(g, s);
+  return launch_bn<128, 1, true>(g, s);
 }
 
 }  // namespace k

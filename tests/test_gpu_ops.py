@@ -96,12 +96,15 @@ def test_gemm_epilogues(prec, epi, M, N, K):
             assert np.abs(host(dAux) - want_aux).max() <= tol * np.abs(want_aux).max()
 
 
-@pytest.mark.skipif(os.environ.get("BB_GEMM_TILE") is not None, reason="already forced")
-@pytest.mark.parametrize("tile", ["256", "128"])
-def test_gemm_forced_single_cta_tiles(tile):
-    """The single-CTA 128 x 256 / 128 x 128 kernels (BB_GEMM_TILE) stay
-    correct: rerun the layout and epilogue tests with the tile forced."""
-    env = dict(os.environ, BB_GEMM_TILE=tile)
+@pytest.mark.skipif(os.environ.get("BB_GEMM_TILE") is not None or
+                    os.environ.get("BB_GEMM_EPI") is not None, reason="already forced")
+@pytest.mark.parametrize("force", [("BB_GEMM_TILE", "256"), ("BB_GEMM_TILE", "128"),
+                                   ("BB_GEMM_EPI", "lsu")])
+def test_gemm_forced_variants(force):
+    """The other GEMM kernels stay correct: single-CTA 128 x 256 / 128 x 128
+    tiles (BB_GEMM_TILE) and the LSU epilogue (BB_GEMM_EPI=lsu, taken for
+    unaligned operands): rerun the layout and epilogue tests forced."""
+    env = dict(os.environ, **{force[0]: force[1]})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
                         "test_gemm_layouts or test_gemm_epilogues"], env=env,
                        capture_output=True, text=True, timeout=900)
