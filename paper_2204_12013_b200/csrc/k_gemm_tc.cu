@@ -780,15 +780,13 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     return te ? launch_bn<128, 1, true>(g, s) : launch_bn<128, 1, false>(g, s);
   if (force == 256) return te ? launch_bn<256, 1, true>(g, s) : launch_bn<256, 1, false>(g, s);
   if (!te) return launch_bn<256, 1, false>(g, s);
-  if (force == 2 || g.epi != EPI_ACC_F32) return launch_bn<256, 2, true>(g, s);
-  // fp32-accumulating dW: the fewest persistent rounds (a 128-wide tile costs
-  // ~0.55 of a 256-wide one on one SM; a pair tile ~ one 256-wide round).
-  const int sms = num_sms();
-  const long tm = (g.M + BM - 1) / BM;
-  const long t256 = tm * ((g.N + 255) / 256), t128 = tm * ((g.N + 127) / 128);
-  const double c256 = (double)((t256 + sms - 1) / sms), c128 = 0.55 * ((t128 + sms - 1) / sms);
-  if (c256 <= c128) return launch_bn<256, 2, true>(g, s);
-  return launch_bn<128, 1, true>(g, s);
+  // fp32-accumulating dW with few output tiles: the serialised split-K chain
+  // (up to 8 links of a few us each on pairs) costs more than the smaller
+  // tiles' lower rate, so take 128 x 128 tiles (shorter chains) there.
+  if (force != 2 && g.epi == EPI_ACC_F32 &&
+      (long)((g.M + 255) / 256) * ((g.N + 255) / 256) < 16)
+    return launch_bn<128, 1, true>(g, s);
+  return launch_bn<256, 2, true>(g, s);
 }
 
 }  // namespace k

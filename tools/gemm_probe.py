@@ -34,7 +34,19 @@ for _ in range(30):
     ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
 us = ts[len(ts) // 2]
-print(f"{M}x{N}x{K} a_mn={amn} b_mn={bmn} epi={epi}: {us:8.1f} us {2*M*N*K/us/1e6:7.1f} TF/s")
+# back-to-back batch: device time per launch with the queue kept full
+import time
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda._sleep(20_000_000)   # ~10 ms of GPU spin so the host runs ahead
+a.record()
+h0 = time.perf_counter()
+for _ in range(50): f()
+h1 = time.perf_counter()
+b.record(); torch.cuda.synchronize()
+bus = a.elapsed_time(b) * 1e3 / 50
+print(f"{M}x{N}x{K} a_mn={amn} b_mn={bmn} epi={epi}: {us:8.1f} us single, {bus:8.1f} us batched"
+      f" {2*M*N*K/bus/1e6:7.1f} TF/s, host {1e6*(h1-h0)/50:5.1f} us/launch")
 '''
 
 
