@@ -225,13 +225,12 @@ bb_status bb_op_layernorm_bwd(int prec, int R, int H, const float *dy, const voi
   const bool b16 = prec == BB_PREC_BF16;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float *part = nullptr;
-  if (cudaMallocAsync((void **)&part, bb::k::colreduce_partial_floats(R, H) * 4, s) != cudaSuccess)
-    return BB_E_OOM;
-  cudaError_t e = bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, nullptr, dx,
-                                          nullptr, s);
-  if (e == cudaSuccess) e = bb::k::colreduce(b16, true, 1, R, H, dy, x, mean, rstd, part, dg, s);
+  const size_t pb = bb::k::colreduce_partial_floats(R, H) * 4;
+  if (cudaMallocAsync((void **)&part, pb, s) != cudaSuccess) return BB_E_OOM;
+  cudaError_t e = cudaMemsetAsync(part, 0, pb, s);
   if (e == cudaSuccess)
-    e = bb::k::colreduce(b16, true, 0, R, H, dy, nullptr, nullptr, nullptr, part, db, s);
+    e = bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, nullptr, dx, nullptr, s);
+  if (e == cudaSuccess) e = bb::k::colreduce_ln(b16, R, H, dy, x, mean, rstd, part, dg, db, s);
   cudaFreeAsync(part, s);
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }

@@ -248,46 +248,77 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
 
 // Column reduction, 8 columns per thread: block = 8 warps x 32 lanes covers
 // 256 columns x CRV_ROWS rows (warp w takes rows w, w+8, ...); the 8 warp
-// partials are added in a fixed order through shared memory.
+// partials are added in a fixed order through shared memory and written to
+// part[row block]. The last block of a column block to arrive (atomic ticket)
+// then adds all row-block partials in ascending order into out: one launch,
+// deterministic whatever the arrival order. out1 (if any) gets the LN-gamma
+// form sum a * xhat, out0 (if any) the plain sum.
 constexpr int CRV_ROWS = 64;
 template <typename TA, typename T>
-__global__ void __launch_bounds__(256) colreduce_vec_kernel(int mode, int R, int N,
+__global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int chunks,
                                                             const TA *__restrict__ A,
                                                             const T *__restrict__ X,
                                                             const float *__restrict__ mean,
                                                             const float *__restrict__ rstd,
-                                                            float *__restrict__ part) {
+                                                            float *__restrict__ part,
+                                                            unsigned *__restrict__ tickets,
+                                                            float *__restrict__ out0,
+                                                            float *__restrict__ out1) {
   __shared__ float sh[8][256];   // 8 warps x 256 columns
+  __shared__ bool last;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = (blockIdx.x * 32 + lane) * 8;
   const int r0 = blockIdx.y * CRV_ROWS, r1 = min(R, r0 + CRV_ROWS);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float a0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float a1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (n < N) {
     for (int r = r0 + warp; r < r1; r += 8) {
       const size_t idx = (size_t)r * N + n;
       const V8 a = ld8(A + idx);
-      if (mode == 1) {
+      if (out1) {
         const V8 xx = ld8(X + idx);
         const float mu = mean[r], rs = rstd[r];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += a.v[i] * ((xx.v[i] - mu) * rs);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += a.v[i];
+        for (int i = 0; i < 8; ++i) a1[i] += a.v[i] * ((xx.v[i] - mu) * rs);
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a0[i] += a.v[i];
     }
   }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) sh[warp][lane * 8 + i] = acc[i];
-  __syncthreads();
   const int c = threadIdx.x;   // 256 columns of this block
   const int nn = blockIdx.x * 256 + c;
-  if (nn < N) {
-    float s = 0.f;
+  const size_t plane = (size_t)chunks * N;          // part[0] = plain sums, part[plane] = gamma form
+  for (int w2 = 0; w2 < 2; ++w2) {
+    float *o = w2 ? out1 : out0;
+    if (!o) continue;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s += sh[w][c];
-    part[(size_t)blockIdx.y * N + nn] = s;
+    for (int i = 0; i < 8; ++i) sh[warp][lane * 8 + i] = w2 ? a1[i] : a0[i];
+    __syncthreads();
+    if (nn < N) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += sh[w][c];
+      part[w2 * plane + (size_t)blockIdx.y * N + nn] = s;
+    }
+    __syncthreads();
   }
+  __threadfence();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == (unsigned)chunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (nn < N) {
+    for (int w2 = 0; w2 < 2; ++w2) {
+      float *o = w2 ? out1 : out0;
+      if (!o) continue;
+      const float *p = part + w2 * plane + nn;
+      float s = 0.f;
+#pragma unroll 8
+      for (int ch = 0; ch < chunks; ++ch) s += __ldcg(p + (size_t)ch * N);
+      o[nn] += s;
+    }
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;   // ready for the next call on this buffer
 }
 
 // -------------------------------------------------------------- embedding
@@ -504,41 +535,64 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
   return cudaGetLastError();
 }
 
+// Layout of `partial`: kTickets arrival counters first (fixed place whatever
+// N a call uses), then 2 planes of row-block partials.
+constexpr int kTickets = 256;   // column blocks of 256: N <= 65536
 size_t colreduce_partial_floats(int R, int N) {
-  return (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;   // >= the vectorized kernel's need
+  return kTickets + 2 * (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;
+}
+
+template <typename TA, typename T>
+void colreduce_vec(int R, int N, const void *A, const void *X, const float *mean,
+                   const float *rstd, float *partial, float *out0, float *out1, cudaStream_t s) {
+  const int chunks = (R + CRV_ROWS - 1) / CRV_ROWS;
+  unsigned *tickets = reinterpret_cast<unsigned *>(partial);
+  dim3 grid((N + 255) / 256, chunks);
+  colreduce_vec_kernel<TA, T><<<grid, 256, 0, s>>>(R, N, chunks, cp<TA>(A), cp<T>(X), mean, rstd,
+                                                   partial + kTickets, tickets, out0, out1);
+  ++g_launches;
+}
+
+cudaError_t colreduce_ln(bool bf16, int R, int N, const float *A, const void *X, const float *mean,
+                         const float *rstd, float *partial, float *out_g, float *out_b,
+                         cudaStream_t s) {
+  if (N % 8 != 0) {
+    cudaError_t e = colreduce(bf16, true, 1, R, N, A, X, mean, rstd, partial, out_g, s);
+    if (e != cudaSuccess) return e;
+    return colreduce(bf16, true, 0, R, N, A, nullptr, nullptr, nullptr, partial, out_b, s);
+  }
+  if (bf16)
+    colreduce_vec<float, __nv_bfloat16>(R, N, A, X, mean, rstd, partial, out_b, out_g, s);
+  else
+    colreduce_vec<float, float>(R, N, A, X, mean, rstd, partial, out_b, out_g, s);
+  return cudaGetLastError();
 }
 
 cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void *A, const void *X,
                       const float *mean, const float *rstd, float *partial, float *out,
                       cudaStream_t s) {
   if (N % 8 == 0) {
-    const int chunks = (R + CRV_ROWS - 1) / CRV_ROWS;
-    dim3 grid((N + 255) / 256, chunks);
+    float *o0 = mode == 0 ? out : nullptr, *o1 = mode == 1 ? out : nullptr;
     if (bf16 && a_f32)
-      colreduce_vec_kernel<float, __nv_bfloat16><<<grid, 256, 0, s>>>(
-          mode, R, N, cp<float>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+      colreduce_vec<float, __nv_bfloat16>(R, N, A, X, mean, rstd, partial, o0, o1, s);
     else if (bf16)
-      colreduce_vec_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
-          mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+      colreduce_vec<__nv_bfloat16, __nv_bfloat16>(R, N, A, X, mean, rstd, partial, o0, o1, s);
     else
-      colreduce_vec_kernel<float, float><<<grid, 256, 0, s>>>(mode, R, N, cp<float>(A),
-                                                              cp<float>(X), mean, rstd, partial);
-    colreduce_final_kernel<<<(N + 31) / 32, 256, 0, s>>>(chunks, N, partial, out);
-    g_launches += 2;
+      colreduce_vec<float, float>(R, N, A, X, mean, rstd, partial, o0, o1, s);
     return cudaGetLastError();
   }
   const int chunks = (R + CR_ROWS - 1) / CR_ROWS;
   dim3 grid((N + CR_COLS - 1) / CR_COLS, chunks);
   if (bf16 && a_f32)
     colreduce_partial_kernel<float, __nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
-        mode, R, N, cp<float>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+        mode, R, N, cp<float>(A), cp<__nv_bfloat16>(X), mean, rstd, partial + kTickets);
   else if (bf16)
     colreduce_partial_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, CR_COLS, 0, s>>>(
-        mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial);
+        mode, R, N, cp<__nv_bfloat16>(A), cp<__nv_bfloat16>(X), mean, rstd, partial + kTickets);
   else
     colreduce_partial_kernel<float, float><<<grid, CR_COLS, 0, s>>>(
-        mode, R, N, cp<float>(A), cp<float>(X), mean, rstd, partial);
-  colreduce_final_kernel<<<(N + 31) / 32, 256, 0, s>>>(chunks, N, partial, out);
+        mode, R, N, cp<float>(A), cp<float>(X), mean, rstd, partial + kTickets);
+  colreduce_final_kernel<<<(N + 31) / 32, 256, 0, s>>>(chunks, N, partial + kTickets, out);
   g_launches += 2;
   return cudaGetLastError();
 }

@@ -49,14 +49,22 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
                              const float *mean, const float *rstd, const void *g,
                              const float *dres32, const void *dresT, void *dxT, float *dx32,
                              cudaStream_t s);
-// Deterministic column reductions, two passes through `partial` (>= colreduce_partial_floats):
+// Deterministic column reductions through `partial` (>= colreduce_partial_floats
+// floats, ZERO-INITIALISED once at allocation: its tail holds self-resetting
+// arrival counters):
 //   mode 0: out[n] += sum_r A[r][n]                     (bias gradient)
 //   mode 1: out[n] += sum_r A[r][n] * (X[r][n]-mean[r])*rstd[r]   (LN gamma gradient)
+// One launch when N % 8 == 0: row-block partials, and the last row block to
+// arrive at a column block adds the partials in ascending row-block order.
 size_t colreduce_partial_floats(int R, int N);
 // a_f32: A is fp32 (else storage type); X is always storage type.
 cudaError_t colreduce(bool bf16, bool a_f32, int mode, int R, int N, const void *A, const void *X,
                       const float *mean, const float *rstd, float *partial, float *out,
                       cudaStream_t s);
+// Both LN parameter gradients in one pass over fp32 dA: out_g (mode 1), out_b (mode 0).
+cudaError_t colreduce_ln(bool bf16, int R, int N, const float *A, const void *X, const float *mean,
+                         const float *rstd, float *partial, float *out_g, float *out_b,
+                         cudaStream_t s);
 
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s);

@@ -357,10 +357,8 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
       Prof pf(c, nd, s, PC_LN, 0);
       CK(k::layernorm_bwd_dx(b16, R, H, dhf, x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
                              pw(c, cp, p.lnfg), nullptr, nullptr, dx, dx32, s));
-      CK(k::colreduce(b16, true, 1, R, H, dhf, x, (float *)(sl + u.meanf),
-                      (float *)(sl + u.rstdf), nd.s_part, pg(cp, p.lnfg), s));
-      CK(k::colreduce(b16, true, 0, R, H, dhf, nullptr, nullptr, nullptr, nd.s_part,
-                      pg(cp, p.lnfb), s));
+      CK(k::colreduce_ln(b16, R, H, dhf, x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
+                         nd.s_part, pg(cp, p.lnfg), pg(cp, p.lnfb), s));
     } else {
       void *dpre = nd.sF, *dx1 = nd.sH[1], *dO = nd.sH[2], *dqkv = nd.s3;
       float *dh2 = nd.s32[0], *dx1_32 = nd.s32[1], *dh1 = nd.s32[0];
@@ -391,10 +389,8 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
         CK(k::layernorm_bwd_dx(b16, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
                                (float *)(sl + u.rstd2), pw(c, cp, p.ln2g), dy32,
                                dy32 ? nullptr : dy, dx1, dx1_32, s));
-        CK(k::colreduce(b16, true, 1, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
-                        (float *)(sl + u.rstd2), nd.s_part, pg(cp, p.ln2g), s));
-        CK(k::colreduce(b16, true, 0, R, H, dh2, nullptr, nullptr, nullptr, nd.s_part,
-                        pg(cp, p.ln2b), s));
+        CK(k::colreduce_ln(b16, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
+                           (float *)(sl + u.rstd2), nd.s_part, pg(cp, p.ln2g), pg(cp, p.ln2b), s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, H, dx1, H, false, pw(c, cp, p.wo), H, true, k::EPI_STORE, dO, H, nullptr,
@@ -428,10 +424,8 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
         CK(k::layernorm_bwd_dx(b16, R, H, dh1, x, (float *)(sl + u.mean1),
                                (float *)(sl + u.rstd1), pw(c, cp, p.ln1g), dx1_32, nullptr, dx,
                                dx32, s));
-        CK(k::colreduce(b16, true, 1, R, H, dh1, x, (float *)(sl + u.mean1),
-                        (float *)(sl + u.rstd1), nd.s_part, pg(cp, p.ln1g), s));
-        CK(k::colreduce(b16, true, 0, R, H, dh1, nullptr, nullptr, nullptr, nd.s_part,
-                        pg(cp, p.ln1b), s));
+        CK(k::colreduce_ln(b16, R, H, dh1, x, (float *)(sl + u.mean1),
+                           (float *)(sl + u.rstd1), nd.s_part, pg(cp, p.ln1g), pg(cp, p.ln1b), s));
       }
     }
     dy = dx;
@@ -895,8 +889,11 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.s3 = dmalloc(R * 3 * H * c.act_bytes);
       for (auto &p : nd.sH) p = dmalloc(R * H * c.act_bytes);
       for (auto &p : nd.s32) p = (float *)dmalloc(R * H * 4);
-      nd.s_part = (float *)dmalloc(
-          k::colreduce_partial_floats((int)R, (int)std::max(F, 3 * H)) * 4);
+      {
+        const size_t pb = k::colreduce_partial_floats((int)R, (int)std::max(F, 3 * H)) * 4;
+        nd.s_part = (float *)dmalloc(pb);
+        CK(cudaMemset(nd.s_part, 0, pb));   // colreduce tickets start at zero
+      }
       nd.s_attn = (float *)dmalloc((size_t)c.d.mb * c.d.nh * c.d.S * 4);
       nd.s_loss_main = (float *)dmalloc(R * 4);
       nd.s_loss_frc = (float *)dmalloc(R * 4);
