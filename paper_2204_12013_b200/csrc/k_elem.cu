@@ -6,6 +6,7 @@
 // ("exactly the same computation").
 #include <cfloat>
 
+
 #include "k_common.cuh"
 
 namespace bb {
@@ -420,6 +421,92 @@ __global__ void __launch_bounds__(CE_T) ce_kernel(int V, T *__restrict__ logits,
   }
 }
 
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return (uint32_t)__bfloat16_as_ushort(h.x) | ((uint32_t)__bfloat16_as_ushort(h.y) << 16);
+}
+
+// Streaming bf16 cross entropy, 16-byte vectors: pass 1 keeps an online
+// (max, sum of exp) per thread, merged in a fixed order; pass 2 re-reads the
+// row (L2-resident by then) and overwrites it with the gradient. 256 threads
+// per row, several rows per SM in flight.
+constexpr int CES_T = 256;
+template <int NT>
+__device__ __forceinline__ void block_merge_fixed(float &m, float &s, float *shm, float *shs) {
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    online_merge(m, s, m2, s2);
+  }
+  if (lane == 0) {
+    shm[w] = m;
+    shs[w] = s;
+  }
+  __syncthreads();
+  m = shm[0];
+  s = shs[0];
+#pragma unroll
+  for (int i = 1; i < NT / 32; ++i) online_merge(m, s, shm[i], shs[i]);
+}
+
+__global__ void __launch_bounds__(CES_T) ce_stream_kernel(int V, __nv_bfloat16 *__restrict__ logits,
+                                                          const int32_t *__restrict__ tgt,
+                                                          float inv_ntok,
+                                                          float *__restrict__ loss_rows) {
+  __shared__ float shm[CES_T / 32], shs[CES_T / 32];
+  const int r = blockIdx.x;
+  uint4 *row = reinterpret_cast<uint4 *>(logits + (size_t)r * V);
+  const int nv = V / 8;
+  const int t = tgt[r];
+  const float xt = threadIdx.x == 0 ? __bfloat162float(logits[(size_t)r * V + t]) : 0.f;
+  const float LOG2E_ = 1.4426950408889634f;
+  float m = -INFINITY, s = 0.f;                     // in log2 units: m2 = max * log2e
+#pragma unroll 4
+  for (int i = threadIdx.x; i < nv; i += CES_T) {
+    const uint4 u = row[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[2 * j] = bf_lo(w[j]) * LOG2E_;
+      v[2 * j + 1] = bf_hi(w[j]) * LOG2E_;
+    }
+    float mx = v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) mx = fmaxf(mx, v[j]);
+    const float mn = fmaxf(m, mx);
+    float add = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) add += exp2f(v[j] - mn);
+    s = s * exp2f(m - mn) + add;
+    m = mn;
+  }
+  // merge in natural-log units for online_merge (uses __expf)
+  m = m / LOG2E_;
+  block_merge_fixed<CES_T>(m, s, shm, shs);
+  const float lse = m + logf(s);
+  if (threadIdx.x == 0) loss_rows[r] = (lse - xt) * inv_ntok;
+  __syncthreads();                                   // the target logit was read
+  const float lse2 = lse * LOG2E_;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < nv; i += CES_T) {
+    const uint4 u = row[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = i * 8 + 2 * j;
+      const float p0 = exp2f(fmaf(bf_lo(w[j]), LOG2E_, -lse2)) - (c == t ? 1.f : 0.f);
+      const float p1 = exp2f(fmaf(bf_hi(w[j]), LOG2E_, -lse2)) - (c + 1 == t ? 1.f : 0.f);
+      o[j] = pack_bf2(p0 * inv_ntok, p1 * inv_ntok);
+    }
+    row[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 __global__ void sum_fixed_kernel(int n, const float *__restrict__ x, float *__restrict__ out) {
   __shared__ float sh[1024];
   float s = 0.f;
@@ -627,7 +714,10 @@ cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const 
 
 cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *targets,
                           float inv_ntok, float *loss_rows, cudaStream_t s) {
-  if (bf16)
+  if (bf16 && V % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+    ce_stream_kernel<<<R, CES_T, 0, s>>>(V, mp<__nv_bfloat16>(logits), targets, inv_ntok,
+                                         loss_rows);
+  } else if (bf16)
     ce_kernel<__nv_bfloat16><<<R, CE_T, 0, s>>>(V, mp<__nv_bfloat16>(logits), targets, inv_ntok,
                                                  loss_rows);
   else
