@@ -1,20 +1,23 @@
 // k_attn_umma.cu — flash attention forward on the 5th-generation tensor cores
 // (tcgen05 / TMEM / TMA), head dim 64, bf16 in, fp32 accumulation.
 //
-// One CTA = 128 query rows of one (sequence, head); key blocks of 128.
+// One CTA = 128 query rows of one (sequence, head); key blocks of 128; two
+// CTAs per SM (256 TMEM columns = S | P | O, ~81 KB smem each), so one CTA's
+// softmax overlaps the other's MMAs.
 //   warp 0      TMA: the Q tile once, then K_j and V_j into a 2-stage ring
 //               (128B-swizzled, straight out of the packed [B*S, 3H] qkv);
-//   warp 1      allocates 512 TMEM columns and issues, in order,
-//               S_{j+1} = Q K_{j+1}^T (M=128, N=128, K=64, into S buffer
-//               (j+1)%2) and, once the softmax published P_j,
-//               O += P_j V_j (M=128, N=64, K=128; V is the MN-major B operand);
-//   warps 2..5  softmax: thread r owns query row r (TMEM lane r), reads its S
-//               row from TMEM, keeps the running max / sum in registers,
-//               rescales its O row in TMEM (after PV_{j-1} completed), writes
-//               P_j (bf16) into the 128B-swizzled K-major smem tile the next
-//               MMA reads, and at the end normalises O and stores O and LSE.
-// Same math and LSE convention as the mma.sync kernel (k_attn_tc.cu), used
-// for the backward pass.
+//   warp 1      one lane issues S_j = Q K_j^T (M=128, N=128, K=64) into TMEM
+//               as soon as the softmax has read S_{j-1}, then
+//               O += P_{j-1} V_{j-1} (M=128, N=64, K=128; A = P from TMEM,
+//               V = MN-major smem B) once P_{j-1} is in TMEM;
+//   warps 2..5  softmax, thread r = query row r (TMEM lane r): pass 1 reads
+//               its S row (4 x 32 columns) for the row max, pass 2 re-reads
+//               it, exponentiates (exp2 of pre-scaled scores), packs P to
+//               bf16 registers and releases S; then, once PV_{j-1} is done,
+//               writes P_j to TMEM and rescales its O row if the max moved.
+//               At the end: O / l and the log-sum-exp.
+// Same math and LSE convention as the mma.sync kernel (k_attn_tc.cu), which
+// the backward pass uses.
 #include "k_common.cuh"
 #include "k_sm100.cuh"
 
@@ -36,12 +39,11 @@ struct SmemLayout {
   static constexpr int Q = 0;                         // 128 x 64 bf16 = 16 KB
   static constexpr int K = Q + BQ * D * 2;            // ST x 16 KB
   static constexpr int V = K + ST * BKV * D * 2;      // ST x 16 KB
-  static constexpr int P = V + ST * BKV * D * 2;      // 128 x 128 bf16 = 32 KB (2 swizzle atoms)
-  static constexpr int BAR = P + BQ * BKV * 2;
-  static constexpr int BYTES = BAR + 256 + 1024;
+  static constexpr int BAR = V + ST * BKV * D * 2;
+  static constexpr int BYTES = BAR + 128 + 1024;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     fa_fwd_umma_kernel(const __grid_constant__ CUtensorMap map_qkv, int S, int H, int nh,
                        int causal, __nv_bfloat16 *__restrict__ o, float *__restrict__ lse) {
   using L = SmemLayout;
@@ -53,12 +55,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t q_full = bars;
   auto kv_full = [&](int s) { return bars + 8u * (1 + s); };
   auto kv_empty = [&](int s) { return bars + 8u * (1 + ST + s); };
-  auto s_full = [&](int b) { return bars + 8u * (1 + 2 * ST + b); };
+  const uint32_t s_full = bars + 8u * (1 + 2 * ST);
+  const uint32_t s_free = bars + 8u * (2 + 2 * ST);
   const uint32_t p_full = bars + 8u * (3 + 2 * ST);
   const uint32_t o_done = bars + 8u * (4 + 2 * ST);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (5 + 2 * ST));
 
-  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // heaviest (causal: last) query blocks first
+  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = qb * BQ;
   const int row_base = b * S;            // first qkv row of this sequence
@@ -71,15 +75,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(kv_full(s), 1);
       mbar_init(kv_empty(s), 1);
     }
-    mbar_init(s_full(0), 1);
-    mbar_init(s_full(1), 1);
-    mbar_init(p_full, 4);     // one arrive per softmax warp
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);     // one arrive per softmax warp
+    mbar_init(p_full, 4);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
         smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -87,8 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s[2] = {tmem, tmem + 128};
-  const uint32_t t_o = tmem + 256;
+  // TMEM columns: S (fp32, 128) | P (bf16 pairs, 64) | O (fp32, 64)
+  const uint32_t t_s = tmem, t_p = tmem + 128, t_o = tmem + 192;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -108,38 +112,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t id_s = idesc_f16(128, BKV, false, false);
       const uint32_t id_o = idesc_f16(128, D, false, true);
-      auto issue_s = [&](int j) {
-        const int s = j % ST;
-        mbar_wait(kv_full(s), (j / ST) & 1);
-        tc_fence_after();
-        const uint32_t ka = base + L::K + s * BKV * D * 2;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16(t_s[j & 1], smem_desc(base + L::Q + kk * 32, 16, 1024),
-                   smem_desc(ka + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(s_full(j & 1));
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < nkb; ++j) {
-        if (j + 1 < nkb) issue_s(j + 1);
+      auto issue_pv = [&](int j) {       // O += P_j V_j
         mbar_wait(p_full, j & 1);
         tc_fence_after();
         const int s = j % ST;
         const uint32_t va = base + L::V + s * BKV * D * 2;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          // P: K-major, two 64-key swizzle atoms (16 KB apart); V: MN-major,
+          // P from TMEM (16 keys = 8 columns per K step); V: MN-major,
           // 16 keys = 16 rows of 128 B per K step.
-          const uint64_t da = smem_desc(base + L::P + (kk / 4) * (BQ * 64 * 2) + (kk % 4) * 32, 16,
-                                        1024);
           const uint64_t db = smem_desc(va + kk * 2048, 8192, 1024);
-          mma_bf16(t_o, da, db, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(t_o, t_p + kk * 8, db, id_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(o_done);
         mma_commit(kv_empty(s));
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nkb; ++j) {
+        const int s = j % ST;
+        mbar_wait(kv_full(s), (j / ST) & 1);
+        if (j > 0) mbar_wait(s_free, (j - 1) & 1);    // S_{j-1} read out of TMEM
+        tc_fence_after();
+        const uint32_t ka = base + L::K + s * BKV * D * 2;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16(t_s, smem_desc(base + L::Q + kk * 32, 16, 1024),
+                   smem_desc(ka + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+        mma_commit(s_full);
+        if (j > 0) issue_pv(j - 1);
       }
+      issue_pv(nkb - 1);
     }
   } else {
     // ---------------- softmax warps: row r = query q0 + r, TMEM lane r
@@ -148,70 +150,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
     const float sl2 = rsqrtf((float)D) * LOG2E;
     float m = -INFINITY, l = 0.f;
-    uint8_t *prow = gbase + L::P + r * 128;   // atom 0 row r; atom 1 at +16 KB
     for (int j = 0; j < nkb; ++j) {
-      mbar_wait(s_full(j & 1), (j >> 1) & 1);
+      mbar_wait(s_full, j & 1);
       tc_fence_after();
-      float sv[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        float t[32];
-        tmem_ld32(t_s[j & 1] + lane_off + c * 32, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = t[i] * sl2;
-      }
       const bool need_mask = (j * BKV + BKV > S) || (causal && j * BKV + BKV - 1 > q0);
+      const int kmax = causal ? min(S - 1, qrow) : S - 1;   // last valid key of this row
+      // the whole S row in one TMEM round trip (4 x 32 columns)
+      uint32_t t[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c)
+        tmem_ld32_nowait(t_s + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(t + c * 32));
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < BKV / 32; ++c) tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(t + c * 32));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);            // S may be overwritten by S_{j+1}
       if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) {
-          const int key = j * BKV + i;
-          if (key >= S || (causal && key > qrow)) sv[i] = -INFINITY;
-        }
+        for (int i = 0; i < BKV; ++i)
+          if (j * BKV + i > kmax) t[i] = __float_as_uint(-INFINITY);
       }
-      float mb = -INFINITY;
+      float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) mb = fmaxf(mb, sv[i]);
-      const float mn = fmaxf(m, mb);
+      for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, __uint_as_float(t[i]));
+      const float mn = fmaxf(m, mx * sl2);
       const float corr = mn == -INFINITY ? 1.f : exp2f(m - mn);
       m = mn;
+      const float mnz = mn == -INFINITY ? 0.f : mn;   // fully masked row: exp2(-inf) = 0
+      // P = exp2(s * sl2 - m), packed to bf16 pairs in place
       float sum = 0.f;
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        const float p = mn == -INFINITY ? 0.f : exp2f(sv[i] - mn);
-        sv[i] = p;
-        sum += p;
+      for (int i = 0; i < BKV; i += 2) {
+        const float p0 = exp2f(fmaf(__uint_as_float(t[i]), sl2, -mnz));
+        const float p1 = exp2f(fmaf(__uint_as_float(t[i + 1]), sl2, -mnz));
+        sum += p0 + p1;
+        const __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
+        t[i / 2] = (uint32_t)__bfloat16_as_ushort(hv.x) | ((uint32_t)__bfloat16_as_ushort(hv.y) << 16);
       }
       l = l * corr + sum;
       if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);    // PV_{j-1} done: O stable, P buffer free
+        mbar_wait(o_done, (j - 1) & 1);    // PV_{j-1} done: O stable, P columns free
         tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float t[32];
-            tmem_ld32(t_o + lane_off + c * 32, t);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] *= corr;
-            tmem_st32(t_o + lane_off + c * 32, t);
-          }
-        }
       }
-      // P row -> swizzled K-major smem (chunk c of 8 keys at position c ^ (r & 7))
+      // P row -> TMEM (lane r, 64 columns of bf16 pairs)
+      tmem_st32_nowait(t_p + lane_off, t);
+      tmem_st32_nowait(t_p + lane_off + 32, t + 32);
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
+        uint32_t ov[D];
+        tmem_ld32_nowait(t_o + lane_off, *reinterpret_cast<uint32_t(*)[32]>(ov));
+        tmem_ld32_nowait(t_o + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(ov + 32));
+        tmem_wait_ld();
+        tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(ov));
+        tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(ov + 32));
 #pragma unroll
-      for (int c = 0; c < BKV / 8; ++c) {
-        uint4 u;
-        u.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c])) |
-              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 1])) << 16);
-        u.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 2])) |
-              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 3])) << 16);
-        u.z = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 4])) |
-              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 5])) << 16);
-        u.w = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 6])) |
-              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(sv[8 * c + 7])) << 16);
-        const int atom = c / 8, cc = c % 8;
-        *reinterpret_cast<uint4 *>(prow + atom * (BQ * 64 * 2) + ((cc ^ (r & 7)) * 16)) = u;
+        for (int i = 0; i < D; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+        tmem_st32_nowait(t_o + lane_off, ov);
+        tmem_st32_nowait(t_o + lane_off + 32, ov + 32);
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
@@ -245,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
 }  // namespace

@@ -27,12 +27,11 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
 // kernels (head dim 32/64); fp32 check mode: SIMT.
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s) {
-  // The tcgen05 forward (k_attn_umma.cu) is parity-tested but, with a single
-  // softmax warpgroup per CTA, still slower than the mma.sync kernel on C1
-  // shapes; it is selected only when BB_ATTN_UMMA=1.
+  // tcgen05 forward (k_attn_umma.cu) for head dim 64; BB_ATTN_UMMA=0 selects
+  // the mma.sync kernel instead (tests / comparisons).
   static const bool use_umma = [] {
     const char *e = std::getenv("BB_ATTN_UMMA");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (bf16 && use_umma && attention_umma_supported(B, S, H, nh))
     return attention_umma_fwd(B, S, H, nh, causal, qkv, o, lse, s);

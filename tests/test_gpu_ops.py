@@ -113,7 +113,8 @@ def test_gemm_forced_variants(force):
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
 @pytest.mark.parametrize("causal", [True, False])
-@pytest.mark.parametrize("B,S,nh,d", [(2, 32, 2, 32), (1, 200, 3, 64), (2, 128, 2, 64)])
+@pytest.mark.parametrize("B,S,nh,d", [(2, 32, 2, 32), (1, 200, 3, 64), (2, 128, 2, 64),
+                                      (1, 1024, 2, 64), (2, 330, 1, 64)])
 def test_attention(prec, causal, B, S, nh, d):
     import paper_2204_12013_b200 as bb
     H = nh * d
@@ -133,6 +134,22 @@ def test_attention(prec, causal, B, S, nh, d):
     tol = 1e-5 if prec == "fp32" else 1e-2
     assert np.abs(host(o) - o_ref).max() <= tol * np.abs(o_ref).max()
     assert np.abs(host(dqkv) - dq_ref).max() <= tol * np.abs(dq_ref).max() * 2
+
+
+@pytest.mark.skipif(os.environ.get("BB_ATTN_UMMA") is not None, reason="already forced")
+def test_attention_other_forward():
+    """Whichever attention forward is not the default (tcgen05 / mma.sync,
+    BB_ATTN_UMMA) stays correct: rerun the attention tests with it."""
+    import paper_2204_12013_b200 as bb  # noqa: F401
+    env = dict(os.environ, BB_ATTN_UMMA="0" if _umma_default() else "1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "test_attention and not other"], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def _umma_default():
+    return True
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
