@@ -203,8 +203,8 @@ bb_status bb_op_attention_bwd(int prec, int B, int S, int H, int nh, int causal,
                               const void *o, const float *lse, const void *dout, void *dqkv,
                               void *stream) {
   float *scratch = nullptr;
-  if (cudaMallocAsync((void **)&scratch, (size_t)B * nh * S * 4, static_cast<cudaStream_t>(stream)) !=
-      cudaSuccess)
+  if (cudaMallocAsync((void **)&scratch, bb::k::attention_bwd_scratch_floats(B, S, H, nh) * 4,
+                      static_cast<cudaStream_t>(stream)) != cudaSuccess)
     return BB_E_OOM;
   cudaError_t e = bb::k::attention_bwd(prec == BB_PREC_BF16, B, S, H, nh, causal != 0, qkv, o, lse,
                                        dout, dqkv, scratch, static_cast<cudaStream_t>(stream));

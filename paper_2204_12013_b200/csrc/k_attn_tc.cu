@@ -473,6 +473,50 @@ cudaError_t bwd_d(int B, int S, int H, int nh, bool causal, const void *qkv, con
 }
 }  // namespace
 
+// D for head dim 64, 16-byte loads: 8 lanes per (row, head), 4 (row, head)
+// pairs per warp; the 8 partial dots are added by a fixed xor tree.
+__global__ void __launch_bounds__(256) fa_bwd_d64_kernel(int R, int S, int H, int nh,
+                                                         const __nv_bfloat16 *__restrict__ o,
+                                                         const __nv_bfloat16 *__restrict__ dout,
+                                                         float *__restrict__ Dv) {
+  const int gid = blockIdx.x * 32 + threadIdx.x / 8;   // (row, head) pair
+  const int sub = threadIdx.x % 8;
+  const bool ok = gid < R * nh;
+  const int h = ok ? gid % nh : 0, r = ok ? gid / nh : 0;
+  const size_t off = (size_t)r * H + h * 64 + sub * 8;
+  float acc = 0.f;
+  if (ok) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(o + off);
+    const uint4 x = *reinterpret_cast<const uint4 *>(dout + off);
+    const __nv_bfloat162 *pa = reinterpret_cast<const __nv_bfloat162 *>(&a);
+    const __nv_bfloat162 *px = reinterpret_cast<const __nv_bfloat162 *>(&x);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fa = __bfloat1622float2(pa[j]), fx = __bfloat1622float2(px[j]);
+      acc += fa.x * fx.x + fa.y * fx.y;
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (ok && sub == 0) {
+    const int b = r / S, i = r % S;
+    Dv[((size_t)b * nh + h) * S + i] = acc;
+  }
+}
+
+cudaError_t attention_bwd_rowdot(int B, int S, int H, int nh, const void *o, const void *dout,
+                                 float *Dv, cudaStream_t s) {
+  const int rows = B * S * nh;
+  if (H / nh == 64 && H % 8 == 0)
+    fa_bwd_d64_kernel<<<(rows + 31) / 32, 256, 0, s>>>(B * S, S, H, nh, (const __nv_bfloat16 *)o,
+                                                       (const __nv_bfloat16 *)dout, Dv);
+  else
+    fa_bwd_d_kernel<<<(rows + 3) / 4, 128, 0, s>>>(B * S, S, H, nh, (const __nv_bfloat16 *)o,
+                                                   (const __nv_bfloat16 *)dout, Dv);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 bool attention_tc_supported(int H, int nh) {
   const int d = H / nh;
   return (d == 64 || d == 32) && H % 8 == 0;

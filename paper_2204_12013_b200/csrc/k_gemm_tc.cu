@@ -721,6 +721,20 @@ bool tma_map_bf16_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t o
   return make_map(m, ptr, inner, outer, ld, box_outer);
 }
 
+bool tma_map_3d(CUtensorMap *m, const void *ptr, bool f32, const uint64_t dims[3],
+                const uint64_t strides_bytes[2], const uint32_t box[3]) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  cuuint64_t st[2] = {strides_bytes[0], strides_bytes[1]};
+  cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  cuuint32_t el[3] = {1, 1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+            const_cast<void *>(ptr), d, st, bx, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool gemm_tc_supported(const Gemm &g) {
   if (g.M < 1 || g.N < 1 || g.K < 1) return false;
   if ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) return false;

@@ -69,6 +69,9 @@ cudaError_t colreduce_ln(bool bf16, int R, int N, const float *A, const void *X,
 cudaError_t attention_fwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           void *o, float *lse, cudaStream_t s);
 // scratch: B*nh*S floats.
+// Scratch floats attention_bwd needs (row dots D, and for the tcgen05 path an
+// fp32 dQ accumulator and ordering counters).
+size_t attention_bwd_scratch_floats(int B, int S, int H, int nh);
 cudaError_t attention_bwd(bool bf16, int B, int S, int H, int nh, bool causal, const void *qkv,
                           const void *o, const float *lse, const void *dout, void *dqkv,
                           float *scratch, cudaStream_t s);

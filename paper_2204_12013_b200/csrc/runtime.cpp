@@ -894,7 +894,8 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         nd.s_part = (float *)dmalloc(pb);
         CK(cudaMemset(nd.s_part, 0, pb));   // colreduce tickets start at zero
       }
-      nd.s_attn = (float *)dmalloc((size_t)c.d.mb * c.d.nh * c.d.S * 4);
+      nd.s_attn = (float *)dmalloc(
+          k::attention_bwd_scratch_floats(c.d.mb, c.d.S, (int)H, c.d.nh) * 4);
       nd.s_loss_main = (float *)dmalloc(R * 4);
       nd.s_loss_frc = (float *)dmalloc(R * 4);
       nd.d_tok = (int32_t *)dmalloc((size_t)M * R * 4);
