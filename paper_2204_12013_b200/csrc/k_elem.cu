@@ -254,7 +254,7 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
 // then adds all row-block partials in ascending order into out: one launch,
 // deterministic whatever the arrival order. out1 (if any) gets the LN-gamma
 // form sum a * xhat, out0 (if any) the plain sum.
-constexpr int CRV_ROWS = 64;
+constexpr int CRV_ROWS = 256;
 template <typename TA, typename T>
 __global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int chunks,
                                                             const TA *__restrict__ A,
@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int ch
   float a0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float a1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (n < N) {
+#pragma unroll 4
     for (int r = r0 + warp; r < r1; r += 8) {
       const size_t idx = (size_t)r * N + n;
       const V8 a = ld8(A + idx);
@@ -538,6 +539,38 @@ __global__ void adam_kernel(size_t n, float *__restrict__ p, const float *__rest
   }
 }
 
+// Same update, 4 parameters per thread with 16-byte accesses (all five arrays
+// 16-byte aligned; the n % 4 tail goes through adam_kernel).
+__device__ __forceinline__ float adam1(float &p, float g, float &m, float &v, float lr, float b1,
+                                       float b2, float eps, float bc1, float bc2) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  p = p - lr * (m / bc1) / (sqrtf(v / bc2) + eps);
+  return p;
+}
+__global__ void __launch_bounds__(256) adam4_kernel(size_t n4, float4 *__restrict__ p,
+                                                    const float4 *__restrict__ g,
+                                                    float4 *__restrict__ m, float4 *__restrict__ v,
+                                                    uint2 *__restrict__ w16, float lr, float b1,
+                                                    float b2, float eps, float bc1, float bc2) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 pp = p[i], mm = m[i], vv = v[i];
+    const float4 gg = __ldcs(g + i);
+    adam1(pp.x, gg.x, mm.x, vv.x, lr, b1, b2, eps, bc1, bc2);
+    adam1(pp.y, gg.y, mm.y, vv.y, lr, b1, b2, eps, bc1, bc2);
+    adam1(pp.z, gg.z, mm.z, vv.z, lr, b1, b2, eps, bc1, bc2);
+    adam1(pp.w, gg.w, mm.w, vv.w, lr, b1, b2, eps, bc1, bc2);
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+    if (w16) {
+      const __nv_bfloat162 a = __floats2bfloat162_rn(pp.x, pp.y), b = __floats2bfloat162_rn(pp.z, pp.w);
+      w16[i] = make_uint2(*reinterpret_cast<const uint32_t *>(&a), *reinterpret_cast<const uint32_t *>(&b));
+    }
+  }
+}
+
 __global__ void cast_kernel(size_t n, const float *__restrict__ s, __nv_bfloat16 *__restrict__ d) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -735,9 +768,24 @@ cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s) {
 cudaError_t adam(size_t n, float *p, const float *g, float *m, float *v, void *w16, float lr,
                  float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  adam_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, p, g, m, v, mp<__nv_bfloat16>(w16), lr, b1, b2,
-                                                eps, bc1, bc2);
-  ++g_launches;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                       reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v) |
+                       (reinterpret_cast<uintptr_t>(w16) & 7);
+  const size_t n4 = (al & 15) == 0 ? n / 4 : 0;
+  if (n4) {
+    adam4_kernel<<<grid_for(n4, 256), 256, 0, s>>>(
+        n4, reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
+        reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v),
+        reinterpret_cast<uint2 *>(w16), lr, b1, b2, eps, bc1, bc2);
+    ++g_launches;
+  }
+  const size_t done = 4 * n4;
+  if (done < n) {
+    adam_kernel<<<grid_for(n - done, 256), 256, 0, s>>>(
+        n - done, p + done, g + done, m + done, v + done,
+        w16 ? mp<__nv_bfloat16>(w16) + done : nullptr, lr, b1, b2, eps, bc1, bc2);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
