@@ -21,7 +21,8 @@
 // key-block order and writes dQ_i in bf16. No CTA ever waits on another.
 // dK, dV leave TMEM once, at the end.
 //
-// Warps: 0 TMA producer (+ LSE / D rows into smem), 1 MMA issuer (one lane),
+// Warps: 0 TMA producer (Q, dO boxes; LSE / D rows by bulk copy, or plain
+// loads with +inf / 0 padding for a ragged S), 1 MMA issuer (one lane),
 // 2..9 softmax (warp w: key rows 32 (w % 4).., query half (w - 2) / 4),
 // 10..13 dQ epilogue (query rows 32 (w % 4)..).
 // D_q = sum_d dO_q,d O_q,d comes from fa_bwd_d_kernel (k_attn_tc.cu).
@@ -38,7 +39,7 @@ cudaError_t attention_bwd_rowdot(int B, int S, int H, int nh, const void *o, con
 namespace {
 using namespace sm100;
 
-constexpr int D = 64, BLK = 128;
+constexpr int D = 64, BLK = 128, NST = 3;   // NST: Q / dO / LSE / D ring depth
 constexpr int kThreads = 14 * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -50,11 +51,11 @@ constexpr uint32_t idesc_f16(int m, int n, bool a_mn, bool b_mn) {
 struct Smem {
   static constexpr int K = 0;                          // 128 x 64 bf16, 16 KB
   static constexpr int V = K + 16384;
-  static constexpr int Q = V + 16384;                  // 2 stages x 16 KB
-  static constexpr int DO = Q + 2 * 16384;             // 2 stages x 16 KB
-  static constexpr int DST = DO + 2 * 16384;           // 2 x dS^T 128 x 128 bf16 (2 atoms each)
-  static constexpr int LSED = DST + 2 * 32768;         // 2 stages x (128 lse2 + 128 D) fp32
-  static constexpr int BAR = LSED + 2 * 2 * BLK * 4;
+  static constexpr int Q = V + 16384;                  // NST stages x 16 KB
+  static constexpr int DO = Q + NST * 16384;           // NST stages x 16 KB
+  static constexpr int DST = DO + NST * 16384;         // 2 x dS^T 128 x 128 bf16 (2 atoms each)
+  static constexpr int LSED = DST + 2 * 32768;         // NST stages x (128 LSE + 128 D) fp32
+  static constexpr int BAR = LSED + NST * 2 * BLK * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -73,7 +74,7 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_umma_kernel(const __grid_constant__ CUtensorMap map_qkv,
                        const __grid_constant__ CUtensorMap map_do, float *__restrict__ ws,
-                       int S, int H, int nh, int causal, int dbg,
+                       int S, int H, int nh, int causal, int bulk_rows, int dbg,
                        const float *__restrict__ lse, const float *__restrict__ Dv,
                        __nv_bfloat16 *__restrict__ dqkv) {
   using L = Smem;
@@ -84,11 +85,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bars = base + L::BAR;
   const uint32_t kv_full = bars;
   auto qdo_full = [&](int s) { return bars + 8u * (1 + s); };
-  auto qdo_empty = [&](int s) { return bars + 8u * (3 + s); };
-  const uint32_t sdp_full = bars + 8u * 5, pds_full = bars + 8u * 6, dv_done = bars + 8u * 7;
-  const uint32_t dq_full = bars + 8u * 8, dq_free = bars + 8u * 9, fin = bars + 8u * 10;
-  auto ds_free = [&](int b2) { return bars + 8u * (11 + b2); };
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * 13);
+  auto qdo_empty = [&](int s) { return bars + 8u * (1 + NST + s); };
+  const uint32_t sdp_full = bars + 8u * (1 + 2 * NST), pds_full = sdp_full + 8u,
+                 dv_done = sdp_full + 16u, dq_full = sdp_full + 24u, dq_free = sdp_full + 32u,
+                 fin = sdp_full + 40u;
+  auto ds_free = [&](int b2) { return sdp_full + 48u + 8u * b2; };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (1 + 2 * NST + 8));
   float *lsed = reinterpret_cast<float *>(gbase + L::LSED);
 
   const int nkb = (S + BLK - 1) / BLK;
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(qdo_full(s), 1);
       mbar_init(qdo_empty(s), 1);
     }
@@ -140,21 +142,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_3d(base + L::V, &map_qkv, kv_full, 2 * H + h * D, kb * BLK, b);
     }
     for (int t = 0; t < n; ++t) {
-      const int i = i0 + t, st = t & 1;
-      mbar_wait(qdo_empty(st), ((t >> 1) & 1) ^ 1);
+      const int i = i0 + t, st = t % NST;
+      mbar_wait(qdo_empty(st), ((t / NST) & 1) ^ 1);
       float *ls = lsed + st * 2 * BLK;
+      const uint32_t lsa = base + L::LSED + st * 2 * BLK * 4;
+      if (!bulk_rows) {
+        // ragged S: rows past S get LSE = +inf (P = 0, dS = 0) and D = 0
 #pragma unroll
-      for (int c = 0; c < BLK / 32; ++c) {
-        const int qi = c * 32 + lane, q = i * BLK + qi;
-        // rows past S: LSE = +inf makes P = 0 (and dS = 0) for them
-        ls[qi] = q < S ? lse[bh * S + q] * LOG2E : INFINITY;
-        ls[BLK + qi] = q < S ? Dv[bh * S + q] : 0.f;
+        for (int c = 0; c < BLK / 32; ++c) {
+          const int qi = c * 32 + lane, q = i * BLK + qi;
+          ls[qi] = q < S ? lse[bh * S + q] : INFINITY;
+          ls[BLK + qi] = q < S ? Dv[bh * S + q] : 0.f;
+        }
+        __syncwarp();
       }
-      __syncwarp();
       if (lane == 0) {
-        mbar_expect_tx(qdo_full(st), 2 * 16384);
+        mbar_expect_tx(qdo_full(st), 2 * 16384 + (bulk_rows ? 2 * BLK * 4 : 0));
         tma_load_3d(base + L::Q + st * 16384, &map_qkv, qdo_full(st), h * D, i * BLK, b);
         tma_load_3d(base + L::DO + st * 16384, &map_do, qdo_full(st), h * D, i * BLK, b);
+        if (bulk_rows) {
+          bulk_load(lsa, lse + bh * S + i * BLK, BLK * 4, qdo_full(st));
+          bulk_load(lsa + BLK * 4, Dv + bh * S + i * BLK, BLK * 4, qdo_full(st));
+        }
       }
       __syncwarp();
     }
@@ -165,8 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_kv = idesc_f16(128, D, false, true);    // dV, dK: B = dO / Q MN-major
       const uint32_t id_q = idesc_f16(128, D, true, true);      // dQ: A = dS (from dS^T), B = K
       auto issue_sdp = [&](int t) {
-        const int st = t & 1;
-        mbar_wait(qdo_full(st), (t >> 1) & 1);
+        const int st = t % NST;
+        mbar_wait(qdo_full(st), (t / NST) & 1);
         tc_fence_after();
         const uint32_t q = base + L::Q + st * 16384, d = base + L::DO + st * 16384;
 #pragma unroll
@@ -182,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(kv_full, 0);
       issue_sdp(0);
       for (int t = 0; t < n; ++t) {
-        const int st = t & 1;
+        const int st = t % NST;
         mbar_wait(pds_full, t & 1);       // P^T, dS^T in smem; S^T, dP^T read out
         tc_fence_after();
         if (t + 1 < n) issue_sdp(t + 1);
@@ -226,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key = kb * BLK + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int t = 0; t < n; ++t) {
-      const int i = i0 + t, st = t & 1;
+      const int i = i0 + t, st = t % NST;
       const bool diag = causal && i == kb;
       const float *ls = lsed + st * 2 * BLK;
       mbar_wait(sdp_full, t & 1);
@@ -245,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
           const int qc = c0 + c;
-          float p0 = exp2f(fmaf(__uint_as_float(sv[c]), sl2, -ls[qc]));
-          float p1 = exp2f(fmaf(__uint_as_float(sv[c + 1]), sl2, -ls[qc + 1]));
+          float p0 = exp2f(fmaf(__uint_as_float(sv[c]), sl2, -ls[qc] * LOG2E));
+          float p1 = exp2f(fmaf(__uint_as_float(sv[c + 1]), sl2, -ls[qc + 1] * LOG2E));
           if (diag) {
             if (key > i * BLK + qc) p0 = 0.f;
             if (key > i * BLK + qc + 1) p1 = 0.f;
@@ -430,7 +439,10 @@ cudaError_t attention_umma_bwd(int B, int S, int H, int nh, bool causal, const v
   }
   dim3 grid(nh * B, nkb);
   fa_bwd_umma_kernel<<<grid, kThreads, Smem::BYTES, s>>>(
-      mq, md, ws, S, H, nh, causal ? 1 : 0, dbg_flags(), lse, Dv,
+      mq, md, ws, S, H, nh, causal ? 1 : 0,
+      (S % BLK == 0 && (reinterpret_cast<uintptr_t>(lse) & 15) == 0 &&
+       (reinterpret_cast<uintptr_t>(Dv) & 15) == 0) ? 1 : 0,
+      dbg_flags(), lse, Dv,
       reinterpret_cast<__nv_bfloat16 *>(dqkv));
   e = cudaGetLastError();
   if (e != cudaSuccess) {

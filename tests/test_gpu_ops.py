@@ -148,6 +148,30 @@ def test_attention_other_forward():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_backward_bitwise_deterministic(causal):
+    """Recovery replays backward passes and must reproduce them bit for bit
+    (SURVEY.md §2.2 K7): two backward calls on the same inputs agree exactly
+    (dQ sums up to 8 key-block partials in a fixed order)."""
+    import paper_2204_12013_b200 as bb
+    B, S, nh, d = 2, 1024, 3, 64
+    H = nh * d
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = (torch.randn(B * S, 3 * H, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    do = (torch.randn(B * S, H, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    o = torch.zeros(B * S, H, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(B, nh, S, device="cuda")
+    bb.op_attention_fwd("bf16", B, S, H, nh, causal, qkv.data_ptr(), o.data_ptr(), lse.data_ptr())
+    outs = []
+    for _ in range(3):
+        dqkv = torch.zeros_like(qkv)
+        bb.op_attention_bwd("bf16", B, S, H, nh, causal, qkv.data_ptr(), o.data_ptr(),
+                            lse.data_ptr(), do.data_ptr(), dqkv.data_ptr())
+        torch.cuda.synchronize()
+        outs.append(dqkv)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 def _umma_default():
     return True
 
