@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = tiles_n * tiles_m;
   // Work unit = (tile, K split). With ksplit > 1 (fp32-accumulating dW only)
   // the splits of a tile add into C in ascending split order, serialised by a
-  // per-(tile, CTA) flag (epoch * 16 + split): deterministic, and deadlock-free
-  // since every CTA is resident and a unit only waits for a lower-numbered unit.
+  // per-(tile, CTA) flag (epoch * 16 + split): deterministic; a split waits
+  // only on a lower-numbered CTA of the same round (grid % ksplit == 0).
   const int units = tiles * ksplit;
 
   if (warp == 0 && lane == 0) {
@@ -692,7 +692,14 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
     if (!flags) ksplit = 1;
   }
   const int units = tiles * ksplit;
-  const int grid = (units < slots ? units : slots) * CG;
+  // Split-K waits only on the previous split of the same tile. With the number
+  // of persistent CTAs (pairs) a multiple of ksplit, every round covers whole
+  // tiles, so that split always runs on a lower-numbered CTA in the same
+  // round: dispatched earlier, hence resident, even when other kernels share
+  // the GPU and this grid is only partly resident (no co-residency assumed).
+  int pids = units < slots ? units : slots;
+  if (ksplit > 1) pids = std::max(ksplit, pids / ksplit * ksplit);
+  const int grid = pids * CG;
   if (CG == 1) {
     kern<<<grid, kThreads, L::BYTES, s>>>(ma, mb, mc, mx, g, ksplit, flags, epoch);
   } else {
