@@ -6,7 +6,8 @@ For each k: `steps` training steps with k preemptions at steps drawn with
 numpy PCG64(seed 7) from [10, 90] (at least 11 steps apart); the victim is
 drawn uniformly among the stages (all protected again after the previous
 rejoin) and the injection point uniformly over the victim's list; the victim
-rejoins (bb_rejoin) 10 steps later. Reports total samples / total
+rejoins (bb_rejoin) 10 steps later. One pipeline serves the whole
+sweep (training continues from one k to the next). Reports total samples / total
 wall time, the pause of every injection (interrupted step incl. bb_recover
 minus the median failure-free step), the failover ("spare tire") step time
 and the rejoin time. One JSON line per k on rank 0.
@@ -53,15 +54,17 @@ def main():
     M, mb = cfg.microbatches, cfg.micro_batch
     flat = make_params(m)
     tok, tgt = make_tokens(cfg, 0)
+    # one pipeline for the whole sweep (training simply continues from one k
+    # to the next; every k starts and ends on the normal, fully protected plan)
+    nid = bench.bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
+    pipe = bb.Pipeline(m, P, M, micro_batch=mb, rc=True, world_rank=rank, world_size=ws,
+                       device=local, nccl_id=nid)
+    pipe.load_params(flat)
+    pipe.stage_inputs(tok, tgt)
+    for _ in range(3):
+        pipe.step()
     for k in args.k:
         ts, rng = schedule(k, args.steps)
-        nid = bench.bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
-        pipe = bb.Pipeline(m, P, M, micro_batch=mb, rc=True, world_rank=rank, world_size=ws,
-                           device=local, nccl_id=nid)
-        pipe.load_params(flat)
-        pipe.stage_inputs(tok, tgt)
-        for _ in range(3):
-            pipe.step()
         plans = {}
         for line in pipe.schedule_dump().splitlines():
             if not line.startswith("#"):
@@ -99,13 +102,12 @@ def main():
                 normal.append(dt)
         bench.barrier(ws)
         wall = time.perf_counter() - t_all
+        if any(t0_ + 10 >= args.steps for t0_ in ts):
+            pipe.rejoin()                  # back to the normal plan for the next k
         med = statistics.median(normal) if normal else float("nan")
         for inj, p in zip(injections, pauses):
             inj["interrupted_step_ms"] = round(p, 2)
             inj["pause_ms"] = round(p - med, 2)
-        pipe.close()
-        del pipe
-        torch.cuda.empty_cache()
         if rank == 0:
             print(json.dumps({
                 "metric": "C4 preemption sweep: samples/s with k preemptions per 100 steps",
@@ -117,6 +119,7 @@ def main():
                 "failover_step_ms": round(statistics.median(fo), 2) if fo else None,
                 "rejoin_ms": [round(r, 2) for r in rejoins],
                 "injections": injections}), flush=True)
+    pipe.close()
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
