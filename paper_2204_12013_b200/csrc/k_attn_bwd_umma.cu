@@ -28,6 +28,7 @@
 // D_q = sum_d dO_q,d O_q,d comes from fa_bwd_d_kernel (k_attn_tc.cu).
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "k_common.cuh"
 #include "k_sm100.cuh"
@@ -66,8 +67,16 @@ __device__ __forceinline__ uint32_t t_p_base(uint32_t t_pt, uint32_t lane_off, i
 }
 
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-  return (uint32_t)__bfloat16_as_ushort(h.x) | ((uint32_t)__bfloat16_as_ushort(h.y) << 16);
+  uint32_t r;   // one F2FP: hi -> upper half, lo -> lower half, round to nearest even
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// 2^x, flush-to-zero approximation (MUFU.EX2 only): the arguments are
+// s*scale - LSE <= ~0, far from the denormal range that matters here.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // 14 warps: at most 4 per SM sub-partition, so 128 registers per thread.
@@ -76,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap map_do, float *__restrict__ ws,
                        int S, int H, int nh, int causal, int bulk_rows, int dbg,
                        const float *__restrict__ lse, const float *__restrict__ Dv,
-                       __nv_bfloat16 *__restrict__ dqkv) {
+                       __nv_bfloat16 *__restrict__ dqkv, unsigned long long *__restrict__ trace) {
   using L = Smem;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -130,6 +139,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  auto stamp = [&](int k) {            // BB_ATTN_DBG & 4: per-CTA timeline (64 slots)
+    if (trace) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + k] = tt;
+    }
+  };
   // TMEM columns: S^T | dP^T (128 each) | dV | dK | dQ (64 each) | P^T (bf16 pairs, 64)
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320,
                  t_dq = tmem + 384, t_pt = tmem + 448;
@@ -188,11 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                    smem_desc(d + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         mma_commit(sdp_full);
       };
+      stamp(0);
       mbar_wait(kv_full, 0);
+      stamp(1);
       issue_sdp(0);
       for (int t = 0; t < n; ++t) {
         const int st = t % NST;
         mbar_wait(pds_full, t & 1);       // P^T, dS^T in smem; S^T, dP^T read out
+        if (t < 8) stamp(2 + t);
         tc_fence_after();
         if (t + 1 < n) issue_sdp(t + 1);
         const uint32_t q = base + L::Q + st * 16384, d = base + L::DO + st * 16384;
@@ -207,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(dq_free, (t - 1) & 1);
           tc_fence_after();
         }
+        if (t < 8) stamp(10 + t);
 #pragma unroll
         for (int kk = 0; kk < BLK / 16; ++kk) {
           // A = dS (queries x keys) read MN-major from the dS^T tile: 64-query
@@ -227,6 +247,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(qdo_empty(st));
       }
       mma_commit(fin);
+      if (trace) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        stamp(60);
+        trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 64 + 61] = sm;
+      }
     }
   } else if (warp < 10) {
     // ---------------- softmax warps
@@ -239,51 +265,78 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag = causal && i == kb;
       const float *ls = lsed + st * 2 * BLK;
       mbar_wait(sdp_full, t & 1);
+      const bool tr = warp == 2 && lane == 0 && t < 8;
+      if (tr) stamp(20 + t);
+      // P^T (TMEM) is free once dV of the previous step has read it, dS^T
+      // buffer t & 1 once dQ / dK of step t - 2 have; both usually are.
+      if (t > 0) mbar_wait(dv_done, (t - 1) & 1);
+      if (t > 1) mbar_wait(ds_free(t & 1), ((t >> 1) & 1) ^ 1);
       tc_fence_after();
-      uint32_t pp[32], dd[32];                      // 64 queries: bf16 pairs of P^T, dS^T
+      if (tr) stamp(28 + t);
+      const uint32_t drow = base + L::DST + (t & 1) * 32768 + g * 16384 + r * 128;
+      // 4 chunks of 16 queries; chunk hh+1's TMEM loads are in flight while
+      // chunk hh is computed (tcgen05.wait::ld waits for all of them)
+      uint32_t sv[2][16], dv[2][16];
+      tmem_ld16_nowait(t_s + lane_off + 64 * g, sv[0]);
+      tmem_ld16_nowait(t_dp + lane_off + 64 * g, dv[0]);
+      tmem_wait_ld();
+      tmem_pin16(sv[0]);
+      tmem_pin16(dv[0]);
 #pragma unroll
       for (int hh = 0; hh < 4; ++hh) {
-        if (dbg & 2) break;
+        const int cur = hh & 1;
         const int c0 = 64 * g + 16 * hh;             // first query column
-        uint32_t sv[16], dv[16];
-        tmem_ld16_nowait(t_s + lane_off + c0, sv);
-        tmem_ld16_nowait(t_dp + lane_off + c0, dv);
-        tmem_wait_ld();
-        tmem_pin16(sv);
-        tmem_pin16(dv);
+        if (hh < 3) {
+          tmem_ld16_nowait(t_s + lane_off + c0 + 16, sv[cur ^ 1]);
+          tmem_ld16_nowait(t_dp + lane_off + c0 + 16, dv[cur ^ 1]);
+        }
+        uint32_t pp[8], dd[8];
+        // LSE (natural units) -> log2 units once per column pair
+        float l2[16], dq[16];
 #pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          const int qc = c0 + c;
-          float p0 = exp2f(fmaf(__uint_as_float(sv[c]), sl2, -ls[qc] * LOG2E));
-          float p1 = exp2f(fmaf(__uint_as_float(sv[c + 1]), sl2, -ls[qc + 1] * LOG2E));
-          if (diag) {
+        for (int c = 0; c < 16; c += 4) {
+          const float4 a = *reinterpret_cast<const float4 *>(ls + c0 + c);
+          const float4 d4 = *reinterpret_cast<const float4 *>(ls + BLK + c0 + c);
+          l2[c] = a.x * LOG2E; l2[c + 1] = a.y * LOG2E; l2[c + 2] = a.z * LOG2E; l2[c + 3] = a.w * LOG2E;
+          dq[c] = d4.x; dq[c + 1] = d4.y; dq[c + 2] = d4.z; dq[c + 3] = d4.w;
+        }
+        if (diag) {                                   // causal diagonal block: mask key > query
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const int qc = c0 + c;
+            float p0 = ex2(fmaf(__uint_as_float(sv[cur][c]), sl2, -l2[c]));
+            float p1 = ex2(fmaf(__uint_as_float(sv[cur][c + 1]), sl2, -l2[c + 1]));
             if (key > i * BLK + qc) p0 = 0.f;
             if (key > i * BLK + qc + 1) p1 = 0.f;
+            pp[c / 2] = pack_bf2(p0, p1);
+            dd[c / 2] = pack_bf2(p0 * (__uint_as_float(dv[cur][c]) - dq[c]),
+                                 p1 * (__uint_as_float(dv[cur][c + 1]) - dq[c + 1]));
           }
-          const float d0 = p0 * (__uint_as_float(dv[c]) - ls[BLK + qc]);
-          const float d1 = p1 * (__uint_as_float(dv[c + 1]) - ls[BLK + qc + 1]);
-          pp[hh * 8 + c / 2] = pack_bf2(p0, p1);
-          dd[hh * 8 + c / 2] = pack_bf2(d0, d1);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(sv[cur][c]), sl2, -l2[c]));
+            const float p1 = ex2(fmaf(__uint_as_float(sv[cur][c + 1]), sl2, -l2[c + 1]));
+            pp[c / 2] = pack_bf2(p0, p1);
+            dd[c / 2] = pack_bf2(p0 * (__uint_as_float(dv[cur][c]) - dq[c]),
+                                 p1 * (__uint_as_float(dv[cur][c + 1]) - dq[c + 1]));
+          }
+        }
+        // P^T: 8 TMEM columns (16 queries); dS^T: 2 swizzled 16-byte chunks
+        tmem_st8_nowait(t_p_base(t_pt, lane_off, g) + 8 * hh, pp);
+        st_shared_v4(drow + (uint32_t)(((2 * hh) ^ (r & 7)) * 16), dd[0], dd[1], dd[2], dd[3]);
+        st_shared_v4(drow + (uint32_t)(((2 * hh + 1) ^ (r & 7)) * 16), dd[4], dd[5], dd[6], dd[7]);
+        if (hh < 3) {
+          tmem_wait_ld();
+          tmem_pin16(sv[cur ^ 1]);
+          tmem_pin16(dv[cur ^ 1]);
         }
       }
-      // P^T -> TMEM once dV of the previous step has read it
-      if (t > 0) {
-        mbar_wait(dv_done, (t - 1) & 1);
-        tc_fence_after();
-      }
-      tmem_st32_nowait(t_p_base(t_pt, lane_off, g), pp);
-      // dS^T -> smem buffer t & 1 once dQ / dK of step t - 2 have read it;
-      // row r of atom g: 8 chunks of 8 queries at position c ^ (r & 7)
-      if (t > 1) mbar_wait(ds_free(t & 1), ((t >> 1) & 1) ^ 1);
-      const uint32_t drow = base + L::DST + (t & 1) * 32768 + g * 16384 + r * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        st_shared_v4(drow + (uint32_t)((c ^ (r & 7)) * 16), dd[4 * c], dd[4 * c + 1], dd[4 * c + 2],
-                     dd[4 * c + 3]);
       fence_async_smem();
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (tr) stamp(36 + t);
       if (lane == 0) mbar_arrive(pds_full);
     }
     // ---------------- dV (group 0) / dK (group 1) out of TMEM, once
@@ -395,6 +448,21 @@ static int dbg_flags() {
   return f;
 }
 
+// BB_ATTN_DBG & 4: per-CTA globaltimer stamps (start, K/V in, each step's
+// softmax hand-off, end, SM id), written to bwd_trace.bin after each call.
+static unsigned long long *g_trace = nullptr;
+static size_t g_trace_n = 0;
+static unsigned long long *trace_buf(size_t ctas) {
+  if (!(dbg_flags() & 4)) return nullptr;
+  if (g_trace_n < ctas) {
+    if (g_trace) cudaFree(g_trace);
+    cudaMalloc(&g_trace, ctas * 64 * 8);
+    g_trace_n = ctas;
+  }
+  cudaMemset(g_trace, 0, ctas * 64 * 8);
+  return g_trace;
+}
+
 size_t attention_umma_bwd_scratch_floats(int B, int S, int H, int nh) {
   const size_t nkb = (S + BLK - 1) / BLK;
   auto up = [](size_t x) { return (x + 63) / 64 * 64; };
@@ -443,11 +511,22 @@ cudaError_t attention_umma_bwd(int B, int S, int H, int nh, bool causal, const v
       (S % BLK == 0 && (reinterpret_cast<uintptr_t>(lse) & 15) == 0 &&
        (reinterpret_cast<uintptr_t>(Dv) & 15) == 0) ? 1 : 0,
       dbg_flags(), lse, Dv,
-      reinterpret_cast<__nv_bfloat16 *>(dqkv));
+      reinterpret_cast<__nv_bfloat16 *>(dqkv), trace_buf(grid.x * grid.y));
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "[bb] attention bwd launch: %s\n", cudaGetErrorString(e));
     return e;
+  }
+  if (dbg_flags() & 4) {
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h((size_t)grid.x * grid.y * 64);
+    cudaMemcpy(h.data(), g_trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE *f = fopen("bwd_trace.bin", "wb")) {
+      const int dims[4] = {(int)grid.x, (int)grid.y, nh, B};
+      fwrite(dims, sizeof(int), 4, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
   }
   const size_t total = (size_t)B * S * nh * (D / 8);
   dq_reduce_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
