@@ -178,6 +178,63 @@ def log(rank, *a):
         print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
+def balanced_partition(m, P, rc=True):
+    """Blocks per stage (bb_opts.layers_per_stage) that balance the per-node
+    work of one micro-batch. An even split by layer count (the default, Q6)
+    leaves the last stage with the LM head on top of its blocks: at C1 the
+    head's GEMM + cross entropy is ~4 blocks' forward, so the last node
+    paces the pipeline. Cost model (per token, FLOP-proportional, calibrated
+    on C1 kernel times: block fwd 220 us, bwd 530 us, head + cross entropy
+    fwd 900 us, bwd 930 us per micro-batch): block fwd 24H^2 + 4SH (causal:
+    halved attention), bwd 2.4x; head fwd 2HV x 0.85, bwd 2HV x 0.87 (the
+    head GEMM runs faster per FLOP than a block). A node's
+    load is its stage's fwd + bwd plus, with RC, its successor's fwd (FRC).
+    Contiguous shards; interior stages keep >= 1 block, the first / last may
+    hold only the embedding / the head. Hill climbing from the even split:
+    move one block across a boundary while the maximum load drops."""
+    L, H, S, V = m.n_layer, m.d_model, m.seq_len, m.vocab
+    fb = 24.0 * H * H + 4.0 * S * H * (0.5 if m.causal else 1.0)
+    bb_ = 2.4 * fb
+    fh, bh = 2.0 * H * V * 0.85, 2.0 * H * V * 0.87
+
+    def loads(c):
+        f = [c[s] * fb + (fh if s == P - 1 else 0.0) for s in range(P)]
+        b = [c[s] * bb_ + (bh if s == P - 1 else 0.0) for s in range(P)]
+        return [f[s] + b[s] + (f[(s + 1) % P] if rc and P > 1 else 0.0) for s in range(P)]
+
+    # exact minimax by depth-first search with branch and bound (the load of
+    # node s is known once c[s+1] is chosen; the last node's needs c[0])
+    A = lambda s, x: x * (fb + bb_) + ((fh + bh) if s == P - 1 else 0.0)   # own fwd + bwd
+    F = lambda s, x: (x * fb + (fh if s == P - 1 else 0.0)) if (rc and P > 1) else 0.0
+    base, rem = divmod(L, P)
+    even = [base + (1 if s >= P - rem else 0) for s in range(P)]
+    best = [max(loads(even)), even]
+
+    def dfs(c, used, cur):
+        s = len(c)
+        if cur >= best[0]:
+            return
+        if s == P:
+            if used == L:
+                full = max(cur, A(P - 1, c[-1]) + F(0, c[0]))
+                if full < best[0] - 1e-9:
+                    best[0], best[1] = full, list(c)
+            return
+        lo = 0 if s in (0, P - 1) else 1
+        left = L - used
+        need_after = max(0, P - 2 - s) if s < P - 1 else 0   # interior stages still to fill
+        for x in range(lo, left - need_after + 1):
+            if s == P - 1 and x != left:
+                continue
+            nxt = cur if s == 0 else max(cur, A(s - 1, c[-1]) + F(s, x))
+            c.append(x)
+            dfs(c, used + x, nxt)
+            c.pop()
+
+    dfs([], 0, 0.0)
+    return best[1]
+
+
 def run_ours(args, rank, ws, local):
     import torch
     import paper_2204_12013_b200 as bb
@@ -192,7 +249,9 @@ def run_ours(args, rank, ws, local):
     flat = make_params(m)
     tok, tgt = make_tokens(cfg, 0)
     host_batches = [make_tokens(cfg, s) for s in range(1, 3)]
-    common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local)
+    lps = balanced_partition(m, P) if args.partition == "balanced" else None
+    common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
+                  layers_per_stage=lps)
 
     results = {}
     for rc in (False, True):
@@ -299,6 +358,7 @@ def run_ours(args, rank, ws, local):
                                f"{P} stages, M={M}, mb={mb}, EFLB (eager FRC, lazy BRC)",
                    "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
                    "seq_len": m.seq_len, "parallelism": f"pp{P} on {ws} GPU(s)",
+                   "layers_per_stage": lps or "even",
                    "l2": "working set (weights, stash, FRC retention) >> 126 MB L2"},
         "rc_off": {"value": round(samples / (off["ms"] / 1e3), 2), "ms_per_step": round(off["ms"], 3)},
         "rc_overhead_pct": round(100.0 * (1 - off["ms"] / on["ms"]), 2),
@@ -407,6 +467,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
+                    help="blocks per stage: cost-balanced (default) or even by count (Q6)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=20.0)

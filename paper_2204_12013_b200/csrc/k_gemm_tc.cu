@@ -788,6 +788,7 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     const char *e = std::getenv("BB_GEMM_TILE");
     if (!e) return 0;
     if (!std::strcmp(e, "pair")) return 2;
+    if (!std::strcmp(e, "pair128")) return 3;
     if (!std::strcmp(e, "256")) return 256;
     if (!std::strcmp(e, "128")) return 128;
     return 0;
@@ -800,6 +801,7 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
   if (force == 128 || g.N < 256)
     return te ? launch_bn<128, 1, true>(g, s) : launch_bn<128, 1, false>(g, s);
   if (force == 256) return te ? launch_bn<256, 1, true>(g, s) : launch_bn<256, 1, false>(g, s);
+  if (force == 3 && te) return launch_bn<128, 2, true>(g, s);
   if (!te) return launch_bn<256, 1, false>(g, s);
   // fp32-accumulating dW with few output tiles: the serialised split-K chain
   // (up to 8 links of a few us each on pairs) costs more than the smaller

@@ -203,3 +203,35 @@ def test_c0_rejoin_and_repeated_preemptions_bitwise():
     for s in range(cfg.stages):   # protection restored: replica == primary again
         assert np.array_equal(p.read_state(s, "params"), p.read_state(s, "params", replica=True))
     p.close()
+
+
+@pytest.mark.parametrize("lps", [[3, 1, 0], [0, 2, 2], [2, 1, 1]])
+def test_custom_partition_matches_oracle(lps):
+    """layers_per_stage (bb_opts): a head-only last stage and an
+    embedding-only first stage (the cost-balanced partitions bench.py uses)
+    give the oracle's loss and gradients, and a preemption of the head-only /
+    embedding-only node recovers bit for bit."""
+    import dataclasses
+    c0 = get_config("C0")
+    cfg = dataclasses.replace(c0, stages=3, microbatches=4)
+    flat = make_params(cfg.model)
+    p = _gpu(cfg, flat, "bf16", layers_per_stage=lps)
+    ref = opipe.Pipeline(cfg, flat, rc=True, lr=LR, layers_per_stage=lps)
+    want = opl.dump(cfg.stages, cfg.microbatches, True, opl.partition(cfg.model.n_layer, 3, lps),
+                    opl.normal_plans(cfg.stages, cfg.microbatches, True))
+    assert p.schedule_dump() == want
+    tok, tgt = make_tokens(cfg, 0)
+    status, st = p.step(tok, tgt)
+    _, ref_loss = ref.step(tok, tgt)
+    _compare_step(cfg, p, ref, "bf16", st.loss, ref_loss, 1)
+    base = {w: _flat_state(p, 3, w) for w in ("params", "grads", "adam_m", "adam_v")}
+    p.close()
+    for victim in (0, 2):
+        q = _gpu(cfg, flat, "bf16", layers_per_stage=lps)
+        q.preempt(victim, 9)
+        status, st = q.step(tok, tgt)
+        assert status == "preempted"
+        q.recover()
+        for w, v in base.items():
+            assert np.array_equal(_flat_state(q, 3, w), v), (victim, w)
+        q.close()

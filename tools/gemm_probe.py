@@ -54,7 +54,8 @@ def main():
     a = [int(x) for x in sys.argv[1:]]
     M, N, K = a[:3]
     amn, bmn, epi = (a[3:] + [0, 0, 0])[:3] if len(a) > 3 else (0, 0, 0)
-    for tile in ("128", "256", "pair"):
+    tiles = os.environ.get("TILES", "128,256,pair").split(",")
+    for tile in tiles:
         env = dict(os.environ, BB_GEMM_TILE=tile)
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, (M, N, K, amn, bmn, epi))],
                            env=env, capture_output=True, text=True)
