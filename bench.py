@@ -241,7 +241,7 @@ def run_ours(args, rank, ws, local):
 
     cfg = get_config(args.config)
     m = cfg.model
-    P = max(cfg.stages, ws)
+    P = max(cfg.stages, ws, args.stages)
     M, mb = cfg.microbatches, cfg.micro_batch
     samples = M * mb
     def fresh_id():   # every communicator needs its own unique id
@@ -467,6 +467,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--stages", type=int, default=0,
+                    help="pipeline stages (default: the config's, at least N)")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
                     help="blocks per stage: cost-balanced (default) or even by count (Q6)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
