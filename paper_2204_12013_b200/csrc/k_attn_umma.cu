@@ -30,6 +30,18 @@ constexpr int D = 64, BQ = 128, BKV = 128, ST = 2;
 constexpr int kThreads = 192;
 constexpr float LOG2E = 1.4426950408889634f;
 
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  uint32_t r;   // one F2FP: hi -> upper half, lo -> lower half, round to nearest even
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// 2^x on MUFU.EX2 alone (flush-to-zero): arguments are s*scale - max <= 0.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 constexpr uint32_t idesc_f16(int m, int n, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
@@ -182,11 +194,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < BKV; i += 2) {
-        const float p0 = exp2f(fmaf(__uint_as_float(t[i]), sl2, -mnz));
-        const float p1 = exp2f(fmaf(__uint_as_float(t[i + 1]), sl2, -mnz));
+        const float p0 = ex2(fmaf(__uint_as_float(t[i]), sl2, -mnz));
+        const float p1 = ex2(fmaf(__uint_as_float(t[i + 1]), sl2, -mnz));
         sum += p0 + p1;
-        const __nv_bfloat162 hv = __floats2bfloat162_rn(p0, p1);
-        t[i / 2] = (uint32_t)__bfloat16_as_ushort(hv.x) | ((uint32_t)__bfloat16_as_ushort(hv.y) << 16);
+        t[i / 2] = pack_bf2(p0, p1);
       }
       l = l * corr + sum;
       if (j > 0) {
