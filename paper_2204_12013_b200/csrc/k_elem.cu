@@ -73,7 +73,7 @@ __global__ void ln_bwd_dx_kernel(int R, int H, const float *__restrict__ dy,
 }
 
 // ------------------------------------------------------- column reductions
-constexpr int CR_ROWS = 64, CR_COLS = 128;
+constexpr int CR_ROWS = 64, CR_COLS = 128;   // scalar path (and partial-buffer sizing)
 
 template <typename TA, typename T>
 __global__ void colreduce_partial_kernel(int mode, int R, int N, const TA *__restrict__ A,
@@ -247,14 +247,15 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
   }
 }
 
-// Column reduction, 8 columns per thread: block = 8 warps x 32 lanes covers
-// 256 columns x CRV_ROWS rows (warp w takes rows w, w+8, ...); the 8 warp
-// partials are added in a fixed order through shared memory and written to
-// part[row block]. The last block of a column block to arrive (atomic ticket)
-// then adds all row-block partials in ascending order into out: one launch,
+// Column reduction over 64-column x 128-row tiles: thread t owns the 8
+// columns 8 (t % 8).. of rows t / 8 + 32 k (k < 4); the 32 row groups are
+// added in a fixed order through shared memory and written to part[row
+// block]. The last tile of a column block to arrive (atomic ticket) adds the
+// row-block partials: 4 threads per column each sum every 4th row block,
+// then the 4 sums are added in a fixed order into out. One launch,
 // deterministic whatever the arrival order. out1 (if any) gets the LN-gamma
 // form sum a * xhat, out0 (if any) the plain sum.
-constexpr int CRV_ROWS = 256;
+constexpr int CRV_ROWS = 128, CRV_COLS = 64;
 template <typename TA, typename T>
 __global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int chunks,
                                                             const TA *__restrict__ A,
@@ -265,62 +266,83 @@ __global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int ch
                                                             unsigned *__restrict__ tickets,
                                                             float *__restrict__ out0,
                                                             float *__restrict__ out1) {
-  __shared__ float sh[8][256];   // 8 warps x 256 columns
+  __shared__ float sh[2][32][CRV_COLS + 1];
+  __shared__ float fin[2][4][CRV_COLS];
   __shared__ bool last;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n = (blockIdx.x * 32 + lane) * 8;
-  const int r0 = blockIdx.y * CRV_ROWS, r1 = min(R, r0 + CRV_ROWS);
+  const int t = threadIdx.x, c8 = t % 8, rs = t / 8;
+  const int n = blockIdx.x * CRV_COLS + 8 * c8;
+  const int r0 = blockIdx.y * CRV_ROWS;
   float a0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float a1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (n < N) {
-#pragma unroll 4
-    for (int r = r0 + warp; r < r1; r += 8) {
+#pragma unroll
+    for (int k = 0; k < CRV_ROWS / 32; ++k) {
+      const int r = r0 + rs + 32 * k;
+      if (r >= R) break;
       const size_t idx = (size_t)r * N + n;
       const V8 a = ld8(A + idx);
       if (out1) {
         const V8 xx = ld8(X + idx);
-        const float mu = mean[r], rs = rstd[r];
+        const float mu = mean[r], rsd = rstd[r];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a1[i] += a.v[i] * ((xx.v[i] - mu) * rs);
+        for (int i = 0; i < 8; ++i) a1[i] += a.v[i] * ((xx.v[i] - mu) * rsd);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) a0[i] += a.v[i];
     }
   }
-  const int c = threadIdx.x;   // 256 columns of this block
-  const int nn = blockIdx.x * 256 + c;
-  const size_t plane = (size_t)chunks * N;          // part[0] = plain sums, part[plane] = gamma form
-  for (int w2 = 0; w2 < 2; ++w2) {
-    float *o = w2 ? out1 : out0;
-    if (!o) continue;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sh[warp][lane * 8 + i] = w2 ? a1[i] : a0[i];
-    __syncthreads();
-    if (nn < N) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s += sh[w][c];
-      part[w2 * plane + (size_t)blockIdx.y * N + nn] = s;
-    }
-    __syncthreads();
+  for (int i = 0; i < 8; ++i) {
+    sh[0][rs][8 * c8 + i] = a0[i];
+    sh[1][rs][8 * c8 + i] = a1[i];
   }
-  __threadfence();
-  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == (unsigned)chunks - 1;
+  __syncthreads();
+  const size_t plane = (size_t)chunks * N;          // part[0] = plain sums, part[plane] = gamma form
+  if (t < 2 * CRV_COLS) {
+    const int w2 = t / CRV_COLS, c = t % CRV_COLS, nn = blockIdx.x * CRV_COLS + c;
+    float *o = w2 ? out1 : out0;
+    if (o && nn < N) {
+      float s = 0.f;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) s += sh[w2][j][c];
+      part[w2 * plane + (size_t)blockIdx.y * N + nn] = s;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (t == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == (unsigned)chunks - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (nn < N) {
+  {
+    const int c = t % CRV_COLS, q = t / CRV_COLS;    // 4 threads per column
+    const int nn = blockIdx.x * CRV_COLS + c;
     for (int w2 = 0; w2 < 2; ++w2) {
-      float *o = w2 ? out1 : out0;
-      if (!o) continue;
-      const float *p = part + w2 * plane + nn;
       float s = 0.f;
-#pragma unroll 8
-      for (int ch = 0; ch < chunks; ++ch) s += __ldcg(p + (size_t)ch * N);
-      o[nn] += s;
+      if ((w2 ? out1 : out0) && nn < N) {
+        const float *p = part + w2 * plane + nn;
+        // 16 loads in flight per batch, then added in ascending order
+        for (int ch0 = q; ch0 < chunks; ch0 += 64) {
+          float v[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int ch = ch0 + 4 * k;
+            v[k] = ch < chunks ? __ldcg(p + (size_t)ch * N) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) s += v[k];
+        }
+      }
+      fin[w2][q][c] = s;
     }
   }
-  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;   // ready for the next call on this buffer
+  __syncthreads();
+  if (t < 2 * CRV_COLS) {
+    const int w2 = t / CRV_COLS, c = t % CRV_COLS, nn = blockIdx.x * CRV_COLS + c;
+    float *o = w2 ? out1 : out0;
+    if (o && nn < N) o[nn] += ((fin[w2][0][c] + fin[w2][1][c]) + fin[w2][2][c]) + fin[w2][3][c];
+  }
+  if (t == 0) tickets[blockIdx.x] = 0u;             // ready for the next call on this buffer
 }
 
 // -------------------------------------------------------------- embedding
@@ -657,7 +679,7 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
 
 // Layout of `partial`: kTickets arrival counters first (fixed place whatever
 // N a call uses), then 2 planes of row-block partials.
-constexpr int kTickets = 256;   // column blocks of 256: N <= 65536
+constexpr int kTickets = 1024;  // column blocks of 64: N <= 65536
 size_t colreduce_partial_floats(int R, int N) {
   return kTickets + 2 * (size_t)((R + CR_ROWS - 1) / CR_ROWS) * N;
 }
@@ -667,7 +689,7 @@ void colreduce_vec(int R, int N, const void *A, const void *X, const float *mean
                    const float *rstd, float *partial, float *out0, float *out1, cudaStream_t s) {
   const int chunks = (R + CRV_ROWS - 1) / CRV_ROWS;
   unsigned *tickets = reinterpret_cast<unsigned *>(partial);
-  dim3 grid((N + 255) / 256, chunks);
+  dim3 grid((N + CRV_COLS - 1) / CRV_COLS, chunks);
   colreduce_vec_kernel<TA, T><<<grid, 256, 0, s>>>(R, N, chunks, cp<TA>(A), cp<T>(X), mean, rstd,
                                                    partial + kTickets, tickets, out0, out1);
   ++g_launches;
