@@ -99,10 +99,13 @@ def test_gemm_epilogues(prec, epi, M, N, K):
 @pytest.mark.skipif(os.environ.get("BB_GEMM_TILE") is not None or
                     os.environ.get("BB_GEMM_EPI") is not None, reason="already forced")
 @pytest.mark.parametrize("force", [("BB_GEMM_TILE", "256"), ("BB_GEMM_TILE", "128"),
+                                   ("BB_GEMM_TILE", "pair"), ("BB_GEMM_TILE", "pair128"),
                                    ("BB_GEMM_EPI", "lsu")])
 def test_gemm_forced_variants(force):
     """The other GEMM kernels stay correct: single-CTA 128 x 256 / 128 x 128
-    tiles (BB_GEMM_TILE) and the LSU epilogue (BB_GEMM_EPI=lsu, taken for
+    tiles (BB_GEMM_TILE), CTA pairs everywhere (small fp32-accumulating dW
+    shapes then take pair tiles with up to 8 serialised K splits and TMA
+    add-reductions), and the LSU epilogue (BB_GEMM_EPI=lsu, taken for
     unaligned operands): rerun the layout and epilogue tests forced."""
     env = dict(os.environ, **{force[0]: force[1]})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
