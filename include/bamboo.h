@@ -83,7 +83,10 @@ typedef struct {
   const void *nccl_id;          /* 128-byte ncclUniqueId (same on all ranks) or NULL       */
   int profile;                  /* 1 = time every kernel class with CUDA events; the local
                                    nodes then share ONE serialised stream (no FRC overlap),
-                                   so use it for per-kernel timing, not for throughput    */
+                                   so use it for per-kernel timing, not for throughput.
+                                   Each step first parks that stream for 200 ms of device
+                                   time (a spin kernel, outside device_ms) so the host
+                                   enqueues ahead: no launch latency inside the brackets */
 } bb_opts;
 
 typedef struct {

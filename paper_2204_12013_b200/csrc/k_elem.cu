@@ -781,6 +781,23 @@ cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *
   return cudaGetLastError();
 }
 
+// One thread spinning on the global timer: holds a stream for `ns` so the host
+// can enqueue ahead of the device (profile mode: no host gaps inside the
+// per-kernel event brackets).
+__global__ void gpu_sleep_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(10000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t gpu_sleep(unsigned long long ns, cudaStream_t s) {
+  gpu_sleep_kernel<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s) {
   sum_fixed_kernel<<<1, 1024, 0, s>>>(n, x, out);
   ++g_launches;

@@ -24,6 +24,9 @@ struct Gemm {
   void *aux;          // pre-activation [M][ldc] storage type (BIAS_GELU out, GELU_BWD in)
 };
 
+// Profile mode: park a stream for `ns` of device time (not counted as a launch).
+cudaError_t gpu_sleep(unsigned long long ns, cudaStream_t s);
+
 // Global launch counter (kernels launched by this library in this process).
 extern long long g_launches;
 

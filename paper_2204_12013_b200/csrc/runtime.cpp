@@ -976,6 +976,9 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     if (!tok && !c.resident) throw RtError{BB_E_STATE, "no resident inputs (bb_stage_inputs)"};
     CK(cudaSetDevice(c.o.device));
     c.x.barrier();   // every rank finished the previous step: receive slots are free
+    // profile mode: park the serialised stream while the host enqueues the
+    // step, so host launch latency never sits inside a kernel's event bracket
+    if (c.o.profile && c.serial) CK(k::gpu_sleep(200000000ull, c.serial));
     begin_step(c);
     c.resident_step = tok == nullptr;
     if (tok) {
