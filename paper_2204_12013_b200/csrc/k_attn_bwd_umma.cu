@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                  dv_done = sdp_full + 16u, dq_full = sdp_full + 24u, dq_free = sdp_full + 32u,
                  fin = sdp_full + 40u;
   auto ds_free = [&](int b2) { return sdp_full + 48u + 8u * b2; };
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (1 + 2 * NST + 8));
+  const uint32_t s_full = sdp_full, dp_full = sdp_full + 64u, s_free = sdp_full + 72u;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (1 + 2 * NST + 10));
   float *lsed = reinterpret_cast<float *>(gbase + L::LSED);
 
   const int nkb = (S + BLK - 1) / BLK;
@@ -118,7 +119,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(qdo_full(s), 1);
       mbar_init(qdo_empty(s), 1);
     }
-    mbar_init(sdp_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(s_free, 8);
     mbar_init(pds_full, 8);
     mbar_init(dv_done, 1);
     mbar_init(ds_free(0), 1);
@@ -189,31 +192,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_s = idesc_f16(128, BLK, false, false);
       const uint32_t id_kv = idesc_f16(128, D, false, true);    // dV, dK: B = dO / Q MN-major
       const uint32_t id_q = idesc_f16(128, D, true, true);      // dQ: A = dS (from dS^T), B = K
-      auto issue_sdp = [&](int t) {
+      // S^T(t+1) is issued as soon as the softmax warps hold S^T(t) in
+      // registers (s_free), dP^T(t+1) once they are done with step t.
+      auto issue_s = [&](int t) {
         const int st = t % NST;
         mbar_wait(qdo_full(st), (t / NST) & 1);
         tc_fence_after();
-        const uint32_t q = base + L::Q + st * 16384, d = base + L::DO + st * 16384;
+        const uint32_t q = base + L::Q + st * 16384;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_bf16(t_s, smem_desc(base + L::K + kk * 32, 16, 1024), smem_desc(q + kk * 32, 16, 1024),
                    id_s, kk > 0 ? 1u : 0u);
+        mma_commit(s_full);
+      };
+      auto issue_dp = [&](int t) {      // Q/dO stage t already waited by issue_s(t)
+        const uint32_t d = base + L::DO + (t % NST) * 16384;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_bf16(t_dp, smem_desc(base + L::V + kk * 32, 16, 1024),
                    smem_desc(d + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(sdp_full);
+        mma_commit(dp_full);
       };
       stamp(0);
       mbar_wait(kv_full, 0);
       stamp(1);
-      issue_sdp(0);
+      issue_s(0);
+      issue_dp(0);
       for (int t = 0; t < n; ++t) {
         const int st = t % NST;
-        mbar_wait(pds_full, t & 1);       // P^T, dS^T in smem; S^T, dP^T read out
+        if (t + 1 < n) {
+          mbar_wait(s_free, t & 1);       // S^T(t) is in the softmax warps' registers
+          tc_fence_after();
+          issue_s(t + 1);
+        }
+        mbar_wait(pds_full, t & 1);       // P^T, dS^T written; dP^T read out
         if (t < 8) stamp(2 + t);
         tc_fence_after();
-        if (t + 1 < n) issue_sdp(t + 1);
+        if (t + 1 < n) issue_dp(t + 1);
         const uint32_t q = base + L::Q + st * 16384, d = base + L::DO + st * 16384;
         const uint32_t dst = base + L::DST + (t & 1) * 32768;
         // dV += P^T dO_i: A = P^T from TMEM (16 queries = 8 columns per K step)
@@ -264,71 +279,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = i0 + t, st = t % NST;
       const bool diag = causal && i == kb;
       const float *ls = lsed + st * 2 * BLK;
-      mbar_wait(sdp_full, t & 1);
+      mbar_wait(s_full, t & 1);
       const bool tr = warp == 2 && lane == 0 && t < 8;
       if (tr) stamp(20 + t);
-      // P^T (TMEM) is free once dV of the previous step has read it, dS^T
-      // buffer t & 1 once dQ / dK of step t - 2 have; both usually are.
+      tc_fence_after();
+      // (a) S^T row of this warp's 64 queries, one TMEM round trip, then
+      // release S^T so the MMA warp can compute S^T(t+1) meanwhile
+      float p[64];
+      {
+        uint32_t sv[4][16];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) tmem_ld16_nowait(t_s + lane_off + 64 * g + 16 * hh, sv[hh]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) tmem_pin16(sv[hh]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          const float4 a = *reinterpret_cast<const float4 *>(ls + 64 * g + c);
+          const float l2[4] = {a.x * LOG2E, a.y * LOG2E, a.z * LOG2E, a.w * LOG2E};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            p[c + j] = ex2(fmaf(__uint_as_float(sv[(c + j) / 16][(c + j) % 16]), sl2, -l2[j]));
+        }
+      }
+      if (diag) {                                     // causal diagonal block: key > query -> 0
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (key > i * BLK + 64 * g + c) p[c] = 0.f;
+      }
+      // P^T -> TMEM once dV of the previous step has read it
       if (t > 0) mbar_wait(dv_done, (t - 1) & 1);
-      if (t > 1) mbar_wait(ds_free(t & 1), ((t >> 1) & 1) ^ 1);
       tc_fence_after();
       if (tr) stamp(28 + t);
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t pp[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) pp[c] = pack_bf2(p[16 * hh + 2 * c], p[16 * hh + 2 * c + 1]);
+        tmem_st8_nowait(t_p_base(t_pt, lane_off, g) + 8 * hh, pp);
+      }
+      // (b) dS^T = P^T (dP^T - D) -> smem buffer t & 1 (free once dQ / dK of
+      // step t - 2 have read it); dP^T chunks pipelined against the math
+      mbar_wait(dp_full, t & 1);
+      if (t > 1) mbar_wait(ds_free(t & 1), ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
       const uint32_t drow = base + L::DST + (t & 1) * 32768 + g * 16384 + r * 128;
-      // 4 chunks of 16 queries; chunk hh+1's TMEM loads are in flight while
-      // chunk hh is computed (tcgen05.wait::ld waits for all of them)
-      uint32_t sv[2][16], dv[2][16];
-      tmem_ld16_nowait(t_s + lane_off + 64 * g, sv[0]);
+      uint32_t dv[2][16];
       tmem_ld16_nowait(t_dp + lane_off + 64 * g, dv[0]);
       tmem_wait_ld();
-      tmem_pin16(sv[0]);
       tmem_pin16(dv[0]);
 #pragma unroll
       for (int hh = 0; hh < 4; ++hh) {
         const int cur = hh & 1;
-        const int c0 = 64 * g + 16 * hh;             // first query column
-        if (hh < 3) {
-          tmem_ld16_nowait(t_s + lane_off + c0 + 16, sv[cur ^ 1]);
-          tmem_ld16_nowait(t_dp + lane_off + c0 + 16, dv[cur ^ 1]);
-        }
-        uint32_t pp[8], dd[8];
-        // LSE (natural units) -> log2 units once per column pair
-        float l2[16], dq[16];
+        if (hh < 3) tmem_ld16_nowait(t_dp + lane_off + 64 * g + 16 * (hh + 1), dv[cur ^ 1]);
+        uint32_t dd[8];
 #pragma unroll
-        for (int c = 0; c < 16; c += 4) {
-          const float4 a = *reinterpret_cast<const float4 *>(ls + c0 + c);
-          const float4 d4 = *reinterpret_cast<const float4 *>(ls + BLK + c0 + c);
-          l2[c] = a.x * LOG2E; l2[c + 1] = a.y * LOG2E; l2[c + 2] = a.z * LOG2E; l2[c + 3] = a.w * LOG2E;
-          dq[c] = d4.x; dq[c + 1] = d4.y; dq[c + 2] = d4.z; dq[c + 3] = d4.w;
+        for (int c = 0; c < 16; c += 2) {
+          const int qc = 64 * g + 16 * hh + c;
+          dd[c / 2] = pack_bf2(p[16 * hh + c] * (__uint_as_float(dv[cur][c]) - ls[BLK + qc]),
+                               p[16 * hh + c + 1] * (__uint_as_float(dv[cur][c + 1]) - ls[BLK + qc + 1]));
         }
-        if (diag) {                                   // causal diagonal block: mask key > query
-#pragma unroll
-          for (int c = 0; c < 16; c += 2) {
-            const int qc = c0 + c;
-            float p0 = ex2(fmaf(__uint_as_float(sv[cur][c]), sl2, -l2[c]));
-            float p1 = ex2(fmaf(__uint_as_float(sv[cur][c + 1]), sl2, -l2[c + 1]));
-            if (key > i * BLK + qc) p0 = 0.f;
-            if (key > i * BLK + qc + 1) p1 = 0.f;
-            pp[c / 2] = pack_bf2(p0, p1);
-            dd[c / 2] = pack_bf2(p0 * (__uint_as_float(dv[cur][c]) - dq[c]),
-                                 p1 * (__uint_as_float(dv[cur][c + 1]) - dq[c + 1]));
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 16; c += 2) {
-            const float p0 = ex2(fmaf(__uint_as_float(sv[cur][c]), sl2, -l2[c]));
-            const float p1 = ex2(fmaf(__uint_as_float(sv[cur][c + 1]), sl2, -l2[c + 1]));
-            pp[c / 2] = pack_bf2(p0, p1);
-            dd[c / 2] = pack_bf2(p0 * (__uint_as_float(dv[cur][c]) - dq[c]),
-                                 p1 * (__uint_as_float(dv[cur][c + 1]) - dq[c + 1]));
-          }
-        }
-        // P^T: 8 TMEM columns (16 queries); dS^T: 2 swizzled 16-byte chunks
-        tmem_st8_nowait(t_p_base(t_pt, lane_off, g) + 8 * hh, pp);
         st_shared_v4(drow + (uint32_t)(((2 * hh) ^ (r & 7)) * 16), dd[0], dd[1], dd[2], dd[3]);
         st_shared_v4(drow + (uint32_t)(((2 * hh + 1) ^ (r & 7)) * 16), dd[4], dd[5], dd[6], dd[7]);
         if (hh < 3) {
           tmem_wait_ld();
-          tmem_pin16(sv[cur ^ 1]);
           tmem_pin16(dv[cur ^ 1]);
         }
       }
