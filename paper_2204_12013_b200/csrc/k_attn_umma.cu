@@ -10,7 +10,9 @@
 //               as soon as the softmax has read S_{j-1}, then
 //               O += P_{j-1} V_{j-1} (M=128, N=64, K=128; A = P from TMEM,
 //               V = MN-major smem B) once P_{j-1} is in TMEM;
-//   warps 2..5  softmax, thread r = query row r (TMEM lane r): pass 1 reads
+//   warps 2..9  softmax, two warps per TMEM lane quarter, each owning half of
+//               the 128 key columns of a row (row max and row sum combined
+//               through shared memory); thread r = query row r: pass 1 reads
 //               its S row (4 x 32 columns) for the row max, pass 2 re-reads
 //               it, exponentiates (exp2 of pre-scaled scores), packs P to
 //               bf16 registers and releases S; then, once PV_{j-1} is done,
@@ -27,7 +29,7 @@ namespace {
 using namespace sm100;
 
 constexpr int D = 64, BQ = 128, BKV = 128, ST = 2;
-constexpr int kThreads = 192;
+constexpr int kThreads = 64 + 8 * 32;   // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
@@ -51,7 +53,8 @@ struct SmemLayout {
   static constexpr int Q = 0;                         // 128 x 64 bf16 = 16 KB
   static constexpr int K = Q + BQ * D * 2;            // ST x 16 KB
   static constexpr int V = K + ST * BKV * D * 2;      // ST x 16 KB
-  static constexpr int BAR = V + ST * BKV * D * 2;
+  static constexpr int XCH = V + ST * BKV * D * 2;    // row-max / row-sum exchange (3 KB)
+  static constexpr int BAR = XCH + (2 * 2 * BQ + 2 * BQ) * 4;
   static constexpr int BYTES = BAR + 128 + 1024;
 };
 
@@ -88,8 +91,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(kv_empty(s), 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 4);     // one arrive per softmax warp
-    mbar_init(p_full, 4);
+    mbar_init(s_free, 8);     // one arrive per softmax warp
+    mbar_init(p_full, 8);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_qkv)) : "memory");
@@ -156,36 +159,43 @@ __global__ void __launch_bounds__(kThreads, 2)
       issue_pv(nkb - 1);
     }
   } else {
-    // ---------------- softmax warps: row r = query q0 + r, TMEM lane r
-    const int r = (warp % 4) * 32 + lane;
+    // ---------------- softmax warps: row r = query q0 + r (TMEM lane r); the
+    // two warps of a lane quarter split the 128 key columns (hf = half) and
+    // combine row max / row sum through shared memory (named barrier 1 + q)
+    const int q = warp % 4, hf = (warp - 2) / 4;
+    const int r = q * 32 + lane;
     const int qrow = q0 + r;
-    const uint32_t lane_off = (uint32_t)((warp % 4) * 32) << 16;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const float sl2 = rsqrtf((float)D) * LOG2E;
-    float m = -INFINITY, l = 0.f;
+    float *xm = reinterpret_cast<float *>(gbase + L::XCH);          // [2 parity][2 half][BQ]
+    float *xl = xm + 2 * 2 * BQ;                                     // [2 half][BQ]
+    float m = -INFINITY, l = 0.f;                                    // l: this half's partial sum
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const bool need_mask = (j * BKV + BKV > S) || (causal && j * BKV + BKV - 1 > q0);
       const int kmax = causal ? min(S - 1, qrow) : S - 1;   // last valid key of this row
-      // the whole S row in one TMEM round trip (4 x 32 columns)
-      uint32_t t[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c)
-        tmem_ld32_nowait(t_s + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(t + c * 32));
+      const int k0 = j * BKV + 64 * hf;                      // first key of this half
+      uint32_t t[64];
+      tmem_ld32_nowait(t_s + lane_off + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(t));
+      tmem_ld32_nowait(t_s + lane_off + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(t + 32));
       tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(t + c * 32));
+      tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(t));
+      tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(t + 32));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free);            // S may be overwritten by S_{j+1}
       if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i)
-          if (j * BKV + i > kmax) t[i] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < 64; ++i)
+          if (k0 + i > kmax) t[i] = __float_as_uint(-INFINITY);
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, __uint_as_float(t[i]));
+      for (int i = 0; i < 64; ++i) mx = fmaxf(mx, __uint_as_float(t[i]));
+      xm[((j & 1) * 2 + hf) * BQ + r] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      mx = fmaxf(xm[((j & 1) * 2 + 0) * BQ + r], xm[((j & 1) * 2 + 1) * BQ + r]);
       const float mn = fmaxf(m, mx * sl2);
       const float corr = mn == -INFINITY ? 1.f : exp2f(m - mn);
       m = mn;
@@ -193,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // P = exp2(s * sl2 - m), packed to bf16 pairs in place
       float sum = 0.f;
 #pragma unroll
-      for (int i = 0; i < BKV; i += 2) {
+      for (int i = 0; i < 64; i += 2) {
         const float p0 = ex2(fmaf(__uint_as_float(t[i]), sl2, -mnz));
         const float p1 = ex2(fmaf(__uint_as_float(t[i + 1]), sl2, -mnz));
         sum += p0 + p1;
@@ -204,49 +214,40 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(o_done, (j - 1) & 1);    // PV_{j-1} done: O stable, P columns free
         tc_fence_after();
       }
-      // P row -> TMEM (lane r, 64 columns of bf16 pairs)
-      tmem_st32_nowait(t_p + lane_off, t);
-      tmem_st32_nowait(t_p + lane_off + 32, t + 32);
-      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {
-        uint32_t ov[D];
-        tmem_ld32_nowait(t_o + lane_off, *reinterpret_cast<uint32_t(*)[32]>(ov));
-        tmem_ld32_nowait(t_o + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(ov + 32));
+      // this half's P -> TMEM (lane r, 32 columns of bf16 pairs)
+      tmem_st32_nowait(t_p + lane_off + 32 * hf, t);
+      if (j > 0 && __any_sync(0xffffffffu, corr != 1.f)) {   // this half's 32 O columns
+        uint32_t ov[32];
+        tmem_ld32_nowait(t_o + lane_off + 32 * hf, ov);
         tmem_wait_ld();
-        tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(ov));
-        tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(ov + 32));
+        tmem_pin(ov);
 #pragma unroll
-        for (int i = 0; i < D; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-        tmem_st32_nowait(t_o + lane_off, ov);
-        tmem_st32_nowait(t_o + lane_off + 32, ov + 32);
+        for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+        tmem_st32_nowait(t_o + lane_off + 32 * hf, ov);
       }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
+    xl[hf * BQ + r] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    const float lt = xl[r] + xl[BQ + r];              // fixed order: half 0 + half 1
     mbar_wait(o_done, (nkb - 1) & 1);
     tc_fence_after();
-    float ov[D];
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float t[32];
-      tmem_ld32(t_o + lane_off + c * 32, t);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) ov[c * 32 + i] = t[i];
-    }
+    float ov[32];
+    tmem_ld32(t_o + lane_off + 32 * hf, ov);
     if (qrow < S) {
-      const float inv = 1.f / l;
-      __nv_bfloat16 *orow = o + ((size_t)row_base + qrow) * H + h * D;
+      const float inv = 1.f / lt;
+      __nv_bfloat16 *orow = o + ((size_t)row_base + qrow) * H + h * D + 32 * hf;
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        uint4 u;
-        __nv_bfloat162 *hv = reinterpret_cast<__nv_bfloat162 *>(&u);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          hv[i] = __floats2bfloat162_rn(ov[8 * c + 2 * i] * inv, ov[8 * c + 2 * i + 1] * inv);
-        *reinterpret_cast<uint4 *>(orow + 8 * c) = u;
-      }
-      lse[((size_t)b * nh + h) * S + qrow] = (m + log2f(l)) / LOG2E;
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4 *>(orow + 8 * c) =
+            make_uint4(pack_bf2(ov[8 * c] * inv, ov[8 * c + 1] * inv),
+                       pack_bf2(ov[8 * c + 2] * inv, ov[8 * c + 3] * inv),
+                       pack_bf2(ov[8 * c + 4] * inv, ov[8 * c + 5] * inv),
+                       pack_bf2(ov[8 * c + 6] * inv, ov[8 * c + 7] * inv));
+      if (hf == 0) lse[((size_t)b * nh + h) * S + qrow] = (m + log2f(lt)) / LOG2E;
     }
   }
   tc_fence_before();
