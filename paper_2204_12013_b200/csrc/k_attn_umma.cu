@@ -68,13 +68,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint8_t *gbase = smem_raw + (base - raw);
   const uint32_t bars = base + L::BAR;
   const uint32_t q_full = bars;
-  auto kv_full = [&](int s) { return bars + 8u * (1 + s); };
-  auto kv_empty = [&](int s) { return bars + 8u * (1 + ST + s); };
-  const uint32_t s_full = bars + 8u * (1 + 2 * ST);
-  const uint32_t s_free = bars + 8u * (2 + 2 * ST);
-  const uint32_t p_full = bars + 8u * (3 + 2 * ST);
-  const uint32_t o_done = bars + 8u * (4 + 2 * ST);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (5 + 2 * ST));
+  // separate K and V rings: K_j is released by S_j (early), V_j by PV_j (late),
+  // so K_{j+1} streams in while the softmax of block j-1 still runs
+  auto k_full = [&](int s) { return bars + 8u * (1 + s); };
+  auto v_full = [&](int s) { return bars + 8u * (1 + ST + s); };
+  auto k_empty = [&](int s) { return bars + 8u * (1 + 2 * ST + s); };
+  auto v_empty = [&](int s) { return bars + 8u * (1 + 3 * ST + s); };
+  const uint32_t s_full = bars + 8u * (1 + 4 * ST);
+  const uint32_t s_free = bars + 8u * (2 + 4 * ST);
+  const uint32_t p_full = bars + 8u * (3 + 4 * ST);
+  const uint32_t o_done = bars + 8u * (4 + 4 * ST);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (5 + 4 * ST));
 
   // heaviest (causal: last) query blocks first
   const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -87,8 +91,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < ST; ++s) {
-      mbar_init(kv_full(s), 1);
-      mbar_init(kv_empty(s), 1);
+      mbar_init(k_full(s), 1);
+      mbar_init(v_full(s), 1);
+      mbar_init(k_empty(s), 1);
+      mbar_init(v_empty(s), 1);
     }
     mbar_init(s_full, 1);
     mbar_init(s_free, 8);     // one arrive per softmax warp
@@ -115,11 +121,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       tma_load_2d(base + L::Q, &map_qkv, q_full, h * D, row_base + q0);
       for (int j = 0; j < nkb; ++j) {
         const int s = j % ST;
-        mbar_wait(kv_empty(s), ((j / ST) & 1) ^ 1);
-        mbar_expect_tx(kv_full(s), 2 * BKV * D * 2);
-        tma_load_2d(base + L::K + s * BKV * D * 2, &map_qkv, kv_full(s), H + h * D,
+        mbar_wait(k_empty(s), ((j / ST) & 1) ^ 1);
+        mbar_expect_tx(k_full(s), BKV * D * 2);
+        tma_load_2d(base + L::K + s * BKV * D * 2, &map_qkv, k_full(s), H + h * D,
                     row_base + j * BKV);
-        tma_load_2d(base + L::V + s * BKV * D * 2, &map_qkv, kv_full(s), 2 * H + h * D,
+        mbar_wait(v_empty(s), ((j / ST) & 1) ^ 1);
+        mbar_expect_tx(v_full(s), BKV * D * 2);
+        tma_load_2d(base + L::V + s * BKV * D * 2, &map_qkv, v_full(s), 2 * H + h * D,
                     row_base + j * BKV);
       }
     }
@@ -128,9 +136,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t id_s = idesc_f16(128, BKV, false, false);
       const uint32_t id_o = idesc_f16(128, D, false, true);
       auto issue_pv = [&](int j) {       // O += P_j V_j
+        const int s = j % ST;
+        mbar_wait(v_full(s), (j / ST) & 1);
         mbar_wait(p_full, j & 1);
         tc_fence_after();
-        const int s = j % ST;
         const uint32_t va = base + L::V + s * BKV * D * 2;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -140,12 +149,12 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma_bf16_ts(t_o, t_p + kk * 8, db, id_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(o_done);
-        mma_commit(kv_empty(s));
+        mma_commit(v_empty(s));
       };
       mbar_wait(q_full, 0);
       for (int j = 0; j < nkb; ++j) {
         const int s = j % ST;
-        mbar_wait(kv_full(s), (j / ST) & 1);
+        mbar_wait(k_full(s), (j / ST) & 1);
         if (j > 0) mbar_wait(s_free, (j - 1) & 1);    // S_{j-1} read out of TMEM
         tc_fence_after();
         const uint32_t ka = base + L::K + s * BKV * D * 2;
@@ -154,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma_bf16(t_s, smem_desc(base + L::Q + kk * 32, 16, 1024),
                    smem_desc(ka + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         mma_commit(s_full);
+        mma_commit(k_empty(s));
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nkb - 1);
