@@ -475,11 +475,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
-    rank, ws, local = dist_setup(args)
     if args.impl == "reference":
-        run_reference(args, rank, ws)
-    else:
-        run_ours(args, rank, ws, local)
+        # the oracle arm needs no GPU and no process group: rank 0 runs it,
+        # the other ranks exit 0 at once
+        run_reference(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
+        return
+    rank, ws, local = dist_setup(args)
+    run_ours(args, rank, ws, local)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
