@@ -7,6 +7,8 @@
 #include <cfloat>
 
 
+#include <algorithm>
+
 #include "k_common.cuh"
 
 namespace bb {
@@ -247,8 +249,8 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
   }
 }
 
-// Column reduction over 64-column x 128-row tiles: thread t owns the 8
-// columns 8 (t % 8).. of rows t / 8 + 32 k (k < 4); the 32 row groups are
+// Column reduction over 64-column x (row group) tiles: thread t owns the 8
+// columns 8 (t % 8).. of rows t / 8 + 32 k of its group; the 32 row groups are
 // added in a fixed order through shared memory and written to part[row
 // block]. The last tile of a column block to arrive (atomic ticket) adds the
 // row-block partials: 4 threads per column each sum every 4th row block,
@@ -271,14 +273,14 @@ __global__ void __launch_bounds__(256) colreduce_vec_kernel(int R, int N, int ch
   __shared__ bool last;
   const int t = threadIdx.x, c8 = t % 8, rs = t / 8;
   const int n = blockIdx.x * CRV_COLS + 8 * c8;
-  const int r0 = blockIdx.y * CRV_ROWS;
+  // this CTA's rows: row group blockIdx.y of `chunks` equal groups (multiples of 32)
+  const int per = ((R + chunks - 1) / chunks + 31) / 32 * 32;
+  const int r0 = blockIdx.y * per, r1 = min(R, r0 + per);
   float a0[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float a1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (n < N) {
-#pragma unroll
-    for (int k = 0; k < CRV_ROWS / 32; ++k) {
-      const int r = r0 + rs + 32 * k;
-      if (r >= R) break;
+#pragma unroll 4
+    for (int r = r0 + rs; r < r1; r += 32) {
       const size_t idx = (size_t)r * N + n;
       const V8 a = ld8(A + idx);
       if (out1) {
@@ -687,7 +689,10 @@ size_t colreduce_partial_floats(int R, int N) {
 template <typename TA, typename T>
 void colreduce_vec(int R, int N, const void *A, const void *X, const float *mean,
                    const float *rstd, float *partial, float *out0, float *out1, cudaStream_t s) {
-  const int chunks = (R + CRV_ROWS - 1) / CRV_ROWS;
+  // long-lived CTAs: ~4 per SM over the whole matrix, each looping over its
+  // row group (short CTAs paid the partial write + fence + ticket per wave)
+  const int cols = (N + CRV_COLS - 1) / CRV_COLS;
+  const int chunks = std::max(1, std::min((R + CRV_ROWS - 1) / CRV_ROWS, (148 * 4) / cols));
   unsigned *tickets = reinterpret_cast<unsigned *>(partial);
   dim3 grid((N + CRV_COLS - 1) / CRV_COLS, chunks);
   colreduce_vec_kernel<TA, T><<<grid, 256, 0, s>>>(R, N, chunks, cp<TA>(A), cp<T>(X), mean, rstd,
