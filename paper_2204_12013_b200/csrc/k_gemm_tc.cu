@@ -147,6 +147,8 @@ struct Smem {
 // on CTA 0's `tempty` (count 2 x kEpiWarps). Each SM fetches 32 KB per
 // K slab instead of 48 KB for the same 128 x 256 x 64 MMA work: the mainloop
 // is bound by L2 -> SM bandwidth, not by the tensor pipe.
+constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
+
 template <int BN, int EPI, int CG, bool TE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -203,12 +205,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CG == 2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(tmem_slot)),
-                   "n"(2 * BN));
+                   "n"(tmem_cols(2 * BN)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(tmem_slot)),
-                   "n"(2 * BN));
+                   "n"(tmem_cols(2 * BN)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -329,8 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int CW = F32OUT ? 32 : 64;
     constexpr bool HAS_IN = EPI == EPI_BIAS_RES || EPI == EPI_GELU_BWD;
     constexpr bool HAS_BIAS = EPI == EPI_BIAS || EPI == EPI_BIAS_RES || EPI == EPI_BIAS_GELU;
-    constexpr int NCH = (BN / 2) / CW;
+    // the tile's BN / CW column chunks alternate between the two warps of a
+    // lane quarter (chunk c goes to warp half c % 2)
+    constexpr int NCT = BN / CW;
     const int q = warp % 4, half = (warp - 2) / 4, ew = warp - 2;
+    const int nch = (NCT - half + 1) / 2;
     const uint32_t box0 = base + L::STAGES * L::STAGE + ew * 8192;
     const uint32_t rowoff = lane * 128;
     const uint32_t my_tempty0 = CG == 2 ? mapa(tempty_bar(0), 0) : tempty_bar(0);
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int fl = tile * CG + rank;
       const int acc = j & 1;
       const int mr = m0 + q * 32;                         // this warp's first row
-      const int nw = n0 + half * (BN / 2);                // this warp's first column
+      const int nw = n0 + half * CW;                      // this warp's first column
       const bool live = mr < g.M && nw < g.N;
       if (HAS_IN && live && lane == 0) {                  // prefetch chunk 0's row operand
         bulk_wait_read<0>();
@@ -362,17 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
 #pragma unroll 1
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int n = nw + ch * CW;
+      for (int ch = 0; ch < nch; ++ch) {
+        const int n = nw + ch * 2 * CW;
         const bool go = live && n < g.N;
         const int b = bsel;
         if (go) {
           if (lane == 0) {
             if (HAS_IN) {
-              if (ch + 1 < NCH && n + CW < g.N) {         // prefetch the next chunk's operand
+              if (ch + 1 < nch && n + 2 * CW < g.N) {     // prefetch the next chunk's operand
                 bulk_wait_read<0>();
                 mbar_expect_tx(in_bar(ew, b ^ 1), 4096);
-                tma_load_2d(box0 + (b ^ 1) * 4096, &map_x, in_bar(ew, b ^ 1), n + CW, mr);
+                tma_load_2d(box0 + (b ^ 1) * 4096, &map_x, in_bar(ew, b ^ 1), n + 2 * CW, mr);
               }
             } else if (EPI == EPI_BIAS_GELU) {
               bulk_wait_read<0>();                        // both boxes are written below
@@ -384,14 +389,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint32_t r0[32], r1[32];
         if (go) {
-          const uint32_t t = tmem + acc * BN + ((uint32_t)(q * 32) << 16) + half * (BN / 2) + ch * CW;
+          const uint32_t t = tmem + acc * BN + ((uint32_t)(q * 32) << 16) + (half + 2 * ch) * CW;
           tmem_ld32_nowait(t, r0);
           if (!F32OUT) tmem_ld32_nowait(t + 32, r1);
           tmem_wait_ld();
           tmem_pin(r0);
           if (!F32OUT) tmem_pin(r1);
         }
-        if (ch == NCH - 1 || !go) {
+        if (ch == nch - 1 || !go) {
           // all TMEM reads of this accumulator done: release it to the MMA warp
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         }
@@ -538,9 +543,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (CG == 2)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN)));
     else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols(2 * BN)));
   }
 }
 
@@ -789,6 +794,7 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     if (!e) return 0;
     if (!std::strcmp(e, "pair")) return 2;
     if (!std::strcmp(e, "pair128")) return 3;
+    if (!std::strcmp(e, "pair192")) return 4;
     if (!std::strcmp(e, "256")) return 256;
     if (!std::strcmp(e, "128")) return 128;
     return 0;
@@ -802,6 +808,11 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     return te ? launch_bn<128, 1, true>(g, s) : launch_bn<128, 1, false>(g, s);
   if (force == 256) return te ? launch_bn<256, 1, true>(g, s) : launch_bn<256, 1, false>(g, s);
   if (force == 3 && te) return launch_bn<128, 2, true>(g, s);
+  // 256 x 192 pair tiles (K-major B only: 96 B rows per CTA, N % 192 == 0):
+  // fewer tile rounds at N = 768, but measured no faster than 256 x 256 there
+  // (18.7 vs 18.9 us, 44.4 vs 43.7 us), so only on request (BB_GEMM_TILE=pair192)
+  if (force == 4 && te && !g.b_mn && g.epi != EPI_ACC_F32 && g.N % 192 == 0)
+    return launch_bn<192, 2, true>(g, s);
   if (!te) return launch_bn<256, 1, false>(g, s);
   // fp32-accumulating dW with few output tiles: the serialised split-K chain
   // (up to 8 links of a few us each on pairs) costs more than the smaller

@@ -59,7 +59,8 @@ def test_gemm_layouts(prec, impl, layout, shape):
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 6])
-@pytest.mark.parametrize("M,N,K", [(300, 200, 136), (300, 520, 136), (130, 768, 200)])
+@pytest.mark.parametrize("M,N,K", [(300, 200, 136), (300, 520, 136), (130, 768, 200),
+                                   (600, 576, 264)])
 def test_gemm_epilogues(prec, epi, M, N, K):
     """N >= 256 runs on CTA pairs (256 x 256 tiles): ragged M leaves the
     second CTA of the last pair partly or wholly past M."""
@@ -100,6 +101,7 @@ def test_gemm_epilogues(prec, epi, M, N, K):
                     os.environ.get("BB_GEMM_EPI") is not None, reason="already forced")
 @pytest.mark.parametrize("force", [("BB_GEMM_TILE", "256"), ("BB_GEMM_TILE", "128"),
                                    ("BB_GEMM_TILE", "pair"), ("BB_GEMM_TILE", "pair128"),
+                                   ("BB_GEMM_TILE", "pair192"),
                                    ("BB_GEMM_EPI", "lsu")])
 def test_gemm_forced_variants(force):
     """The other GEMM kernels stay correct: single-CTA 128 x 256 / 128 x 128
