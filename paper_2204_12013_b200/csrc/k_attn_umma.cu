@@ -20,6 +20,10 @@
 //               At the end: O / l and the log-sum-exp.
 // Same math and LSE convention as the mma.sync kernel (k_attn_tc.cu), which
 // the backward pass uses.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "k_common.cuh"
 #include "k_sm100.cuh"
 
@@ -60,7 +64,15 @@ struct SmemLayout {
 
 __global__ void __launch_bounds__(kThreads, 2)
     fa_fwd_umma_kernel(const __grid_constant__ CUtensorMap map_qkv, int S, int H, int nh,
-                       int causal, __nv_bfloat16 *__restrict__ o, float *__restrict__ lse) {
+                       int causal, __nv_bfloat16 *__restrict__ o, float *__restrict__ lse,
+                       unsigned long long *__restrict__ trace) {
+  auto stamp = [&](int k) {            // BB_ATTN_DBG & 8: per-CTA timeline (64 slots)
+    if (trace && k < 64) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      trace[((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + k] = tt;
+    }
+  };
   using L = SmemLayout;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -139,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = j % ST;
         mbar_wait(v_full(s), (j / ST) & 1);
         mbar_wait(p_full, j & 1);
+        if (j < 16) stamp(18 + j);
         tc_fence_after();
         const uint32_t va = base + L::V + s * BKV * D * 2;
 #pragma unroll
@@ -151,7 +164,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         mma_commit(o_done);
         mma_commit(v_empty(s));
       };
+      stamp(0);
       mbar_wait(q_full, 0);
+      stamp(1);
       for (int j = 0; j < nkb; ++j) {
         const int s = j % ST;
         mbar_wait(k_full(s), (j / ST) & 1);
@@ -163,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma_bf16(t_s, smem_desc(base + L::Q + kk * 32, 16, 1024),
                    smem_desc(ka + kk * 32, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         mma_commit(s_full);
+        if (j < 16) stamp(2 + j);
         mma_commit(k_empty(s));
         if (j > 0) issue_pv(j - 1);
       }
@@ -182,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float m = -INFINITY, l = 0.f;                                    // l: this half's partial sum
     for (int j = 0; j < nkb; ++j) {
       mbar_wait(s_full, j & 1);
+      if (warp == 2 && lane == 0 && j < 14) stamp(34 + j);
       tc_fence_after();
       const bool need_mask = (j * BKV + BKV > S) || (causal && j * BKV + BKV - 1 > q0);
       const int kmax = causal ? min(S - 1, qrow) : S - 1;   // last valid key of this row
@@ -238,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (warp == 2 && lane == 0 && j < 14) stamp(48 + j);
       if (lane == 0) mbar_arrive(p_full);
     }
     xl[hf * BQ + r] = l;
@@ -287,9 +305,34 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
     attr = true;
   }
   dim3 grid((S + BQ - 1) / BQ, nh, B);
+  static const bool tr = [] {
+    const char *e = std::getenv("BB_ATTN_DBG");
+    return e && (std::atoi(e) & 8);
+  }();
+  static unsigned long long *tbuf = nullptr;
+  static size_t tn = 0;
+  const size_t ctas = (size_t)grid.x * grid.y * grid.z;
+  if (tr && tn < ctas) {
+    if (tbuf) cudaFree(tbuf);
+    cudaMalloc(&tbuf, ctas * 64 * 8);
+    tn = ctas;
+  }
+  if (tr) cudaMemsetAsync(tbuf, 0, ctas * 64 * 8, s);
   fa_fwd_umma_kernel<<<grid, kThreads, SmemLayout::BYTES, s>>>(
-      map, S, H, nh, causal ? 1 : 0, reinterpret_cast<__nv_bfloat16 *>(o), lse);
+      map, S, H, nh, causal ? 1 : 0, reinterpret_cast<__nv_bfloat16 *>(o), lse,
+      tr ? tbuf : nullptr);
   ++g_launches;
+  if (tr) {   // write fwd_trace.bin: dims, then 64 stamps per CTA
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h(ctas * 64);
+    cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE *f = fopen("fwd_trace.bin", "wb")) {
+      const int dims[3] = {(int)grid.x, (int)grid.y, (int)grid.z};
+      fwrite(dims, sizeof(int), 3, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   return cudaGetLastError();
 }
 
