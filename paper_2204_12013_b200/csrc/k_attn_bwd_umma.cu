@@ -221,11 +221,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < n; ++t) {
         const int st = t % NST;
         if (t + 1 < n) {
-          mbar_wait(s_free, t & 1);       // S^T(t) is in the softmax warps' registers
+          mbar_wait_spin(s_free, t & 1);  // S^T(t) is in the softmax warps' registers
           tc_fence_after();
           issue_s(t + 1);
         }
-        mbar_wait(pds_full, t & 1);       // P^T, dS^T written; dP^T read out
+        mbar_wait_spin(pds_full, t & 1);  // P^T, dS^T written; dP^T read out
         if (t < 8) stamp(2 + t);
         tc_fence_after();
         if (t + 1 < n) issue_dp(t + 1);
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       (t > 0 || kk > 0) ? 1u : 0u);
         mma_commit(dv_done);
         if (t > 0) {
-          mbar_wait(dq_free, (t - 1) & 1);
+          mbar_wait_spin(dq_free, (t - 1) & 1);
           tc_fence_after();
         }
         if (t < 8) stamp(10 + t);

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       auto issue_pv = [&](int j) {       // O += P_j V_j
         const int s = j % ST;
         mbar_wait(v_full(s), (j / ST) & 1);
-        mbar_wait(p_full, j & 1);
+        mbar_wait_spin(p_full, j & 1);
         if (j < 16) stamp(18 + j);
         tc_fence_after();
         const uint32_t va = base + L::V + s * BKV * D * 2;
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j = 0; j < nkb; ++j) {
         const int s = j % ST;
         mbar_wait(k_full(s), (j / ST) & 1);
-        if (j > 0) mbar_wait(s_free, (j - 1) & 1);    // S_{j-1} read out of TMEM
+        if (j > 0) mbar_wait_spin(s_free, (j - 1) & 1);    // S_{j-1} read out of TMEM
         tc_fence_after();
         const uint32_t ka = base + L::K + s * BKV * D * 2;
 #pragma unroll

@@ -66,6 +66,20 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap *map, uint32
       : "memory");
 }
 
+// Busy-poll variant (mbarrier.test_wait never suspends the thread): for the
+// single MMA-issuing thread, where wake-up latency is on the critical path.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
                                             int c0, int c1) {
   asm volatile(
