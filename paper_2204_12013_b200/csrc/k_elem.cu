@@ -5,7 +5,6 @@
 // computation on another node reproduces the normal one bit for bit
 // ("exactly the same computation").
 #include <cfloat>
-#include <cstdlib>
 
 
 #include <algorithm>
@@ -533,69 +532,6 @@ __global__ void __launch_bounds__(CES_T) ce_stream_kernel(int V, __nv_bfloat16 *
   }
 }
 
-// Row-staged bf16 cross entropy: the row (V·2 bytes, ~100 KB at the GPT-2
-// vocabulary) is read from HBM once into shared memory while the online
-// (max, sum) runs; the gradient is then computed from shared memory and
-// written back. HBM traffic is exactly one read + one write of the logits;
-// two CTAs fit per SM so one row's loads overlap the other's write-back.
-constexpr int CEM_T = 512;
-__global__ void __launch_bounds__(CEM_T) ce_smem_kernel(int V, __nv_bfloat16 *__restrict__ logits,
-                                                        const int32_t *__restrict__ tgt,
-                                                        float inv_ntok,
-                                                        float *__restrict__ loss_rows) {
-  extern __shared__ uint4 srow[];
-  __shared__ float shm[CEM_T / 32], shs[CEM_T / 32];
-  const int r = blockIdx.x;
-  uint4 *row = reinterpret_cast<uint4 *>(logits + (size_t)r * V);
-  const int nv = V / 8;
-  const int t = tgt[r];
-  const float xt = threadIdx.x == 0 ? __bfloat162float(logits[(size_t)r * V + t]) : 0.f;
-  const float LOG2E_ = 1.4426950408889634f;
-  float m = -INFINITY, s = 0.f;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < nv; i += CEM_T) {
-    const uint4 u = __ldcs(row + i);
-    srow[i] = u;
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      v[2 * j] = bf_lo(w[j]) * LOG2E_;
-      v[2 * j + 1] = bf_hi(w[j]) * LOG2E_;
-    }
-    float mx = v[0];
-#pragma unroll
-    for (int j = 1; j < 8; ++j) mx = fmaxf(mx, v[j]);
-    const float mn = fmaxf(m, mx);
-    float add = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) add += exp2f(v[j] - mn);
-    s = s * exp2f(m - mn) + add;
-    m = mn;
-  }
-  m = m / LOG2E_;
-  block_merge_fixed<CEM_T>(m, s, shm, shs);
-  const float lse = m + logf(s);
-  if (threadIdx.x == 0) loss_rows[r] = (lse - xt) * inv_ntok;
-  const float lse2 = lse * LOG2E_;
-  // each thread re-reads only the vectors it staged itself: no barrier needed
-#pragma unroll 4
-  for (int i = threadIdx.x; i < nv; i += CEM_T) {
-    const uint4 u = srow[i];
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = i * 8 + 2 * j;
-      const float p0 = exp2f(fmaf(bf_lo(w[j]), LOG2E_, -lse2)) - (c == t ? 1.f : 0.f);
-      const float p1 = exp2f(fmaf(bf_hi(w[j]), LOG2E_, -lse2)) - (c + 1 == t ? 1.f : 0.f);
-      o[j] = pack_bf2(p0 * inv_ntok, p1 * inv_ntok);
-    }
-    __stcs(row + i, make_uint4(o[0], o[1], o[2], o[3]));
-  }
-}
-constexpr int CEM_MAX_SMEM = 110 * 1024;   // two CTAs per SM (228 KB)
-
 __global__ void sum_fixed_kernel(int n, const float *__restrict__ x, float *__restrict__ out) {
   __shared__ float sh[1024];
   float s = 0.f;
@@ -838,15 +774,7 @@ cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const 
 
 cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *targets,
                           float inv_ntok, float *loss_rows, cudaStream_t s) {
-  const bool vec = V % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0;
-  if (bf16 && vec && (size_t)V * 2 <= CEM_MAX_SMEM && !getenv("BB_CE_STREAM")) {
-    // per device and cheap: set on every call (several devices per process)
-    cudaError_t e = cudaFuncSetAttribute(ce_smem_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CEM_MAX_SMEM);
-    if (e != cudaSuccess) return e;
-    ce_smem_kernel<<<R, CEM_T, (size_t)V * 2, s>>>(V, mp<__nv_bfloat16>(logits), targets,
-                                                   inv_ntok, loss_rows);
-  } else if (bf16 && vec) {
+  if (bf16 && V % 8 == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
     ce_stream_kernel<<<R, CES_T, 0, s>>>(V, mp<__nv_bfloat16>(logits), targets, inv_ntok,
                                          loss_rows);
   } else if (bf16)

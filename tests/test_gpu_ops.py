@@ -211,7 +211,7 @@ def test_layernorm(prec, R, H):
 
 
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
-@pytest.mark.parametrize("R,V", [(16, 128), (7, 50304), (33, 30528), (5, 65536)])
+@pytest.mark.parametrize("R,V", [(16, 128), (7, 50304), (33, 30528)])
 def test_cross_entropy(prec, R, V):
     import paper_2204_12013_b200 as bb
     logits = rnd(R, V, scale=2.0)
