@@ -1,20 +1,27 @@
 """Benchmark of the Bamboo redundant-computation pipeline step on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
 
 A step = one synchronous 1F1B training step with eager FRC in the bubbles
 (BASELINE.json north star) over M*mb synthetic sequences: every stage's
 forward/backward, the FRC forward of its successor, P2P activations /
-gradients, replica gradient sync and both Adam updates. Workload: BASELINE
-configs[1] = GPT-2 small (12 layers, H 768, S 1024), 4 stages, M=8 micro-
-batches of 8 sequences; stages are spread over the N GPUs (N=1: all four on
-one B200; N=8: 8 stages, one per GPU, same model and batch -> strong scaling).
+gradients, replica gradient sync and both Adam updates. Workload (default):
+BASELINE configs[3] = GPT-2 XL (48 layers, H 1600, 25 heads, S 1024), 8
+stages, M=32 micro-batches of 4 sequences — the north-star model. The 8
+stages are spread over the N GPUs (N=1: all eight on one B200; N=8: one per
+GPU; same model and batch -> strong scaling). At N=1 the FRC retention of
+all 8 replicas does not fit next to the 1F1B stash (DESIGN.md §4 "HBM"): the
+FRC budget (bb_opts.frc_retain_bytes) keeps what HBM leaves free and
+the lazy BRC recomputes the rest. --config C1/C2 select the other models.
 
 Prints ONE JSON line (rank 0). `value` = samples/s with inputs resident in HBM
 (bb_stage_inputs), device-timed with CUDA events between synchronised
 barriers, max over ranks; `e2e` = the same through bb_step with host buffers
-(token upload and loss read-back inside the timed region).
+(token upload and loss read-back inside the timed region). Also: RC-off
+throughput and the RC overhead, per-node busy / bubble / FRC time, the
+recovery matrix (victims 0, 1, P/2, P-1 x first FWD / mid BWD), the GEMM
+roofline fraction and the oracle's CPU baseline.
 """
 import argparse
 import json
@@ -107,6 +114,7 @@ def dist_setup(args):
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # (the harness's own barriers / max-over-ranks only: the library never uses NCCL)
     return rank, ws, local
 
 
@@ -235,6 +243,58 @@ def balanced_partition(m, P, rc=True):
     return best[1]
 
 
+AUTO = (1 << 64) - 1   # bb_opts.frc_retain_bytes: what HBM leaves free after the rest
+
+
+def plan_index(pipe, node, kind, nth):
+    """Index (into node's current list) just after its nth (1-based) `kind`."""
+    idx = [int(f[1]) for f in (l.split() for l in pipe.schedule_dump().splitlines()
+                               if not l.startswith("#")) if f[0] == str(node) and f[2] == kind]
+    return idx[nth - 1] + 1
+
+
+def recovery_matrix(pipe, P, M, ws, step_ms, rank):
+    """victims {0, 1, P/2, P-1} x {first FWD, ceil(M/2)-th
+    BWD}. Per point: the interrupted step + bb_recover (host wall time,
+    max over ranks), pause = that - the failure-free step (Q11), one step on
+    the failover plan (the spare tire), then bb_rejoin and one normal
+    step before the next point."""
+    import torch
+    out = []
+    for v in sorted({0, 1, P // 2, P - 1}):
+        for phase, kind, nth in (("first_fwd", "FWD", 1), ("mid_bwd", "BWD", -(-M // 2))):
+            pi = plan_index(pipe, v, kind, nth)
+            pipe.preempt(v, pi)
+            barrier(ws)
+            t0 = time.perf_counter()
+            status, _ = pipe.step()
+            rec = pipe.recover() if status == "preempted" else None
+            torch.cuda.synchronize()
+            barrier(ws)
+            t_int = allreduce_max((time.perf_counter() - t0) * 1e3, ws)
+            t1 = time.perf_counter()
+            pipe.step()
+            barrier(ws)
+            t_fo = allreduce_max((time.perf_counter() - t1) * 1e3, ws)
+            t2 = time.perf_counter()
+            pipe.rejoin()
+            barrier(ws)
+            t_rj = allreduce_max((time.perf_counter() - t2) * 1e3, ws)
+            pipe.step()
+            r = {"victim": v, "phase": phase, "at_instr": pi,
+                 "interrupted_step_ms": round(t_int, 2), "pause_ms": round(t_int - step_ms, 2),
+                 "relative_pause": round((t_int - step_ms) / step_ms, 4),
+                 "recover_ms": round(allreduce_max(rec.recover_ms if rec else 0.0, ws), 2),
+                 "brc_mb": rec.brc_mb if rec else 0,
+                 "frc_reused_mb": rec.frc_done_mb if rec else 0,
+                 "frc_recomputed_mb": rec.frc_recomputed_mb if rec else 0,
+                 "bytes_resent": int(rec.bytes_resent) if rec else 0,
+                 "failover_step_ms": round(t_fo, 2), "rejoin_ms": round(t_rj, 2)}
+            log(rank, "recovery", r)
+            out.append(r)
+    return out
+
+
 def run_ours(args, rank, ws, local):
     import torch
     import paper_2204_12013_b200 as bb
@@ -244,19 +304,22 @@ def run_ours(args, rank, ws, local):
     P = max(cfg.stages, ws, args.stages)
     M, mb = cfg.microbatches, cfg.micro_batch
     samples = M * mb
-    def fresh_id():   # every communicator needs its own unique id
-        return bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
+    def fresh_id():   # every context needs its own rendezvous
+        return bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None
     flat = make_params(m)
     tok, tgt = make_tokens(cfg, 0)
     host_batches = [make_tokens(cfg, s) for s in range(1, 3)]
     lps = balanced_partition(m, P) if args.partition == "balanced" else None
     common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
                   layers_per_stage=lps)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
 
     results = {}
     for rc in (False, True):
         log(rank, f"init rc={rc} P={P} M={M} mb={mb}")
-        pipe = bb.Pipeline(m, P, M, rc=rc, nccl_id=fresh_id(), **common)
+        extra = dict(frc_retain_bytes=AUTO if args.retain == "auto" else int(args.retain),
+                     timing=True) if rc else {}
+        pipe = bb.Pipeline(m, P, M, rc=rc, session_id=fresh_id(), **common, **extra)
         pipe.load_params(flat)
         pipe.stage_inputs(tok, tgt)
         for i in range(args.warmup):
@@ -269,34 +332,20 @@ def run_ours(args, rank, ws, local):
             clocks.start()
         ms, launches, _, _ = timed(pipe, args.steps, ws)
         clk = clocks.stop() if rc else None
-        # end to end through the public call with host buffers
         log(rank, f"timed: {ms / args.steps:.2f} ms/step")
-        ms_e2e, _, h2d, d2h = timed(pipe, args.steps, ws, host_inputs=host_batches)
-        log(rank, f"e2e: {ms_e2e / args.steps:.2f} ms/step")
-        pipe.stage_inputs(tok, tgt)
-        results[rc] = dict(ms=ms / args.steps, launches=launches, clocks=clk,
-                           e2e_ms=ms_e2e / args.steps, h2d=h2d / args.steps, d2h=d2h / args.steps)
+        res = dict(ms=ms / args.steps, launches=launches, clocks=clk)
         if rc:
-            # recovery latency: preempt the middle node in its backward phase
-            # (P:69), pause = interrupted step incl. bb_recover - failure-free step
-            v = P // 2
-            dump = pipe.schedule_dump().splitlines()
-            bwd_idx = [int(l.split()[1]) for l in dump if not l.startswith("#")
-                       and l.split()[0] == str(v) and l.split()[2] == "BWD"]
-            pi = bwd_idx[(M + 1) // 2 - 1] + 1
-            pipe.preempt(v, pi)
-            barrier(ws)
-            t0 = time.perf_counter()
-            status, _ = pipe.step()
-            rec = pipe.recover() if status == "preempted" else None
-            torch.cuda.synchronize()
-            barrier(ws)
-            t_int = allreduce_max((time.perf_counter() - t0) * 1e3, ws)
-            ms_fo, _, _, _ = timed(pipe, max(1, min(3, args.steps)), ws)
-            results["recovery"] = dict(victim=v, at_instr=pi, interrupted_step_ms=t_int,
-                                       recover_ms=allreduce_max(rec.recover_ms if rec else 0, ws),
-                                       brc_mb=rec.brc_mb if rec else 0,
-                                       failover_step_ms=ms_fo / max(1, min(3, args.steps)))
+            res["nodes"] = pipe.node_stats()       # the last timed step
+            res["retained"] = [pipe.stage_memory(s)[1] for s in range(P)]
+            res["slot_mb"] = [round(pipe.stage_memory(s)[0] / 2**20, 1) for s in range(P)]
+        # end to end through the public call with host buffers
+        ms_e2e, _, h2d, d2h = timed(pipe, e2e_steps, ws, host_inputs=host_batches)
+        log(rank, f"e2e: {ms_e2e / e2e_steps:.2f} ms/step")
+        pipe.stage_inputs(tok, tgt)
+        res.update(e2e_ms=ms_e2e / e2e_steps, h2d=h2d / e2e_steps, d2h=d2h / e2e_steps)
+        results[rc] = res
+        if rc and args.recovery:
+            results["recovery"] = recovery_matrix(pipe, P, M, ws, res["ms"], rank)
         pipe.close()
         del pipe
         torch.cuda.empty_cache()
@@ -305,7 +354,9 @@ def run_ours(args, rank, ws, local):
     # node on one serialised stream, each kernel bracketed by CUDA events on
     # that stream (concurrent streams would double-count overlapped time).
     log(rank, "profiled (serialised) steps for per-kernel times")
-    pipe = bb.Pipeline(m, P, M, rc=True, profile=True, nccl_id=fresh_id(), **common)
+    pipe = bb.Pipeline(m, P, M, rc=True, profile=True, session_id=fresh_id(),
+                       frc_retain_bytes=AUTO if args.retain == "auto" else int(args.retain),
+                       **common)
     pipe.load_params(flat)
     pipe.stage_inputs(tok, tgt)
     for _ in range(2):
@@ -329,24 +380,34 @@ def run_ours(args, rank, ws, local):
     launches = allreduce_sum(on["launches"], ws)
     on["h2d"] = allreduce_sum(on["h2d"], ws)
     on["d2h"] = allreduce_sum(on["d2h"], ws)
-    rec = results.get("recovery", {})
+    recm = results.get("recovery", [])
+    if ws > 1:   # every rank's own nodes
+        import torch.distributed as dist
+        allnodes = [None] * ws
+        dist.all_gather_object(allnodes, on["nodes"])
+        on["nodes"] = sorted((n for part in allnodes for n in part), key=lambda n: n["node"])
     if rank != 0:
         return
-    roof = {"bound": "tensor", "achieved": round(achieved, 1),
-            "peak": pk.get("bf16_tflops_sustained", 1377.6), "unit": "TFLOP/s",
-            "frac": round(achieved / pk.get("bf16_tflops_sustained", 1377.6), 4),
-            "traffic": None, "kernel": "gemm_tc (tcgen05 bf16, all GEMM launches of the step)",
+    sust = pk.get("bf16_tflops_sustained", 1377.6)
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": sust, "unit": "TFLOP/s",
+            "frac": round(achieved / sust, 4), "traffic": None,
+            "kernel": "gemm_tc (tcgen05 bf16, all GEMM launches of the step)",
             "launches_per_step": gemm_n,
             "timing": "CUDA events around every GEMM launch of one full step (RC on), all "
                       "local nodes serialised on one stream; sum of 2MNK over sum of durations",
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"}
-    ncu = os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")
+    ncu = os.path.join(ROOT, "profiles", f"r02_ncu_gemm_{cfg.name.lower()}.json")
     if os.path.exists(ncu):
         try:
-            roof["traffic"] = json.load(open(ncu)).get("dram_bytes_per_launch")
+            d = json.load(open(ncu))
+            roof["traffic"] = d.get("dram_bytes_per_launch")
+            roof["traffic_source"] = os.path.relpath(ncu, ROOT)
         except Exception:
             pass
     train_flop = useful_flop_per_sample(cfg)
+    mid = [r for r in recm if r["phase"] == "mid_bwd" and r["victim"] == P // 2]
+    nodes = [{k: (round(v, 2) if isinstance(v, float) else v) for k, v in n.items()}
+             for n in on["nodes"]]
     line = {
         "metric": BASELINE_METRIC,
         "value": round(value, 2), "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
@@ -359,15 +420,19 @@ def run_ours(args, rank, ws, local):
                    "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
                    "seq_len": m.seq_len, "parallelism": f"pp{P} on {ws} GPU(s)",
                    "layers_per_stage": lps or "even",
+                   "frc_retained_per_step": on["retained"], "saved_set_mb": on["slot_mb"],
                    "l2": "working set (weights, stash, FRC retention) >> 126 MB L2"},
         "rc_off": {"value": round(samples / (off["ms"] / 1e3), 2), "ms_per_step": round(off["ms"], 3)},
         "rc_overhead_pct": round(100.0 * (1 - off["ms"] / on["ms"]), 2),
-        "recovery": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in rec.items()},
-        "recovery_ms": round(rec.get("interrupted_step_ms", 0) - on["ms"], 3) if rec else None,
+        "rc_slowdown_pct": round(100.0 * (on["ms"] / off["ms"] - 1), 2),
+        "recovery_ms": mid[0]["pause_ms"] if mid else None,
+        "recovery": recm,
+        "nodes": nodes,
         "roofline": roof,
         "model_flops_frac": round(value * train_flop / (ws * pk.get("bf16_tflops", 1657.2) * 1e12), 4),
         "e2e": {"value": round(samples / (on["e2e_ms"] / 1e3), 2), "unit": "samples/s",
-                "h2d_bytes_per_step": int(on["h2d"]), "d2h_bytes_per_step": int(on["d2h"])},
+                "h2d_bytes_per_step": int(on["h2d"]), "d2h_bytes_per_step": int(on["d2h"]),
+                "steps": e2e_steps},
         "gpu_launches": int(launches),
         "clocks": on["clocks"],
         "kernel_ms_per_step": {k: round(v[1], 3) for k, v in ks.items()},
@@ -427,7 +492,7 @@ def cpu_baseline(cfg, budget_s=20.0):
     info = threadpoolctl.threadpool_info()
     threads = max([i.get("num_threads", 1) for i in info] or [1])
     return {"value": round(1.0 / per_seq, 5), "unit": "samples/s", "cores": threads,
-            "host_cpus": os.cpu_count(), "kind": "oracle",
+            "host_cpus": os.cpu_count(), "kind": "oracle (extrapolated)",
             "sample": f"{reps} reps of 1 sequence (S={m.seq_len}) through 1 block + LM head at "
                       f"{cfg.name} width, fp64 numpy fwd+bwd, scaled to {m.n_layer} blocks fwd+bwd"
                       f" + head + FRC forward"}
@@ -466,7 +531,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C1")
+    ap.add_argument("--config", default="C3",
+                    help="C3 (GPT-2 XL, the north-star model) by default; C1 / C2 / C0")
     ap.add_argument("--stages", type=int, default=0,
                     help="pipeline stages (default: the config's, at least N)")
     ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
@@ -474,6 +540,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--e2e-steps", type=int, default=5,
+                    help="steps of the end-to-end (host buffers) measurement")
+    ap.add_argument("--retain", default="auto",
+                    help="frc_retain_bytes per node: auto (free HBM) or bytes (0 = all M)")
+    ap.add_argument("--no-recovery", dest="recovery", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":
         # the oracle arm needs no GPU and no process group: rank 0 runs it,

@@ -13,18 +13,20 @@
  *
  * Processes and devices. One process per GPU. A context hosts the pipeline
  * NODES mapped to its rank (node n runs stage n until a failover); several
- * nodes may share one process/GPU (stages > GPUs). Nodes on different ranks
- * exchange activations, gradients and replica gradients with NCCL P2P over
- * NVLink on 2-rank communicators, one per (src node, dst node, message kind)
- * edge, created inside bb_init from the 128-byte ncclUniqueId the caller
- * broadcasts (bb_nccl_unique_id on rank 0). Each node uses two streams and
- * each edge one, so processes should set CUDA_DEVICE_MAX_CONNECTIONS=32 before
- * creating their CUDA context (otherwise unrelated streams share hardware
- * queues and can serialise behind spinning P2P kernels).
+ * nodes may share one process/GPU (stages > GPUs), and several processes may
+ * share one GPU (tests). Nodes on different ranks exchange activations,
+ * gradients and replica gradients through the library's own transport: the
+ * sender's copy engine writes the payload into the receiver's HBM over
+ * NVLink/NVSwitch (CUDA IPC), records an interprocess event and publishes a
+ * sequence number in host shared memory. The ranks rendezvous through a
+ * POSIX shared-memory segment named after a session id that the caller
+ * creates on rank 0 (bb_session_id) and broadcasts. Each node uses two
+ * streams and each cross-rank edge one, so processes should set
+ * CUDA_DEVICE_MAX_CONNECTIONS=32 before creating their CUDA context.
  *
  * Conventions for every entry point:
  *  - Returns bb_status (0 = BB_OK). No exception, exit() or abort() crosses
- *    the ABI; CUDA / NCCL failures map to BB_E_CUDA / BB_E_NCCL and the
+ *    the ABI; CUDA failures map to BB_E_CUDA (BB_E_NCCL is reserved) and the
  *    message is kept per context (bb_last_error).
  *  - Host pointers passed in are borrowed for the duration of the call only
  *    (copied before return). Output host buffers are caller-owned.
@@ -57,7 +59,15 @@ typedef enum {
   BB_E_UNSUPPORTED = -8   /* valid request this build does not implement                    */
 } bb_status;
 
-typedef enum { BB_RC_NONE = 0, BB_RC_EFLB = 1 /* eager FRC, lazy BRC */ } bb_rc_mode;
+/* Redundant-computation modes:
+ *  NONE  no replicas, no FRC: a preemption is fatal;
+ *  EFLB  eager FRC in the bubbles, lazy BRC on failure (the paper's choice);
+ *  LFLB  replicas kept in sync but no FRC: a failure recomputes the victim's
+ *        forward (lazy FRC) and backward (lazy BRC) for the whole step;
+ *  EFEB  eager FRC and eager BRC: node s also runs stage s+1's backward every
+ *        step from the gradient node s+2 sends it ("requires the output
+ *        of BNC_{n+2}"), so a failure needs no recomputation at all. */
+typedef enum { BB_RC_NONE = 0, BB_RC_EFLB = 1, BB_RC_LFLB = 2, BB_RC_EFEB = 3 } bb_rc_mode;
 typedef enum { BB_PREC_BF16 = 0, BB_PREC_FP32_CHECK = 1 } bb_precision;
 
 /* Transformer shape (readings in DESIGN.md): pre-LN GPT-2 block,
@@ -76,17 +86,28 @@ typedef struct {
   const int *layers_per_stage;  /* [stages] transformer blocks per stage, NULL = even split
                                    with the remainder on the last stages          */
   float lr, beta1, beta2, eps;  /* Adam, bias-corrected, no weight decay          */
-  int world_rank, world_size;   /* this process / number of processes (1 = no NCCL)        */
+  int world_rank, world_size;   /* this process / number of processes (1 = single process) */
   int device;                   /* CUDA device ordinal this process uses                   */
   const int *node_rank;         /* [stages] process rank hosting node n; NULL = contiguous
                                    blocks of ceil(stages/world_size) nodes per rank        */
-  const void *nccl_id;          /* 128-byte ncclUniqueId (same on all ranks) or NULL       */
+  const void *session_id;       /* 32-byte session id (bb_session_id on rank 0, same bytes
+                                   on every rank) naming the host-shm rendezvous; NULL
+                                   when world_size = 1                                    */
   int profile;                  /* 1 = time every kernel class with CUDA events; the local
                                    nodes then share ONE serialised stream (no FRC overlap),
                                    so use it for per-kernel timing, not for throughput.
                                    Each step first parks that stream for 200 ms of device
                                    time (a spin kernel, outside device_ms) so the host
                                    enqueues ahead: no launch latency inside the brackets */
+  size_t frc_retain_bytes;      /* per node: HBM for FRC saved sets kept for a lazy BRC
+                                   (SURVEY Q10). 0 = keep all M. Micro-batches past
+                                   the budget keep only the stage input and the output;
+                                   BRC recomputes their forward (bit-identical)          */
+  int frc_persistent;           /* 0 (default): FRC GEMMs launch one CTA per tile, so the
+                                   high-priority main stream takes SMs back at tile
+                                   granularity; 1: persistent full-device grids (r01)     */
+  int timing;                   /* 1 = per-instruction CUDA events on every node for
+                                   bb_node_stats (busy / bubble / FRC accounting)        */
 } bb_opts;
 
 typedef struct {
@@ -105,21 +126,42 @@ typedef struct {
   int resent_mb;         /* gradients the successor re-sent to the shadow                 */
   float recover_ms;      /* host wall time of bb_recover                                   */
   float loss;            /* loss of the interrupted step (NaN where not local)           */
+  float interrupted_step_ms;  /* host wall time of the bb_step call that was interrupted  */
+  int frc_recomputed_mb; /* forwards of the victim's stage recomputed during recovery: FRC
+                            catch-up, beyond-budget BRC re-forwards, LFLB lazy FRC        */
+  uint64_t bytes_resent; /* bytes re-sent (RESEND_GRAD) or rerouted during the recovery  */
 } bb_recovery_stats;
+
+/* Per-node accounting of the last step (opts.timing = 1), from CUDA events
+ * around every FWD / BWD (main stream) and FRC_FWD (FRC stream), relative to
+ * the node's step start. bubble = step - main busy; frc_hidden = FRC time
+ * that ran while the main stream was idle (fig:bubble). */
+typedef struct {
+  int node;              /* node id                                                        */
+  int n_fwd, n_bwd, n_frc;
+  float step_ms;         /* node main-stream step time (device)                           */
+  float busy_ms;         /* union of main-stream FWD/BWD intervals                         */
+  float bubble_ms;       /* step_ms - busy_ms                                              */
+  float frc_ms;          /* union of FRC intervals                                         */
+  float frc_hidden_ms;   /* FRC time inside main-stream idle time                          */
+} bb_node_stat;
 
 /* Fill *o with defaults: micro_batch 1, rc EFLB, bf16, Adam(1e-4, 0.9, 0.999, 1e-8),
  * single process on device 0. */
 void bb_default_opts(bb_opts *o);
 
-/* Write a fresh ncclUniqueId (128 bytes) into out (rank 0 only). */
-bb_status bb_nccl_unique_id(void *out, size_t cap);
+/* Write a fresh random 32-byte session id into out (cap >= 32; rank 0 only,
+ * then broadcast by the caller). */
+bb_status bb_session_id(void *out, size_t cap);
 
 /* Create a context for `stages` pipeline stages (P) and `microbatches` (M) per
  * step. Partitions layers, builds every node's static plan
  * (1F1B P:497; eager FRC P:520-521), allocates parameters, replicas
  * (P:429), activation stashes and FRC retention in HBM, creates
- * streams and the NCCL edge communicators. Errors: BB_E_INVAL for
- * n_layer < stages, rc with stages < 2, bad shapes; BB_E_OOM; BB_E_CUDA/NCCL. */
+ * streams and the cross-rank transport (rendezvous on opts.session_id).
+ * Errors: BB_E_INVAL for n_layer < stages, rc with stages < 2, bad shapes;
+ * BB_E_UNSUPPORTED for shapes the kernels do not take (bf16 needs
+ * d_model >= 64; head dim 64 or 32); BB_E_OOM; BB_E_CUDA. */
 bb_status bb_init(const bb_model *m, int stages, int microbatches, const bb_opts *o,
                   void **ctx_out);
 
@@ -132,7 +174,8 @@ bb_status bb_load_params(void *ctx, const float *host, size_t n);
 /* One training step over M*mb sequences: tokens, targets = host int32 arrays
  * [M*mb, seq_len] row-major (micro-batch k = rows k*mb..k*mb+mb-1). Every rank
  * passes the full arrays and uploads what its nodes need (the last node
- * fetches inputs for its FRC). Returns BB_E_PREEMPTED if an armed injection
+ * fetches inputs for its FRC). Token and target ids must lie in [0, vocab):
+ * BB_E_INVAL otherwise (checked before any device work). Returns BB_E_PREEMPTED if an armed injection
  * fired (bb_recover must follow). st may be NULL. tokens = targets = NULL
  * reuses the inputs last staged with bb_stage_inputs (already in HBM: no
  * host-to-device copy inside the call). */
@@ -175,6 +218,19 @@ enum { BB_STATE_PARAMS = 0, BB_STATE_GRADS = 1, BB_STATE_ADAM_M = 2, BB_STATE_AD
  * by its predecessor. BB_E_INVAL if that copy is not hosted by this process. */
 bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n);
 
+/* Overwrite stage `stage`'s fp32 state (what = BB_STATE_PARAMS, _ADAM_M or
+ * _ADAM_V; PARAMS also refreshes the bf16 working copy) in every copy this
+ * process hosts (primary and replica, so replica == primary is kept), from
+ * host[n]. For starting a step from a given state (e.g. an oracle's), at a
+ * step boundary. BB_E_INVAL for a bad stage, kind or size. */
+bb_status bb_write_state(void *ctx, int stage, int what, const float *host, size_t n);
+
+/* HBM plan of `stage`: bytes of one saved set (the activations its backward
+ * reads, one micro-batch) and how many FRC saved sets its replica keeps per
+ * step under opts.frc_retain_bytes (-1 if this process hosts no replica of
+ * the stage). Either output may be NULL. */
+bb_status bb_stage_memory(void *ctx, int stage, size_t *slot_bytes, int *retained);
+
 /* Number of parameters of `stage` and its offset in the canonical flat vector. */
 bb_status bb_stage_params(void *ctx, int stage, size_t *offset, size_t *count);
 
@@ -186,6 +242,10 @@ bb_status bb_schedule_dump(void *ctx, char *buf, size_t cap, size_t *needed);
 /* Text dump of the last recovery: the cut (instructions executed per node)
  * and the continuation lists, same line format. */
 bb_status bb_recovery_dump(void *ctx, char *buf, size_t cap, size_t *needed);
+
+/* Per-node busy / bubble / FRC accounting of the last step (opts.timing = 1):
+ * one entry per live local node, *n = count. BB_E_STATE if timing is off. */
+bb_status bb_node_stats(void *ctx, bb_node_stat *out, int cap, int *n);
 
 /* Per-kernel-class device time of the last step (profile = 1): for each class
  * c < *n_classes: name, launches, total ms, algorithmic flops or bytes. */

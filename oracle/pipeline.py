@@ -46,15 +46,18 @@ class Pipeline:
                  lr=1e-4, b1=0.9, b2=0.999, eps=1e-8):
         self.cfg = cfg
         m = cfg.model
-        self.P, self.M, self.rc = cfg.stages, cfg.microbatches, rc
+        self.P, self.M = cfg.stages, cfg.microbatches
+        self.mode_rc = pl.rc_mode(rc)       # none / eflb / lflb
+        self.rc = self.mode_rc != "none"
         self.lay = model.Layout(m)
         self.ranges = pl.partition(m.n_layer, self.P, layers_per_stage)
         self.hp = (lr, b1, b2, eps)
         self.nodes = {n: Node(n) for n in range(self.P)}
         self.mode = "normal"
-        self.victim = None
+        self.victims = []          # preempted nodes, oldest first (rejoin is LIFO)
+        self.history = []          # (plans, host, replica_on) before each failover
         self.dead = set()
-        self.plans = pl.normal_plans(self.P, self.M, rc)
+        self.plans = pl.normal_plans(self.P, self.M, self.mode_rc)
         self.host = {s: s for s in range(self.P)}
         self.replica_on = {s: ((s - 1) % self.P if rc else None) for s in range(self.P)}
         flat = np.asarray(flat_params, dtype=np.float64)
@@ -183,15 +186,22 @@ class Pipeline:
         for k in range(self.M):
             vals = [node.store[("loss", k)] for n, node in self.nodes.items()
                     if n not in self.dead and ("loss", k) in node.store]
-            loss += vals[0]
+            # LFLB: a last stage lost after its commit point took the only
+            # copy of its losses with it (no FRC recomputed them): the
+            # step's loss is unknown (its update is complete)
+            loss += vals[0] if vals else float("nan")
         self.step_no += 1
         self.last_stores = {n: node.store for n, node in self.nodes.items()}
         return loss
 
     # ------------------------------------------------------------ public API
     def preempt(self, v, pi):
-        """Arm a preemption of node v after pi instructions of the next step."""
-        if self.mode != "normal" or not self.rc:
+        """Arm a preemption of node v after pi instructions of the next step.
+        After a failover, another node can be lost if it is not adjacent to a
+        dead one (two independent recoveries); P:464's
+        consecutive-node case (the double-duty shadow, or a node whose
+        replica holder is dead) is Fatal."""
+        if not self.rc or not pl.recoverable(self.P, self.host, self.replica_on, self.dead, v):
             raise pl.Fatal("no replica available for the victim")
         self.pending = (v, pi)
 
@@ -233,15 +243,15 @@ class Pipeline:
         # promote the replica (the shadow executes the victim's work)
         c = self.nodes[u].copies[v]
         c["role"] = "primary"
-        self.host[v] = u
+        self.history.append((self.plans, dict(self.host), dict(self.replica_on)))
+        self.host, self.replica_on = pl.lose_node(P, self.host, self.replica_on, v)
         self.mode = "failover"
-        self.victim = v
-        _, self.replica_on = pl.failover_topology(P, v)
+        self.victims.append(v)
         live = {n: p for n, p in new.items()}
         pcs2, ch = self._run(live, {n: 0 for n in live}, ch)
         if any(pcs2[n] < len(live[n]) for n in live):
             raise pl.PlanError("deadlock in recovery continuation")
-        self.plans = pl.failover_plans(P, M, v)
+        self.plans = pl.failover_plans(P, M, v, self.history[-1][0])
         self.interrupted = None
         return self._end_step(), info
 
@@ -254,7 +264,7 @@ class Pipeline:
         normal plans resume. Values are unchanged by construction."""
         if self.mode != "failover" or self.interrupted is not None:
             raise RuntimeError("rejoin needs a recovered failover pipeline")
-        P, v = self.P, self.victim
+        P, v = self.P, self.victims[-1]    # the most recent victim returns first
         u, w = (v - 1) % P, (v + 1) % P
         node = self.nodes[v]
         node.copies = {}
@@ -268,14 +278,12 @@ class Pipeline:
         node.copies[w]["role"] = "replica"
         src["role"] = "replica"
         self.dead.discard(v)
-        self.host[v] = v
-        self.mode = "normal"
-        self.victim = None
-        self.replica_on = {s: (s - 1) % P for s in range(P)}
-        self.plans = pl.normal_plans(P, self.M, self.rc)
+        self.victims.pop()
+        self.plans, self.host, self.replica_on = self.history.pop()
+        self.mode = "failover" if self.victims else "normal"
 
     def dump(self):
         host, rep = (self.host, self.replica_on)
         mode = self.mode
-        return pl.dump(self.P, self.M, self.rc, self.ranges, self.plans, host, rep, None, mode,
-                       self.victim)
+        return pl.dump(self.P, self.M, self.mode_rc, self.ranges, self.plans, host, rep, None, mode,
+                       self.victims)

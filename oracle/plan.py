@@ -76,8 +76,25 @@ def partition(n_layer, P, layers_per_stage=None):
 # ----------------------------------------------------------------------------
 # normal plans (A2)
 # ----------------------------------------------------------------------------
+MODES = ("none", "eflb", "lflb")
+
+
+def rc_mode(rc):
+    """RC mode name from a bool (False = none, True = eflb) or a name."""
+    if isinstance(rc, str):
+        if rc not in MODES:
+            raise PlanError(f"unknown RC mode {rc}")
+        return rc
+    return "eflb" if rc else "none"
+
+
 def stage_plan(s, P, M, rc):
-    """Instruction list of node s in a failure-free step."""
+    """Instruction list of node s in a failure-free step. rc: False / "none"
+    (no redundancy), True / "eflb" (replica + eager FRC) or
+    "lflb" (replica kept in sync, no FRC: the victim's forward is recomputed
+    lazily on failure, "LFLB")."""
+    mode = rc_mode(rc)
+    rc, frc = mode != "none", mode == "eflb"
     if rc and P < 2:
         raise PlanError("RC needs P >= 2")
     I = []
@@ -88,14 +105,14 @@ def stage_plan(s, P, M, rc):
     W = min(P - 1 - s, M)
 
     def fwd(k):
-        if rc and s == P - 1:
+        if frc and s == P - 1:
             I.append(Instr(FRC_FWD, k, None, 0))
         if s > 0:
             I.append(Instr(RECV_ACT, k, s - 1, s))
         I.append(Instr(FWD, k, None, s))
         if s < P - 1:
             I.append(Instr(SEND_ACT, k, s + 1, s))
-            if rc:
+            if frc:
                 I.append(Instr(FRC_FWD, k, None, s + 1))
 
     def bwd(k):
@@ -410,11 +427,27 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     return new, info
 
 
-def failover_plans(P, M, v):
-    """Static failover plans for the iterations after a recovery."""
-    plans = normal_plans(P, M, True)
+def failover_plans(P, M, v, plans=None):
+    """Static failover plans for the iterations after a recovery:
+    the recovery transform of `plans` (default: the normal plans; after an
+    earlier failover, that failover's plans) at an empty cut."""
+    plans = normal_plans(P, M, True) if plans is None else plans
     new, _ = recovery_plans(plans, P, M, v, {n: 0 for n in plans}, {})
     return new
+
+
+def recoverable(P, host, replica_on, dead, v):
+    """A preemption of node v is recoverable iff v is alive, runs exactly its
+    own stage (a shadow running two stages loses one with no replica left:
+    P:464 "consecutive nodes"), and v's stage has a replica on a live node
+    (its predecessor). Non-adjacent preemptions after a failover are two
+    independent recoveries."""
+    if v in dead or not (0 <= v < P):
+        return False
+    if [X for X in range(P) if host[X] == v] != [v]:
+        return False
+    r = replica_on[v]
+    return r is not None and r not in dead and r == (v - 1) % P
 
 
 def cut(plans, v, pi):
@@ -446,9 +479,11 @@ def dump(P, M, rc, ranges, plans, host=None, replica_on=None, device=None, mode=
     if replica_on is None:
         replica_on = {s: ((s - 1) % P if rc else None) for s in range(P)}
     device = device or {n: 0 for n in range(P)}
-    hdr = f"# bamboo-plan v1 P={P} M={M} rc={'eflb' if rc else 'none'} mode={mode}"
+    hdr = f"# bamboo-plan v1 P={P} M={M} rc={rc_mode(rc)} mode={mode}"
     if mode != "normal":
-        hdr += f" victim={victim} shadow={(victim - 1) % P}"
+        vs = list(victim) if isinstance(victim, (list, tuple)) else [victim]
+        hdr += (f" victim={','.join(map(str, vs))}"
+                f" shadow={','.join(str((x - 1) % P) for x in vs)}")
     lines = [hdr]
     for X in range(P):
         a, b = ranges[X]
@@ -460,17 +495,23 @@ def dump(P, M, rc, ranges, plans, host=None, replica_on=None, device=None, mode=
     return "\n".join(lines) + "\n"
 
 
+def lose_node(P, host, replica_on, v):
+    """(host, replica_on) after node v died and its stage moved to the shadow
+    v-1 (Q21): v's stage runs on the shadow without a replica (the replica was
+    promoted), and every stage whose replica lived on v is unprotected."""
+    u = (v - 1) % P
+    host, replica_on = dict(host), dict(replica_on)
+    host[v] = u
+    for X in range(P):
+        if replica_on[X] == v:
+            replica_on[X] = None
+    replica_on[v] = None
+    return host, replica_on
+
+
 def failover_topology(P, v):
     """(host, replica_on) after stage v moved to its shadow (Q21)."""
-    u, w = (v - 1) % P, (v + 1) % P
-    host = {s: s for s in range(P)}
-    host[v] = u
-    replica_on = {s: (s - 1) % P for s in range(P)}
-    replica_on[v] = None
-    replica_on[w] = None
-    if (u - 1) % P == v:
-        replica_on[u] = None
-    return host, replica_on
+    return lose_node(P, {s: s for s in range(P)}, {s: (s - 1) % P for s in range(P)}, v)
 
 
 # ----------------------------------------------------------------------------
@@ -527,9 +568,9 @@ def dump_lines(plans):
     return "".join(line + "\n" for line in out)
 
 
-def recovery_dump(P, M, v, pi):
+def recovery_dump(P, M, v, pi, rc=True):
     """Cut + continuation text of an injection at (v, pi) (DESIGN.md format)."""
-    plans = normal_plans(P, M, True)
+    plans = normal_plans(P, M, rc)
     pcs, ch = cut(plans, v, pi)
     new, info = recovery_plans(plans, P, M, v, pcs, ch)
     hdr = (f"# bamboo-recovery v1 P={P} M={M} victim={v} shadow={info['shadow']} "

@@ -1,6 +1,7 @@
 """ctypes binding of include/bamboo.h — argument marshalling only.
 
-Every step of the hot path runs inside libbamboo.so (CUDA kernels + NCCL);
+Every step of the hot path runs inside libbamboo.so (CUDA kernels + its own
+CUDA-IPC transport);
 this module converts Python/numpy arguments into the C structs and pointers
 the C ABI takes and turns bb_status codes into exceptions. There is no
 fallback: if the library cannot be loaded, importing the product fails.
@@ -20,10 +21,11 @@ STATUS_NAMES = {0: "BB_OK", -1: "BB_E_INVAL", -2: "BB_E_CUDA", -3: "BB_E_NCCL", 
 PREC = {"bf16": 0, "fp32": 1}
 STATE = {"params": 0, "grads": 1, "adam_m": 2, "adam_v": 3}
 
-EXPORTED = ["bb_default_opts", "bb_nccl_unique_id", "bb_init", "bb_load_params", "bb_step",
-            "bb_stage_inputs",
-            "bb_preempt", "bb_recover", "bb_rejoin", "bb_read_state", "bb_stage_params", "bb_schedule_dump",
-            "bb_recovery_dump", "bb_kernel_stats", "bb_plan_dump", "bb_last_error", "bb_destroy",
+RC = {"none": 0, "eflb": 1, "lflb": 2, "efeb": 3}
+EXPORTED = ["bb_default_opts", "bb_session_id", "bb_init", "bb_load_params", "bb_step",
+            "bb_stage_inputs", "bb_preempt", "bb_recover", "bb_rejoin", "bb_read_state",
+            "bb_write_state", "bb_stage_memory", "bb_stage_params", "bb_schedule_dump", "bb_recovery_dump",
+            "bb_kernel_stats", "bb_node_stats", "bb_plan_dump", "bb_last_error", "bb_destroy",
             "bb_op_gemm", "bb_op_attention_fwd", "bb_op_attention_bwd", "bb_op_layernorm_fwd",
             "bb_op_layernorm_bwd", "bb_op_cross_entropy", "bb_op_adam"]
 
@@ -45,8 +47,9 @@ class BBOpts(ctypes.Structure):
                 ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
                 ("eps", ctypes.c_float), ("world_rank", ctypes.c_int),
                 ("world_size", ctypes.c_int), ("device", ctypes.c_int),
-                ("node_rank", ctypes.POINTER(ctypes.c_int)), ("nccl_id", ctypes.c_void_p),
-                ("profile", ctypes.c_int)]
+                ("node_rank", ctypes.POINTER(ctypes.c_int)), ("session_id", ctypes.c_void_p),
+                ("profile", ctypes.c_int), ("frc_retain_bytes", ctypes.c_size_t),
+                ("frc_persistent", ctypes.c_int), ("timing", ctypes.c_int)]
 
 
 class BBStepStats(ctypes.Structure):
@@ -59,7 +62,15 @@ class BBRecoveryStats(ctypes.Structure):
     _fields_ = [("victim", ctypes.c_int), ("shadow", ctypes.c_int), ("successor", ctypes.c_int),
                 ("commit", ctypes.c_int), ("brc_mb", ctypes.c_int), ("frc_done_mb", ctypes.c_int),
                 ("resent_mb", ctypes.c_int), ("recover_ms", ctypes.c_float),
-                ("loss", ctypes.c_float)]
+                ("loss", ctypes.c_float), ("interrupted_step_ms", ctypes.c_float),
+                ("frc_recomputed_mb", ctypes.c_int), ("bytes_resent", ctypes.c_uint64)]
+
+
+class BBNodeStat(ctypes.Structure):
+    _fields_ = [("node", ctypes.c_int), ("n_fwd", ctypes.c_int), ("n_bwd", ctypes.c_int),
+                ("n_frc", ctypes.c_int), ("step_ms", ctypes.c_float), ("busy_ms", ctypes.c_float),
+                ("bubble_ms", ctypes.c_float), ("frc_ms", ctypes.c_float),
+                ("frc_hidden_ms", ctypes.c_float)]
 
 
 class BBKernelStat(ctypes.Structure):
@@ -79,8 +90,8 @@ def lib():
         _lib.bb_init.argtypes = [ctypes.POINTER(BBModel), ctypes.c_int, ctypes.c_int,
                                  ctypes.POINTER(BBOpts), ctypes.POINTER(ctypes.c_void_p)]
         for name in ("bb_load_params", "bb_step", "bb_preempt", "bb_recover", "bb_read_state",
-                     "bb_stage_params", "bb_schedule_dump", "bb_recovery_dump", "bb_kernel_stats",
-                     "bb_last_error"):
+                     "bb_write_state", "bb_stage_memory", "bb_stage_params", "bb_schedule_dump", "bb_recovery_dump",
+                     "bb_kernel_stats", "bb_node_stats", "bb_last_error", "bb_session_id"):
             getattr(_lib, name).restype = ctypes.c_int
         _lib.bb_load_params.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
         _lib.bb_step.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -91,6 +102,13 @@ def lib():
         _lib.bb_rejoin.argtypes = [ctypes.c_void_p]
         _lib.bb_read_state.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_void_p, ctypes.c_size_t]
+        _lib.bb_write_state.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_size_t]
+        _lib.bb_node_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(BBNodeStat), ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int)]
+        _lib.bb_stage_memory.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_size_t),
+                                         ctypes.POINTER(ctypes.c_int)]
         _lib.bb_stage_params.argtypes = [ctypes.c_void_p, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_size_t),
                                          ctypes.POINTER(ctypes.c_size_t)]
@@ -104,7 +122,7 @@ def lib():
         _lib.bb_destroy.restype = None
         _lib.bb_default_opts.argtypes = [ctypes.POINTER(BBOpts)]
         _lib.bb_default_opts.restype = None
-        _lib.bb_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        _lib.bb_session_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
         _lib.bb_plan_dump.argtypes = [ctypes.POINTER(BBModel), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(BBOpts), ctypes.c_int, ctypes.c_int,
                                       ctypes.c_char_p, ctypes.c_size_t,
@@ -137,12 +155,14 @@ def _ints(xs):
 
 def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-4, beta1=0.9,
               beta2=0.999, eps=1e-8, world_rank=0, world_size=1, device=0, node_rank=None,
-              nccl_id=None, profile=False):
+              session_id=None, profile=False, frc_retain_bytes=0, frc_persistent=False,
+              timing=False):
+    """rc: True (= "eflb"), False (= "none") or a mode name in RC."""
     o = BBOpts()
     lib().bb_default_opts(ctypes.byref(o))
     keep = []
     o.micro_batch = micro_batch
-    o.rc = 1 if rc else 0
+    o.rc = RC[rc] if isinstance(rc, str) else (1 if rc else 0)
     o.prec = PREC[prec]
     a, p = _ints(layers_per_stage)
     keep.append(a)
@@ -152,19 +172,23 @@ def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-
     a, p = _ints(node_rank)
     keep.append(a)
     o.node_rank = p
-    if nccl_id is not None:
-        buf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+    if session_id is not None:
+        buf = ctypes.create_string_buffer(bytes(session_id), len(session_id))
         keep.append(buf)
-        o.nccl_id = ctypes.cast(buf, ctypes.c_void_p)
+        o.session_id = ctypes.cast(buf, ctypes.c_void_p)
     o.profile = int(bool(profile))
+    o.frc_retain_bytes = int(frc_retain_bytes)
+    o.frc_persistent = int(bool(frc_persistent))
+    o.timing = int(bool(timing))
     return o, keep
 
 
-def nccl_unique_id():
-    buf = ctypes.create_string_buffer(128)
-    st = lib().bb_nccl_unique_id(buf, 128)
+def session_id():
+    """32 random bytes (rank 0); broadcast them to the other ranks."""
+    buf = ctypes.create_string_buffer(32)
+    st = lib().bb_session_id(buf, 32)
     if st != BB_OK:
-        raise BambooError(st, "ncclGetUniqueId")
+        raise BambooError(st, "bb_session_id")
     return buf.raw
 
 
@@ -254,12 +278,33 @@ class Pipeline:
                     "bb_stage_params")
         return off.value, cnt.value
 
+    def stage_memory(self, stage):
+        """(bytes of one saved set, FRC saved sets the replica retains or -1)."""
+        b, r = ctypes.c_size_t(), ctypes.c_int()
+        self._check(lib().bb_stage_memory(self._h, stage, ctypes.byref(b), ctypes.byref(r)),
+                    "bb_stage_memory")
+        return b.value, r.value
+
     def read_state(self, stage, what="params", replica=False):
         _, n = self.stage_params(stage)
         out = np.empty(n, np.float32)
         self._check(lib().bb_read_state(self._h, stage, int(replica), STATE[what],
                                         out.ctypes.data, n), "bb_read_state")
         return out
+
+    def write_state(self, stage, what, values):
+        """Overwrite stage's fp32 params / adam_m / adam_v in every copy this
+        process hosts (primary and replica), e.g. to start a step from an
+        oracle state."""
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        self._check(lib().bb_write_state(self._h, stage, STATE[what], v.ctypes.data, v.size),
+                    "bb_write_state")
+
+    def node_stats(self):
+        arr = (BBNodeStat * 64)()
+        n = ctypes.c_int()
+        self._check(lib().bb_node_stats(self._h, arr, 64, ctypes.byref(n)), "bb_node_stats")
+        return [{f: getattr(arr[i], f) for f, _ in BBNodeStat._fields_} for i in range(n.value)]
 
     def schedule_dump(self):
         return _text(lib().bb_schedule_dump, self._h)

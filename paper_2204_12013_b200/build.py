@@ -16,16 +16,6 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def _nccl_libdir():
-    import importlib.util
-    spec = importlib.util.find_spec("torch")
-    if spec and spec.origin:
-        d = os.path.join(os.path.dirname(os.path.dirname(spec.origin)), "nvidia", "nccl", "lib")
-        if os.path.exists(os.path.join(d, "libnccl.so.2")):
-            return d
-    return "/usr/lib/x86_64-linux-gnu"
-
-
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                    "-I", INC, "-I", CSRC, "--expt-relaxed-constexpr", "-Xptxas", "-v"]
@@ -43,7 +33,7 @@ def _compile(src, force):
             os.path.getmtime(obj) >= max(os.path.getmtime(src), _newest_header()):
         return obj, None
     cmd = [NVCC] + _flags() + ["-c", src, "-o", obj]
-    if src.endswith(".cpp"):   # host code: plain g++ against the CUDA / NCCL headers
+    if src.endswith(".cpp"):   # host code: plain g++ against the CUDA headers
         cmd = ["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-Wall", "-I", INC, "-I", CSRC,
                "-I", "/usr/local/cuda/include", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,9 +56,7 @@ def build(force=False, verbose=False):
             if log:
                 print(log)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        nccl = _nccl_libdir()
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + \
-            ["-L", nccl, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl}"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

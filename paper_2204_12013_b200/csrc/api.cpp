@@ -1,6 +1,8 @@
 // api.cpp — the extern "C" boundary declared in include/bamboo.h.
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <fcntl.h>
+#include <unistd.h>
+#include <time.h>
 
 #include <cmath>
 #include <cstring>
@@ -41,11 +43,24 @@ void bb_default_opts(bb_opts *o) {
   o->device = 0;
 }
 
-bb_status bb_nccl_unique_id(void *out, size_t cap) {
-  if (!out || cap < sizeof(ncclUniqueId)) return BB_E_INVAL;
-  ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return BB_E_NCCL;
-  std::memcpy(out, &id, sizeof(id));
+bb_status bb_session_id(void *out, size_t cap) {
+  if (!out || cap < 32) return BB_E_INVAL;
+  uint8_t b[32] = {};
+  int fd = open("/dev/urandom", O_RDONLY);
+  size_t got = 0;
+  if (fd >= 0) {
+    const ssize_t r = read(fd, b, sizeof(b));
+    got = r > 0 ? (size_t)r : 0;
+    close(fd);
+  }
+  if (got < sizeof(b)) {   // no urandom: pid and clock are unique enough per launch
+    struct timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    const uint64_t v[3] = {(uint64_t)getpid(), (uint64_t)ts.tv_sec, (uint64_t)ts.tv_nsec};
+    std::memcpy(b, v, sizeof(v));
+  }
+  std::memset(out, 0, cap);
+  std::memcpy(out, b, sizeof(b));
   return BB_OK;
 }
 
@@ -93,6 +108,30 @@ bb_status bb_rejoin(void *ctx) {
 bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n) {
   if (!ctx || !host) return BB_E_INVAL;
   return bb::rt_read_state(*static_cast<Ctx *>(ctx), stage, replica, what, host, n);
+}
+
+bb_status bb_write_state(void *ctx, int stage, int what, const float *host, size_t n) {
+  if (!ctx || !host) return BB_E_INVAL;
+  return bb::rt_write_state(*static_cast<Ctx *>(ctx), stage, what, host, n);
+}
+
+bb_status bb_node_stats(void *ctx, bb_node_stat *out, int cap, int *n) {
+  if (!ctx) return BB_E_INVAL;
+  return bb::rt_node_stats(*static_cast<Ctx *>(ctx), out, cap, n);
+}
+
+bb_status bb_stage_memory(void *ctx, int stage, size_t *slot_bytes, int *retained) {
+  if (!ctx) return BB_E_INVAL;
+  Ctx &c = *static_cast<Ctx *>(ctx);
+  if (stage < 0 || stage >= (int)c.stages.size()) return BB_E_INVAL;
+  if (slot_bytes) *slot_bytes = c.stages[stage].slot_bytes;
+  if (retained) {
+    *retained = -1;
+    for (auto &kv : c.nodes)
+      for (auto &cc : kv.second.copies)
+        if (cc.first == stage && cc.second.replica) *retained = cc.second.retain;
+  }
+  return BB_OK;
 }
 
 bb_status bb_stage_params(void *ctx, int stage, size_t *offset, size_t *count) {
@@ -148,15 +187,15 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
     const int ws = op.world_size < 1 ? 1 : op.world_size;
     const int per = (P + ws - 1) / ws;
     for (int n = 0; n < P; ++n) dev[n] = op.node_rank ? op.node_rank[n] : std::min(n / per, ws - 1);
-    bb::Plans plans = bb::normal_plans(P, M, rc);
+    bb::Plans plans = bb::normal_plans(P, M, (int)op.rc);
     std::string s;
     if (victim < 0) {
-      s = bb::dump(P, M, rc, ranges, plans, bb::normal_topology(P, rc), dev, false, -1);
+      s = bb::dump(P, M, (int)op.rc, ranges, plans, bb::normal_topology(P, rc), dev, false, {});
     } else {
       if (!rc || victim >= P) return BB_E_INVAL;
       if (at_instr < 0) {
-        s = bb::dump(P, M, rc, ranges, bb::failover_plans(P, M, victim),
-                     bb::failover_topology(P, victim), dev, true, victim);
+        s = bb::dump(P, M, (int)op.rc, ranges, bb::failover_plans(P, M, victim, &plans),
+                     bb::failover_topology(P, victim), dev, true, {victim});
       } else {
         bb::Cut cut = bb::cut(plans, victim, at_instr);
         bb::RecoveryInfo info;
@@ -185,10 +224,12 @@ bb_status bb_op_gemm(int prec, int impl, int M, int N, int K, const void *A, int
   const bool b16 = prec == BB_PREC_BF16;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  if (b16 && impl == 0 && bb::k::gemm_tc_supported(g))
+  if (b16 && impl == 0) {
+    if (!bb::k::gemm_tc_supported(g)) return BB_E_UNSUPPORTED;   // no silent SIMT fallback
     e = bb::k::gemm_tc(g, s);
-  else
-    e = bb::k::gemm_simt(b16, g, s);
+  } else {
+    e = bb::k::gemm_simt(b16, g, s);   // fp32 check mode, or impl = 1 (explicit request)
+  }
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 
@@ -196,6 +237,7 @@ bb_status bb_op_attention_fwd(int prec, int B, int S, int H, int nh, int causal,
                               void *o, float *lse, void *stream) {
   cudaError_t e = bb::k::attention_fwd(prec == BB_PREC_BF16, B, S, H, nh, causal != 0, qkv, o,
                                        lse, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return BB_E_UNSUPPORTED;
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 
@@ -209,6 +251,7 @@ bb_status bb_op_attention_bwd(int prec, int B, int S, int H, int nh, int causal,
   cudaError_t e = bb::k::attention_bwd(prec == BB_PREC_BF16, B, S, H, nh, causal != 0, qkv, o, lse,
                                        dout, dqkv, scratch, static_cast<cudaStream_t>(stream));
   cudaFreeAsync(scratch, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return BB_E_UNSUPPORTED;
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 

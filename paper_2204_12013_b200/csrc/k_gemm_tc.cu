@@ -606,7 +606,10 @@ int *split_flags(int n, int *epoch) {
   std::lock_guard<std::mutex> lk(mu);
   if (!ring) {
     if (cudaMalloc(&ring, kRing * sizeof(int)) != cudaSuccess) return nullptr;
+    // legacy-stream memset, then a device sync: the flags are read by
+    // kernels on non-blocking streams
     if (cudaMemset(ring, 0, kRing * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
   }
   if (cursor + n > kRing) cursor = 0;
   int *p = ring + cursor;
@@ -688,7 +691,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
   // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU.
   const int nk = (g.K + BK - 1) / BK;
   int ksplit = 1;
-  if (EPI == EPI_ACC_F32 && tiles * 2 <= slots)
+  if (EPI == EPI_ACC_F32 && tiles * 2 <= slots && !g.tile_grid)
     ksplit = std::max(1, std::min({slots / tiles, nk / 8, 8}));
   int *flags = nullptr;
   int epoch = 0;
@@ -702,7 +705,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
   // tiles, so that split always runs on a lower-numbered CTA in the same
   // round: dispatched earlier, hence resident, even when other kernels share
   // the GPU and this grid is only partly resident (no co-residency assumed).
-  int pids = units < slots ? units : slots;
+  int pids = units < slots || g.tile_grid ? units : slots;
   if (ksplit > 1) pids = std::max(ksplit, pids / ksplit * ksplit);
   const int grid = pids * CG;
   if (CG == 1) {

@@ -22,6 +22,8 @@ struct Gemm {
   const void *bias;   // [N] storage type
   const void *res;    // [M][ldc] storage type (EPI_BIAS_RES)
   void *aux;          // pre-activation [M][ldc] storage type (BIAS_GELU out, GELU_BWD in)
+  bool tile_grid = false;   // one CTA (pair) per output tile instead of a persistent grid:
+                            // a low-priority stream's GEMM then yields SMs tile by tile
 };
 
 // Profile mode: park a stream for `ns` of device time (not counted as a launch).

@@ -109,7 +109,10 @@ std::vector<std::pair<int, int>> partition(int L, int P, const int *lps) {
 }
 
 // -------------------------------------------------------------- normal plan
-std::vector<Instr> stage_plan(int s, int P, int M, bool rc) {
+std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
+  // mode = bb_rc_mode: NONE 0, EFLB 1 (replicas + eager FRC), LFLB 2
+  // (replicas, no FRC: the forward is recomputed lazily on failure)
+  const bool rc = mode != 0, frc = mode == 1;
   if (rc && P < 2) throw PlanError("RC needs stages >= 2");
   std::vector<Instr> I;
   const bool need_tok = s == 0 || (rc && s == P - 1);
@@ -117,12 +120,12 @@ std::vector<Instr> stage_plan(int s, int P, int M, bool rc) {
   if (need_tok || need_tgt) I.push_back({LOAD_INPUTS, -1, -1, -1});
   const int W = std::min(P - 1 - s, M);
   auto fwd = [&](int k) {
-    if (rc && s == P - 1) I.push_back({FRC_FWD, k, -1, 0});
+    if (frc && s == P - 1) I.push_back({FRC_FWD, k, -1, 0});
     if (s > 0) I.push_back({RECV_ACT, k, s - 1, s});
     I.push_back({FWD, k, -1, s});
     if (s < P - 1) {
       I.push_back({SEND_ACT, k, s + 1, s});
-      if (rc) I.push_back({FRC_FWD, k, -1, s + 1});
+      if (frc) I.push_back({FRC_FWD, k, -1, s + 1});
     }
   };
   auto bwd = [&](int k) {
@@ -147,9 +150,9 @@ std::vector<Instr> stage_plan(int s, int P, int M, bool rc) {
   return I;
 }
 
-Plans normal_plans(int P, int M, bool rc) {
+Plans normal_plans(int P, int M, int mode) {
   Plans p;
-  for (int s = 0; s < P; ++s) p[s] = stage_plan(s, P, M, rc);
+  for (int s = 0; s < P; ++s) p[s] = stage_plan(s, P, M, mode);
   return p;
 }
 
@@ -383,8 +386,8 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
   return nw;
 }
 
-Plans failover_plans(int P, int M, int v) {
-  Plans plans = normal_plans(P, M, true);
+Plans failover_plans(int P, int M, int v, const Plans *base) {
+  Plans plans = base ? *base : normal_plans(P, M, true);
   std::map<int, int> pcs;
   for (auto &kv : plans) pcs[kv.first] = 0;
   return recovery_plans(plans, P, M, v, pcs, Channels{}, nullptr);
@@ -399,14 +402,24 @@ Topology normal_topology(int P, bool rc) {
   return t;
 }
 
-Topology failover_topology(int P, int v) {
-  Topology t = normal_topology(P, true);
-  const int u = (v - 1 + P) % P, w = (v + 1) % P;
-  t.host[v] = u;
+Topology lose_node(int P, const Topology &t0, int v) {
+  Topology t = t0;
+  t.host[v] = (v - 1 + P) % P;
+  for (int X = 0; X < P; ++X)
+    if (t.replica_on[X] == v) t.replica_on[X] = -1;
   t.replica_on[v] = -1;
-  t.replica_on[w] = -1;
-  if ((u - 1 + P) % P == v) t.replica_on[u] = -1;
   return t;
+}
+
+Topology failover_topology(int P, int v) { return lose_node(P, normal_topology(P, true), v); }
+
+bool recoverable(int P, const Topology &t, const std::vector<int> &dead, int v) {
+  auto is_dead = [&](int n) { return std::find(dead.begin(), dead.end(), n) != dead.end(); };
+  if (v < 0 || v >= P || is_dead(v)) return false;
+  for (int X = 0; X < P; ++X)
+    if ((t.host[X] == v) != (X == v)) return false;   // v runs exactly its own stage
+  const int r = t.replica_on[v];
+  return r >= 0 && !is_dead(r) && r == (v - 1 + P) % P;
 }
 
 // --------------------------------------------------------------------- dump
@@ -424,13 +437,19 @@ std::string dump_lines(const Plans &plans) {
   return o.str();
 }
 
-std::string dump(int P, int M, bool rc, const std::vector<std::pair<int, int>> &ranges,
+std::string dump(int P, int M, int rc, const std::vector<std::pair<int, int>> &ranges,
                  const Plans &plans, const Topology &topo, const std::vector<int> &node_device,
-                 bool failover, int victim) {
+                 bool failover, const std::vector<int> &victims) {
   std::ostringstream o;
-  o << "# bamboo-plan v1 P=" << P << " M=" << M << " rc=" << (rc ? "eflb" : "none")
+  static const char *names[] = {"none", "eflb", "lflb", "efeb"};
+  o << "# bamboo-plan v1 P=" << P << " M=" << M << " rc=" << names[rc]
     << " mode=" << (failover ? "failover" : "normal");
-  if (failover) o << " victim=" << victim << " shadow=" << (victim - 1 + P) % P;
+  if (failover) {
+    o << " victim=";
+    for (size_t i = 0; i < victims.size(); ++i) o << (i ? "," : "") << victims[i];
+    o << " shadow=";
+    for (size_t i = 0; i < victims.size(); ++i) o << (i ? "," : "") << (victims[i] - 1 + P) % P;
+  }
   o << '\n';
   for (int X = 0; X < P; ++X) {
     const int n = topo.host[X];

@@ -70,8 +70,9 @@ struct PlanError : std::exception {
 // Stage unit ranges [a, b] inclusive (units: 0 emb, 1..L blocks, L+1 head).
 std::vector<std::pair<int, int>> partition(int n_layer, int P, const int *layers_per_stage);
 
-std::vector<Instr> stage_plan(int s, int P, int M, bool rc);
-Plans normal_plans(int P, int M, bool rc);
+// mode = bb_rc_mode (0 none, 1 EFLB, 2 LFLB); a bool converts to none / EFLB.
+std::vector<Instr> stage_plan(int s, int P, int M, int mode);
+Plans normal_plans(int P, int M, int mode);
 
 // Round-robin lockstep (one instruction per node per round, ascending node
 // id); RECVs wait for their message, SENDs are buffered per (src,dst,kind).
@@ -93,7 +94,10 @@ struct RecoveryInfo {
 };
 Plans recovery_plans(const Plans &plans, int P, int M, int victim, const std::map<int, int> &pcs,
                      const Channels &ch, RecoveryInfo *info);
-Plans failover_plans(int P, int M, int victim);
+// Static failover plans after losing `victim`: the recovery transform of
+// `base` (nullptr = the normal plans; after an earlier failover, its plans)
+// at an empty cut.
+Plans failover_plans(int P, int M, int victim, const Plans *base = nullptr);
 
 struct Topology {
   std::vector<int> host;        // stage -> node
@@ -101,10 +105,18 @@ struct Topology {
 };
 Topology normal_topology(int P, bool rc);
 Topology failover_topology(int P, int victim);
+// Topology after node v died and its stage moved to the shadow v-1 (Q21):
+// v's stage runs unprotected on the shadow; every stage whose replica lived
+// on v loses its protection.
+Topology lose_node(int P, const Topology &t, int victim);
+// A preemption of node v is recoverable iff v is alive, runs exactly its own
+// stage, and that stage's replica lives on its live predecessor (a
+// non-adjacent second loss is an independent recovery).
+bool recoverable(int P, const Topology &t, const std::vector<int> &dead, int victim);
 
-std::string dump(int P, int M, bool rc, const std::vector<std::pair<int, int>> &ranges,
+std::string dump(int P, int M, int rc, const std::vector<std::pair<int, int>> &ranges,
                  const Plans &plans, const Topology &topo, const std::vector<int> &node_device,
-                 bool failover, int victim);
+                 bool failover, const std::vector<int> &victims);
 std::string dump_lines(const Plans &plans);
 
 }  // namespace bb

@@ -29,12 +29,6 @@ struct RtError {
       throw RtError{e_ == cudaErrorMemoryAllocation ? BB_E_OOM : BB_E_CUDA,                \
                     std::string(#x) + ": " + cudaGetErrorString(e_)};                      \
   } while (0)
-#define NK(x)                                                                              \
-  do {                                                                                     \
-    ncclResult_t r_ = (x);                                                                 \
-    if (r_ != ncclSuccess)                                                                 \
-      throw RtError{BB_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)};           \
-  } while (0)
 
 constexpr size_t ALIGN = 256;
 size_t al(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
@@ -181,13 +175,50 @@ void wait_ev(cudaStream_t s, cudaEvent_t e) {
   if (e) CK(cudaStreamWaitEvent(s, e, 0));
 }
 
+// Per-step bump arena. A step that needs more (a failover shadow runs two
+// stages; an interrupted step runs its prefix plus the continuation) spills
+// into extra chunks; the next begin_step regrows the arena to the peak, so
+// only the first step of a new plan pays a cudaMalloc.
 void *arena_alloc(Node &nd, size_t bytes) {
   const size_t b = al(bytes);
-  if (nd.arena_used + b > nd.arena_bytes) throw RtError{BB_E_OOM, "step arena exhausted"};
-  void *p = nd.arena + nd.arena_used;
-  nd.arena_used += b;
+  nd.arena_peak += b;
+  if (nd.arena_used + b <= nd.arena_bytes) {
+    void *p = nd.arena + nd.arena_used;
+    nd.arena_used += b;
+    return p;
+  }
+  void *p = dmalloc(b);
+  nd.arena_spill.push_back({static_cast<char *>(p), b});
   return p;
 }
+
+// opts.timing: a timing-enabled event pair around one instruction's work.
+cudaEvent_t tevent(Node &nd) {
+  if (nd.tnext == nd.tpool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    nd.tpool.push_back(e);
+  }
+  return nd.tpool[nd.tnext++];
+}
+struct TMark {
+  Ctx &c;
+  Node &nd;
+  cudaStream_t s;
+  int kind;
+  cudaEvent_t a = nullptr;
+  TMark(Ctx &c_, Node &nd_, cudaStream_t s_, int kind_) : c(c_), nd(nd_), s(s_), kind(kind_) {
+    if (!c.o.timing) return;
+    a = tevent(nd);
+    CK(cudaEventRecord(a, s));
+  }
+  ~TMark() noexcept(false) {
+    if (!a) return;
+    cudaEvent_t b = tevent(nd);
+    CK(cudaEventRecord(b, s));
+    nd.trec.push_back({kind, a, b});
+  }
+};
 
 const Entry &need(Node &nd, const Key &k) {
   auto it = nd.store.find(k);
@@ -231,14 +262,14 @@ enum ProfCls { PC_GEMM_FWD = 0, PC_GEMM_DX, PC_GEMM_DW, PC_ATTN_FWD, PC_ATTN_BWD
 const char *prof_names[PC_N] = {"gemm_fwd", "gemm_dx", "gemm_dw", "attn_fwd", "attn_bwd",
                                 "layernorm", "cross_entropy", "embedding", "adam", "colreduce"};
 
-void gemm(Ctx &c, Node &nd, cudaStream_t s, int cls, const k::Gemm &g) {
+void gemm(Ctx &c, Node &nd, cudaStream_t s, int cls, k::Gemm g, bool tile_grid = false) {
   Prof pf(c, nd, s, cls, 2.0 * g.M * (double)g.N * g.K);
-  cudaError_t e;
-  if (c.bf16 && k::gemm_tc_supported(g))
-    e = k::gemm_tc(g, s);
-  else
-    e = k::gemm_simt(c.bf16, g, s);
-  CK(e);
+  g.tile_grid = tile_grid;
+  // bf16: tcgen05 only (no silent SIMT fallback; rt_init rejects shapes the
+  // tensor-core path cannot take); fp32 check mode: SIMT FMA by definition.
+  if (c.bf16 && !k::gemm_tc_supported(g))
+    throw RtError{BB_E_UNSUPPORTED, "GEMM shape/alignment not supported by the tcgen05 path"};
+  CK(c.bf16 ? k::gemm_tc(g, s) : k::gemm_simt(false, g, s));
 }
 }  // namespace
 
@@ -252,7 +283,7 @@ float *pg(const Copy &cp, size_t off) { return cp.grad + off; }
 // Forward of stage X for micro-batch k on stream s. Returns the output
 // pointer (activation in the arena) or nullptr for the last stage.
 void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStream_t s,
-                   const void *x_in, void *x_out, float *loss_rows) {
+                   const void *x_in, void *x_out, float *loss_rows, bool tg = false) {
   const Dims &d = c.d;
   const StageInfo &si = c.stages[X];
   char *sl = cp.slots + (size_t)slot * si.slot_bytes;
@@ -276,7 +307,7 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
       }
       gemm(c, nd, s, PC_GEMM_FWD,
            {R, 3 * H, H, sl + u.h1, H, false, pw(c, cp, p.wqkv), H, false, k::EPI_BIAS,
-            sl + u.qkv, 3 * H, pw(c, cp, p.bqkv), nullptr, nullptr});
+            sl + u.qkv, 3 * H, pw(c, cp, p.bqkv), nullptr, nullptr}, tg);
       {
         Prof pf(c, nd, s, PC_ATTN_FWD, 0);
         CK(k::attention_fwd(b16, d.mb, d.S, H, d.nh, d.causal, sl + u.qkv, sl + u.o,
@@ -284,7 +315,7 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
       }
       gemm(c, nd, s, PC_GEMM_FWD,
            {R, H, H, sl + u.o, H, false, pw(c, cp, p.wo), H, false, k::EPI_BIAS_RES, sl + u.x1, H,
-            pw(c, cp, p.bo), x, nullptr});
+            pw(c, cp, p.bo), x, nullptr}, tg);
       {
         Prof pf(c, nd, s, PC_LN, 0);
         CK(k::layernorm_fwd(b16, R, H, sl + u.x1, pw(c, cp, p.ln2g), pw(c, cp, p.ln2b),
@@ -292,10 +323,10 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
       }
       gemm(c, nd, s, PC_GEMM_FWD,
            {R, F, H, sl + u.h2, H, false, pw(c, cp, p.w1), H, false, k::EPI_BIAS_GELU, sl + u.act,
-            F, pw(c, cp, p.b1), nullptr, sl + u.pre});
+            F, pw(c, cp, p.b1), nullptr, sl + u.pre}, tg);
       gemm(c, nd, s, PC_GEMM_FWD,
            {R, H, F, sl + u.act, F, false, pw(c, cp, p.w2), F, false, k::EPI_BIAS_RES, out, H,
-            pw(c, cp, p.b2), sl + u.x1, nullptr});
+            pw(c, cp, p.b2), sl + u.x1, nullptr}, tg);
     } else {
       {
         Prof pf(c, nd, s, PC_LN, 0);
@@ -304,7 +335,7 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
       }
       gemm(c, nd, s, PC_GEMM_FWD,
            {R, d.V, H, sl + u.hf, H, false, pw(c, cp, p.whead), H, false, k::EPI_STORE,
-            sl + u.dlog, d.V, nullptr, nullptr, nullptr});
+            sl + u.dlog, d.V, nullptr, nullptr, nullptr}, tg);
       {
         Prof pf(c, nd, s, PC_CE, 0);
         const float inv = 1.0f / (float)((double)d.M * d.mb * d.S);
@@ -469,6 +500,22 @@ bool debug_on() {
   return on;
 }
 
+// Input of stage X for micro-batch k on node nd: tokens (X = 0) or the
+// activation key; makes stream s wait for it (and for the targets on the last
+// stage). Returns the activation pointer (nullptr for X = 0).
+const void *stage_input(Ctx &c, Node &nd, cudaStream_t s, int X, int k) {
+  const void *x_in = nullptr;
+  if (X == 0) {
+    wait_ev(s, need(nd, {K_TOK, k, 0}).ev);
+  } else {
+    const Entry &e = need(nd, {K_ACT, X, k});
+    wait_ev(s, e.ev);
+    x_in = e.p;
+  }
+  if (X == c.d.P - 1) wait_ev(s, need(nd, {K_TGT, k, 0}).ev);
+  return x_in;
+}
+
 // Execute one instruction of node nd; false = blocked on a local message.
 bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
   if (debug_on())
@@ -496,24 +543,33 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
     case FWD:
     case FRC_FWD: {
       Copy &cp = nd.copies.at(X);
-      cudaStream_t s = ins.kind == FRC_FWD ? nd.frc : nd.main;
-      const void *x_in = nullptr;
-      if (X == 0) {
-        wait_ev(s, need(nd, {K_TOK, k, 0}).ev);
+      const bool frc = ins.kind == FRC_FWD;
+      cudaStream_t s = frc ? nd.frc : nd.main;
+      const void *x_in = stage_input(c, nd, s, X, k);
+      // FRC retention budget (Q10): the first cp.retain FRC saved sets
+      // of a step stay in the pool for a lazy BRC; later ones run in the
+      // scratch slot and keep only their input and output (BRC recomputes).
+      bool keep = true;
+      int slot;
+      if (frc && cp.retain_left <= 0) {
+        keep = false;
+        slot = cp.nslots;
       } else {
-        const Entry &e = need(nd, {K_ACT, X, k});
-        wait_ev(s, e.ev);
-        x_in = e.p;
+        if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
+        slot = cp.free_slots.back();
+        cp.free_slots.pop_back();
+        if (frc) --cp.retain_left;
       }
-      if (X == P - 1) wait_ev(s, need(nd, {K_TGT, k, 0}).ev);
-      if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
-      const int slot = cp.free_slots.back();
-      cp.free_slots.pop_back();
       void *out = X < P - 1 ? arena_alloc(nd, msg_bytes(c, MSG_ACT, X)) : nullptr;
-      stage_forward(c, nd, cp, X, k, slot, s, x_in, out,
-                    s == nd.main ? nd.s_loss_main : nd.s_loss_frc);
+      {
+        TMark tm(c, nd, s, frc ? 1 : 0);
+        stage_forward(c, nd, cp, X, k, slot, s, x_in, out,
+                      s == nd.main ? nd.s_loss_main : nd.s_loss_frc,
+                      frc && !c.o.frc_persistent && !c.o.profile);
+      }
+      if (c.recovering && !frc && X == c.rec_stage) ++c.frc_recomputed;
       cudaEvent_t e = record(nd, s);
-      nd.store[{K_SAVED, X, k}] = {nullptr, e, slot};
+      nd.store[{K_SAVED, X, k}] = {nullptr, e, keep ? slot : -1};
       if (X < P - 1)
         nd.store[{K_ACT, X + 1, k}] = {out, e};
       else
@@ -532,9 +588,23 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       }
       const void *x_in = X == 0 ? nullptr : need(nd, {K_ACT, X, k}).p;
       void *dx = X > 0 ? arena_alloc(nd, msg_bytes(c, MSG_GRAD, X)) : nullptr;
-      stage_backward(c, nd, cp, X, k, sv.slot, nd.main, x_in, dout, dx);
+      TMark tm(c, nd, nd.main, 2);
+      int slot = sv.slot;
+      if (slot < 0) {
+        // an FRC saved set beyond the retention budget: recompute the forward
+        // from the retained stage input (same kernels, same order: the saved
+        // set is bit-identical to the one FNC / FRC produced)
+        if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
+        slot = cp.free_slots.back();
+        cp.free_slots.pop_back();
+        const void *xi = stage_input(c, nd, nd.main, X, k);
+        void *tmp = X < P - 1 ? arena_alloc(nd, msg_bytes(c, MSG_ACT, X)) : nullptr;
+        stage_forward(c, nd, cp, X, k, slot, nd.main, xi, tmp, nd.s_loss_main);
+        if (c.recovering) ++c.frc_recomputed;
+      }
+      stage_backward(c, nd, cp, X, k, slot, nd.main, x_in, dout, dx);
       cudaEvent_t e = record(nd, nd.main);
-      cp.free_slots.push_back(sv.slot);
+      cp.free_slots.push_back(slot);
       if (X > 0) nd.store[{K_DACT, X, k}] = {dx, e};
       if (k == M - 1) nd.store[{K_GRADSUM, X, 0}] = {cp.grad, e};
       return true;
@@ -553,10 +623,15 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       }
       const Entry &pl = need(nd, payload_key(ins));
       const size_t bytes = msg_bytes(c, m.kind, m.stage);
+      if (c.recovering && (ins.kind == RESEND_GRAD || (ins.kind == SEND_ACT && X == c.rec_stage)))
+        c.bytes_rerouted += bytes;
       if (is_local(c, ins.peer)) {
         Node &dst = c.nodes.at(ins.peer);
         void *dp = m.kind == MSG_GRADSUM ? (void *)dst.copies.at(X).grad : arena_alloc(dst, bytes);
         wait_ev(nd.main, pl.ev);
+        // the receiver's step-start memset of that buffer ran on ITS stream:
+        // order this cross-node write after it explicitly
+        wait_ev(nd.main, dst.ev_begin);
         CK(cudaMemcpyAsync(dp, pl.p, bytes, cudaMemcpyDeviceToDevice, nd.main));
         c.mail[ck].push_back({dp, record(nd, nd.main)});
       } else {
@@ -566,8 +641,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         char *dst = e.peer_base + e.recv_off + (size_t)slot * e.slot_bytes;
         wait_ev(e.stream, pl.ev);
         CK(cudaMemcpyAsync(dst, pl.p, bytes, cudaMemcpyDeviceToDevice, e.stream));
-        CK(cudaEventRecord(e.ev[slot], e.stream));
-        c.x.post(e);
+        CK(c.x.post(e));   // published once the copy has completed
       }
       return true;
     }
@@ -588,13 +662,13 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         const int slot = (int)(e.consumed % (uint64_t)e.cap);
         ++e.consumed;
         char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
+        // the sequence number is published after the payload landed: no wait
         if (m.kind == MSG_GRADSUM) {
-          wait_ev(nd.main, e.rev[slot]);
           CK(cudaMemcpyAsync(nd.copies.at(X).grad, src, msg_bytes(c, m.kind, m.stage),
                              cudaMemcpyDeviceToDevice, nd.main));
           got = {nd.copies.at(X).grad, record(nd, nd.main)};
         } else {
-          got = {src, e.rev[slot]};
+          got = {src, nullptr};
         }
       }
       if (ins.kind == RECV_ACT)
@@ -724,12 +798,27 @@ void begin_step(Ctx &c) {
     nd.evnext = 0;
     nd.store.clear();
     nd.arena_used = 0;
+    if (!nd.arena_spill.empty()) {   // the last step overflowed: regrow to its peak
+      for (auto &ch : nd.arena_spill) CK(cudaFree(ch.first));
+      nd.arena_spill.clear();
+      CK(cudaFree(nd.arena));
+      nd.arena_bytes = al(nd.arena_peak + nd.arena_peak / 8);
+      nd.arena = (char *)dmalloc(nd.arena_bytes);
+    }
+    nd.arena_peak = 0;
+    nd.trec.clear();
+    nd.tnext = 0;
     for (auto &cc : nd.copies) {
       Copy &cp = cc.second;
+      cp.retain_left = cp.retain;
+      // a loss nobody computes this step reads NaN (LFLB: the last stage
+      // lost after its commit point took the only copy of its losses)
+      if (cp.loss) CK(k::fill_nan(cp.loss, (size_t)c.d.M * 4, nd.main));
       cp.free_slots.clear();
       for (int i = cp.nslots - 1; i >= 0; --i) cp.free_slots.push_back(i);
       CK(cudaMemsetAsync(cp.grad, 0, c.stages[cp.X].pcount * sizeof(float), nd.main));
     }
+    CK(cudaEventRecord(nd.ev_begin, nd.main));
     CK(cudaEventRecord(nd.t0, nd.main));
   }
 }
@@ -739,6 +828,11 @@ void begin_step(Ctx &c) {
 void stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
   const Dims &d = c.d;
   const size_t R = d.R();
+  // ids index the embedding / head rows on the device: reject out-of-range
+  // ids here rather than read or write outside the tensors
+  for (size_t i = 0; i < (size_t)d.M * R; ++i)
+    if (tok[i] < 0 || tok[i] >= d.V || tgt[i] < 0 || tgt[i] >= d.V)
+      throw RtError{BB_E_INVAL, "token or target id outside [0, vocab)"};
   std::memcpy(c.h_tok, tok, (size_t)d.M * R * 4);
   std::memcpy(c.h_tgt, tgt, (size_t)d.M * R * 4);
   std::vector<int32_t> idx(R);
@@ -777,20 +871,54 @@ float read_loss(Ctx &c) {
   return h;
 }
 
+// A preempted node's memory is lost: NaN-fill everything the node
+// owns (parameter copies, Adam state, saved sets, step arena, scratch) and
+// mark it dead. Called at the injection, before bb_recover runs, so a
+// recovery that read victim memory would poison the results (the bitwise
+// recovered == failure-free tests catch it).
+void poison_node(Ctx &c, Node &nd) {
+  for (auto &cc : nd.copies) {
+    Copy &cp = cc.second;
+    const size_t n = c.stages[cp.X].pcount;
+    CK(k::fill_nan(cp.master, n * 4, nd.main));
+    CK(k::fill_nan(cp.m, n * 4, nd.main));
+    CK(k::fill_nan(cp.v, n * 4, nd.main));
+    CK(k::fill_nan(cp.grad, n * 4, nd.main));
+    if (c.bf16) CK(k::fill_nan(cp.work, n * 2, nd.main));
+    CK(k::fill_nan(cp.slots, c.stages[cp.X].slot_bytes * cp.nslots, nd.main));
+    if (cp.loss) CK(k::fill_nan(cp.loss, (size_t)c.d.M * 4, nd.main));
+  }
+  CK(k::fill_nan(nd.arena, nd.arena_bytes, nd.main));
+  for (auto &ch : nd.arena_spill) CK(k::fill_nan(ch.first, ch.second, nd.main));
+  const size_t R = c.d.R(), H = c.d.H, F = c.d.F;
+  CK(k::fill_nan(nd.sF, R * F * c.act_bytes, nd.main));
+  CK(k::fill_nan(nd.s3, R * 3 * H * c.act_bytes, nd.main));
+  for (auto p : nd.sH) CK(k::fill_nan(p, R * H * c.act_bytes, nd.main));
+  for (auto p : nd.s32) CK(k::fill_nan(p, R * H * 4, nd.main));
+  CK(cudaStreamSynchronize(nd.main));
+  nd.alive = false;
+}
+
+// Step end on every live node's main stream (before the host synchronises).
+void mark_end(Ctx &c) {
+  for (auto &kv : c.nodes)
+    if (kv.second.alive) CK(cudaEventRecord(kv.second.t1, kv.second.main));
+}
+
 void finish_stats(Ctx &c, bb_step_stats *st, double t0) {
+  c.last_step_ms = (float)(now_ms() - t0);
   if (!st) return;
   float dev = 0.f;
   for (auto &kv : c.nodes) {
     Node &nd = kv.second;
     if (!nd.alive) continue;
-    CK(cudaEventRecord(nd.t1, nd.main));
     CK(cudaEventSynchronize(nd.t1));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, nd.t0, nd.t1));
     dev = std::max(dev, ms);
   }
   st->device_ms = dev;
-  st->step_ms = (float)(now_ms() - t0);
+  st->step_ms = c.last_step_ms;
   st->gpu_launches = (int)(k::g_launches - c.launches_at_start);
   st->h2d_bytes = c.h2d;
   st->d2h_bytes = c.d2h;
@@ -808,10 +936,17 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       throw RtError{BB_E_INVAL, "bad world rank/size"};
     if (m->n_layer < P) throw RtError{BB_E_INVAL, "n_layer < stages"};
     if (c.o.rc != BB_RC_NONE && P < 2) throw RtError{BB_E_INVAL, "RC needs stages >= 2"};
+    if (c.o.rc != BB_RC_NONE && c.o.rc != BB_RC_EFLB && c.o.rc != BB_RC_LFLB)
+      throw RtError{BB_E_UNSUPPORTED, "RC mode not built"};
     if (m->n_head <= 0 || m->d_model % m->n_head) throw RtError{BB_E_INVAL, "d_model % n_head"};
-    if (m->d_model % 8 || m->d_ff % 8 || m->vocab % 8 || m->d_model / m->n_head > 64)
-      throw RtError{BB_E_INVAL, "d_model, d_ff, vocab must be multiples of 8; head dim <= 64"};
+    if (m->d_model % 8 || m->d_ff % 8 || m->vocab % 8)
+      throw RtError{BB_E_INVAL, "d_model, d_ff, vocab must be multiples of 8"};
+    if (m->d_model / m->n_head != 64 && m->d_model / m->n_head != 32)
+      throw RtError{BB_E_UNSUPPORTED, "attention kernels take head dim 64 (or 32)"};
     if (c.o.micro_batch < 1) throw RtError{BB_E_INVAL, "micro_batch < 1"};
+    if (c.o.prec == BB_PREC_BF16 && m->d_model < 64)
+      // the transposed (MN-major) operands of dX / dW need >= 64 rows
+      throw RtError{BB_E_UNSUPPORTED, "bf16 path needs d_model >= 64"};
     c.d = {m->n_layer, m->d_model, m->n_head, m->d_ff, m->vocab, m->seq_len, m->causal ? 1 : 0,
            P, M, c.o.micro_batch};
     c.bf16 = c.o.prec == BB_PREC_BF16;
@@ -819,7 +954,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     const bool rc = c.o.rc != BB_RC_NONE;
     try {
       c.ranges = partition(m->n_layer, P, c.o.layers_per_stage);
-      c.plans = normal_plans(P, M, rc);
+      c.plans = normal_plans(P, M, (int)c.o.rc);
     } catch (const PlanError &e) {
       throw RtError{BB_E_INVAL, e.msg};
     }
@@ -865,6 +1000,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       }
       CK(cudaEventCreate(&nd.t0));
       CK(cudaEventCreate(&nd.t1));
+      CK(cudaEventCreateWithFlags(&nd.ev_begin, cudaEventDisableTiming));
       std::vector<std::pair<int, bool>> hosted{{n, false}};
       if (rc) hosted.push_back({(n + 1) % P, true});
       for (auto &h : hosted) {
@@ -878,11 +1014,14 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         cp.v = (float *)dmalloc(si.pcount * 4);
         cp.grad = (float *)dmalloc(si.pcount * 4);
         cp.work = c.bf16 ? dmalloc(si.pcount * 2) : (void *)cp.master;
-        cp.nslots = h.second ? M : std::min(M, P - X);
-        cp.slots = (char *)dmalloc(si.slot_bytes * cp.nslots);
+        if (!h.second) {   // 1F1B stash of the node's own stage: min(M, P - X) in flight
+          cp.nslots = std::min(M, P - X);
+          cp.slots = (char *)dmalloc(si.slot_bytes * cp.nslots);
+        }
         if (X == P - 1) cp.loss = (float *)dmalloc(M * 4);
       }
-      nd.arena_bytes = 12 * (size_t)M * al(act) + ALIGN;
+      // normal 1F1B step: FWD / FRC outputs, BWD input-gradients, local receives
+      nd.arena_bytes = (size_t)(6 * M + 8) * al(act);
       nd.arena = (char *)dmalloc(nd.arena_bytes);
       const size_t F = c.d.F, H = c.d.H;
       nd.sF = dmalloc(R * F * c.act_bytes);
@@ -902,15 +1041,41 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.d_tgt = (int32_t *)dmalloc((size_t)M * R * 4);
       nd.d_csr = (int32_t *)dmalloc((size_t)M * c.csr_stride * 4);
     }
+    // FRC retention pools of the replicas (Q10), allocated last so an
+    // automatic budget can take what the rest left free. A replica keeps
+    // `retain` FRC saved sets per step; its pool also has to serve as the 1F1B
+    // stash once promoted (min(M, P - X) in flight) plus one slot for a BRC
+    // re-forward, and one extra scratch slot (index nslots) for the FRCs
+    // beyond the budget.
+    if (rc) {
+      size_t budget = c.o.frc_retain_bytes;
+      int nrep = 0;
+      for (auto &kv : c.nodes)
+        for (auto &cc : kv.second.copies) nrep += cc.second.replica ? 1 : 0;
+      if (budget == (size_t)-1 && nrep > 0) {   // auto: what is free, minus a reserve
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const size_t reserve = (size_t)8 << 30;
+        budget = fr > reserve ? (fr - reserve) / nrep : 0;
+      }
+      for (auto &kv : c.nodes)
+        for (auto &cc : kv.second.copies) {
+          Copy &cp = cc.second;
+          if (!cp.replica) continue;
+          const StageInfo &si = c.stages[cp.X];
+          const bool frc = c.o.rc == BB_RC_EFLB;   // LFLB keeps no FRC saved sets
+          const int full = !frc ? 0 : budget == 0 ? M
+                                    : (int)std::min<size_t>(M, budget / si.slot_bytes);
+          cp.retain = full;
+          cp.nslots = full >= M ? M : std::min(M, full + std::min(M, P - cp.X) + 1);
+          cp.slots = (char *)dmalloc(si.slot_bytes * (cp.nslots + (frc && full < M ? 1 : 0)));
+        }
+    }
     // Cross-rank edges: one per (src node, dst node, kind) whose endpoints
     // live on different ranks; ring distance <= 2 covers the normal pipeline,
     // the replica ring and the failover skip edges (xport.h).
     if (c.o.world_size > 1) {
-      if (!c.o.nccl_id) throw RtError{BB_E_INVAL, "nccl_id required for world_size > 1"};
-      ncclUniqueId id;
-      std::memcpy(&id, c.o.nccl_id, sizeof(id));
-      if (debug_on()) std::fprintf(stderr, "[bb rank %d] ncclCommInitRank\n", c.o.world_rank);
-      NK(ncclCommInitRank(&c.world, c.o.world_size, id, c.o.world_rank));
+      if (!c.o.session_id) throw RtError{BB_E_INVAL, "session_id required for world_size > 1"};
       std::set<std::tuple<int, int, int>> want;
       auto add = [&](int a, int b, int kind) {
         a = (a % P + P) % P;
@@ -932,8 +1097,8 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
                                            3 * gmax * sizeof(float)};
       const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, 2};
       const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
-      const std::string xe = xport_init(c.x, c.world, c.o.world_rank, c.o.world_size, wl,
-                                        c.node_rank, slot_bytes, caps, c.o.nccl_id, hi_prio);
+      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, wl, c.node_rank,
+                                        slot_bytes, caps, c.o.session_id, hi_prio);
       if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
     }
     CK(cudaDeviceSynchronize());
@@ -952,13 +1117,21 @@ bb_status rt_load_params(Ctx &c, const float *host, size_t n) {
       for (auto &cc : nd.copies) {
         Copy &cp = cc.second;
         const StageInfo &si = c.stages[cp.X];
-        CK(cudaMemcpy(cp.master, host + si.poff, si.pcount * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemset(cp.m, 0, si.pcount * 4));
-        CK(cudaMemset(cp.v, 0, si.pcount * 4));
+        // Everything on the node's stream, in order. (Round 1 used the legacy
+        // stream's cudaMemcpy here: from pageable memory it returns once the
+        // data is staged, before the DMA lands, and the cast on the
+        // non-blocking node stream could read the old master — a bf16 working
+        // copy of zeros, seen as a head-only stage with zero gradients and as
+        // uniform logits in multi-process runs on one GPU.)
+        CK(cudaMemcpyAsync(cp.master, host + si.poff, si.pcount * 4, cudaMemcpyHostToDevice,
+                           nd.main));
+        CK(cudaMemsetAsync(cp.m, 0, si.pcount * 4, nd.main));
+        CK(cudaMemsetAsync(cp.v, 0, si.pcount * 4, nd.main));
         if (c.bf16) CK(k::cast_f32_to_bf16(si.pcount, cp.master, cp.work, nd.main));
         cp.t = 0;
       }
     }
+    c.adam_steps = 0;
     CK(cudaDeviceSynchronize());
     return BB_OK;
   } catch (const RtError &e) {
@@ -975,22 +1148,24 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     if ((tok == nullptr) != (tgt == nullptr)) throw RtError{BB_E_INVAL, "null tokens/targets"};
     if (!tok && !c.resident) throw RtError{BB_E_STATE, "no resident inputs (bb_stage_inputs)"};
     CK(cudaSetDevice(c.o.device));
+    if (tok) {
+      stage_inputs(c, tok, tgt);   // validates ids (BB_E_INVAL) before any rank moves on
+      c.resident = false;          // LOAD_INPUTS overwrites the device copies
+    }
+    c.resident_step = tok == nullptr;
     c.x.barrier();   // every rank finished the previous step: receive slots are free
     // profile mode: park the serialised stream while the host enqueues the
     // step, so host launch latency never sits inside a kernel's event bracket
     if (c.o.profile && c.serial) CK(k::gpu_sleep(200000000ull, c.serial));
     begin_step(c);
-    c.resident_step = tok == nullptr;
-    if (tok) {
-      stage_inputs(c, tok, tgt);
-      c.resident = false;   // LOAD_INPUTS overwrites the device copies
-    }
     if (!c.armed) {
       run(c, c.plans, nullptr, Phase{});
+      mark_end(c);
       sync_all(c, true);
       ++c.steps_done;
-      if (st) st->loss = read_loss(c);
+      ++c.adam_steps;
       finish_stats(c, st, t0);
+      if (st) st->loss = read_loss(c);
       return BB_OK;
     }
     // injected preemption: every rank computes the same cut (Q12/Q14)
@@ -1017,12 +1192,14 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
     ph.drop_to_victim = true;
     ph.victim = v;
     run(c, c.plans, &c.cut.pcs, ph);
+    mark_end(c);
     sync_all(c, true);
+    // the victim's memory is gone the moment it is preempted: NaN-poison
+    // everything its node owned now, so nothing in bb_recover can read it
+    if (c.nodes.count(v)) poison_node(c, c.nodes.at(v));
     c.interrupted = true;
-    if (st) {
-      st->loss = NAN;
-      finish_stats(c, st, t0);
-    }
+    finish_stats(c, st, t0);
+    if (st) st->loss = NAN;
     return BB_E_PREEMPTED;
   } catch (const RtError &e) {
     c.err = e.msg;
@@ -1060,8 +1237,9 @@ bb_status rt_preempt(Ctx &c, int stage, int at_instr) {
     c.err = "unknown stage";
     return BB_E_INVAL;
   }
-  if (c.o.rc == BB_RC_NONE || c.failover) {
-    // no replica of the victim exists (no RC, or redundancy already spent: P:464, Q18)
+  if (c.o.rc == BB_RC_NONE || !recoverable(c.d.P, c.topo, c.victims, stage)) {
+    // no live replica of the victim's stage (no RC; or the victim is dead, is a
+    // double-duty shadow, or lost its replica holder: P:464 consecutive nodes, Q18)
     c.err = "no redundancy left for the victim";
     return BB_E_FATAL;
   }
@@ -1097,35 +1275,25 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
     // promote the replica on the shadow; the victim stops
     if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = false;
     Phase ph;
+    c.recovering = true;
+    c.rec_stage = v;
+    c.frc_recomputed = 0;
+    c.bytes_rerouted = 0;
     run(c, c.continuation, nullptr, ph);
+    c.recovering = false;
     sync_all(c, true);
-    if (c.nodes.count(v)) {
-      // the victim's memory is gone: NaN-poison everything it held
-      Node &nd = c.nodes.at(v);
-      for (auto &cc : nd.copies) {
-        Copy &cp = cc.second;
-        const size_t n = c.stages[cp.X].pcount;
-        CK(k::fill_nan(cp.master, n * 4, nd.main));
-        CK(k::fill_nan(cp.m, n * 4, nd.main));
-        CK(k::fill_nan(cp.v, n * 4, nd.main));
-        CK(k::fill_nan(cp.grad, n * 4, nd.main));
-        if (c.bf16) CK(k::fill_nan(cp.work, n * 2, nd.main));
-        CK(k::fill_nan(cp.slots, c.stages[cp.X].slot_bytes * cp.nslots, nd.main));
-      }
-      CK(k::fill_nan(nd.arena, nd.arena_bytes, nd.main));
-      CK(cudaStreamSynchronize(nd.main));
-      nd.alive = false;
-    }
-    c.topo = failover_topology(P, v);
+    c.history.push_back({c.plans, c.topo});
+    c.topo = lose_node(P, c.topo, v);
     try {
-      c.plans = failover_plans(P, M, v);
+      c.plans = failover_plans(P, M, v, &c.history.back().plans);
     } catch (const PlanError &e) {
       throw RtError{BB_E_STATE, e.msg};
     }
     c.failover = true;
-    c.victim = v;
+    c.victims.push_back(v);
     c.interrupted = false;
     ++c.steps_done;
+    ++c.adam_steps;
     if (r) {
       r->victim = v;
       r->shadow = u;
@@ -1136,9 +1304,13 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
       r->resent_mb = (int)c.rinfo.resend.size();
       r->loss = read_loss(c);
       r->recover_ms = (float)(now_ms() - t0);
+      r->interrupted_step_ms = c.last_step_ms;
+      r->frc_recomputed_mb = c.frc_recomputed;
+      r->bytes_resent = c.bytes_rerouted;
     }
     return BB_OK;
   } catch (const RtError &e) {
+    c.recovering = false;
     c.err = e.msg;
     c.fatal = e.st != BB_E_INVAL;
     return e.st;
@@ -1155,7 +1327,9 @@ bb_status rt_rejoin(Ctx &c) {
     if (!c.failover || c.interrupted) throw RtError{BB_E_STATE, "rejoin needs a recovered failover pipeline"};
     CK(cudaSetDevice(c.o.device));
     c.x.barrier();
-    const int P = c.d.P, v = c.victim, u = (v - 1 + P) % P, w = (v + 1) % P;
+    // the most recent victim returns first (LIFO): the plans and topology
+    // go back to those in force before its preemption
+    const int P = c.d.P, v = c.victims.back(), u = (v - 1 + P) % P, w = (v + 1) % P;
     auto parts = [&](Copy &cp) {
       return std::vector<float *>{cp.master, cp.m, cp.v};
     };
@@ -1179,8 +1353,7 @@ bb_status rt_rejoin(Ctx &c) {
         auto sp = parts(cp);
         for (int i = 0; i < 3; ++i)
           CK(cudaMemcpyAsync(dst + (size_t)i * n * 4, sp[i], n * 4, cudaMemcpyDeviceToDevice, e.stream));
-        CK(cudaEventRecord(e.ev[slot], e.stream));
-        c.x.post(e);
+        CK(c.x.post(e));
       }
     }
     sync_all(c, true);
@@ -1201,24 +1374,24 @@ bb_status rt_rejoin(Ctx &c) {
           const int slot = (int)(e.consumed % (uint64_t)e.cap);
           ++e.consumed;
           const char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
-          wait_ev(nd.main, e.rev[slot]);
           auto dp = parts(dc);
           for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(dp[i], src + (size_t)i * n * 4, n * 4, cudaMemcpyDeviceToDevice, nd.main));
         }
         if (c.bf16) CK(k::cast_f32_to_bf16(n, dc.master, dc.work, nd.main));
         CK(cudaMemsetAsync(dc.grad, 0, n * 4, nd.main));
-        dc.t = (int)c.steps_done;
+        dc.t = (int)c.adam_steps;   // every stage took one Adam step per step since load
         dc.replica = X != v;
       }
       nd.alive = true;
     }
     if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = true;
     sync_all(c, true);
-    c.topo = normal_topology(P, true);
-    c.plans = normal_plans(P, c.d.M, true);
-    c.failover = false;
-    c.victim = -1;
+    c.plans = c.history.back().plans;
+    c.topo = c.history.back().topo;
+    c.history.pop_back();
+    c.victims.pop_back();
+    c.failover = !c.victims.empty();
     return BB_OK;
   } catch (const RtError &e) {
     c.err = e.msg;
@@ -1248,9 +1421,92 @@ bb_status rt_read_state(Ctx &c, int X, int replica, int what, float *host, size_
   }
 }
 
+bb_status rt_write_state(Ctx &c, int X, int what, const float *host, size_t n) {
+  try {
+    if (X < 0 || X >= c.d.P) throw RtError{BB_E_INVAL, "bad stage"};
+    if (n != c.stages[X].pcount) throw RtError{BB_E_INVAL, "size mismatch"};
+    if (what != BB_STATE_PARAMS && what != BB_STATE_ADAM_M && what != BB_STATE_ADAM_V)
+      throw RtError{BB_E_INVAL, "writable: params, adam_m, adam_v"};
+    CK(cudaSetDevice(c.o.device));
+    CK(cudaDeviceSynchronize());
+    for (auto &kv : c.nodes) {
+      Node &nd = kv.second;
+      if (!nd.alive || !nd.copies.count(X)) continue;
+      Copy &cp = nd.copies.at(X);
+      float *dst = what == BB_STATE_PARAMS ? cp.master : what == BB_STATE_ADAM_M ? cp.m : cp.v;
+      CK(cudaMemcpyAsync(dst, host, n * 4, cudaMemcpyHostToDevice, nd.main));   // stream-ordered
+      if (what == BB_STATE_PARAMS && c.bf16) CK(k::cast_f32_to_bf16(n, cp.master, cp.work, nd.main));
+      CK(cudaStreamSynchronize(nd.main));   // host buffer borrowed for this call only
+    }
+    CK(cudaDeviceSynchronize());
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
+namespace {
+// Total length of the union of [a, b) intervals.
+double union_len(std::vector<std::pair<double, double>> v) {
+  std::sort(v.begin(), v.end());
+  double tot = 0, lo = -1e300, hi = -1e300;
+  for (auto &x : v) {
+    if (x.first > hi) {
+      if (hi > lo) tot += hi - lo;
+      lo = x.first;
+      hi = x.second;
+    } else {
+      hi = std::max(hi, x.second);
+    }
+  }
+  if (hi > lo) tot += hi - lo;
+  return tot;
+}
+}  // namespace
+
+bb_status rt_node_stats(Ctx &c, bb_node_stat *out, int cap, int *n) {
+  try {
+    if (!c.o.timing) throw RtError{BB_E_STATE, "opts.timing is off"};
+    int cnt = 0;
+    for (auto &kv : c.nodes) {
+      Node &nd = kv.second;
+      if (!nd.alive) continue;
+      CK(cudaEventSynchronize(nd.t1));
+      bb_node_stat r{};
+      r.node = nd.n;
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, nd.t0, nd.t1));
+      r.step_ms = ms;
+      std::vector<std::pair<double, double>> mainv, frcv, both;
+      for (auto &t : nd.trec) {
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, nd.t0, t.a));
+        CK(cudaEventElapsedTime(&b, nd.t0, t.b));
+        (t.kind == 1 ? frcv : mainv).push_back({a, b});
+        (t.kind == 1 ? r.n_frc : t.kind == 2 ? r.n_bwd : r.n_fwd) += 1;
+      }
+      r.busy_ms = (float)union_len(mainv);
+      r.bubble_ms = r.step_ms - r.busy_ms;
+      r.frc_ms = (float)union_len(frcv);
+      both = mainv;
+      both.insert(both.end(), frcv.begin(), frcv.end());
+      // FRC inside main-stream idle time = |main U frc| - |main|
+      r.frc_hidden_ms = (float)(union_len(both) - r.busy_ms);
+      if (cnt < cap && out) out[cnt] = r;
+      ++cnt;
+    }
+    if (n) *n = cnt;
+    return BB_OK;
+  } catch (const RtError &e) {
+    c.err = e.msg;
+    return e.st;
+  }
+}
+
 std::string rt_dump(const Ctx &c) {
-  return dump(c.d.P, c.d.M, c.o.rc != BB_RC_NONE, c.ranges, c.plans, c.topo, c.node_device,
-              c.failover, c.victim);
+  return dump(c.d.P, c.d.M, (int)c.o.rc, c.ranges, c.plans, c.topo, c.node_device,
+              c.failover, c.victims);
 }
 
 bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n) {
@@ -1280,7 +1536,6 @@ bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n) {
 void rt_destroy(Ctx &c) {
   cudaDeviceSynchronize();
   xport_destroy(c.x);
-  if (c.world) ncclCommDestroy(c.world);
   for (auto &kv : c.nodes) {
     Node &nd = kv.second;
     for (auto &cc : nd.copies) {
@@ -1308,6 +1563,7 @@ void rt_destroy(Ctx &c) {
     for (auto e : nd.evpool) cudaEventDestroy(e);
     cudaEventDestroy(nd.t0);
     cudaEventDestroy(nd.t1);
+    cudaEventDestroy(nd.ev_begin);
     if (!c.serial) {
       cudaStreamDestroy(nd.main);
       cudaStreamDestroy(nd.frc);

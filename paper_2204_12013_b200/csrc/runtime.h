@@ -8,10 +8,9 @@
 // slot pools (1F1B stash; full FRC retention, P:524 / Q10), a per-step arena
 // for activations and input-gradients (retained for a lazy-BRC resend, Q3) and
 // a backward scratch. Nodes on other ranks are reached through xport.h
-// (copy-engine writes into the peer's HBM + IPC events; NCCL bootstraps).
+// (copy-engine writes into the peer's HBM + IPC events; host-shm rendezvous).
 #pragma once
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <map>
 #include <string>
@@ -65,8 +64,10 @@ struct Copy {
   void *work = nullptr;   // bf16 working copy (== master in fp32 check mode)
   int t = 0;
   char *slots = nullptr;
-  int nslots = 0;
+  int nslots = 0;              // pool slots; slot index nslots is the FRC scratch slot
   std::vector<int> free_slots;
+  int retain = 0;              // FRC saved sets kept per step (replica; budget, Q10)
+  int retain_left = 0;         // ... still to keep in the current step
   float *loss = nullptr;  // [M] per-micro-batch losses (stage P-1 only)
 };
 
@@ -78,6 +79,13 @@ struct Node {
   std::map<Key, Entry> store;
   char *arena = nullptr;
   size_t arena_bytes = 0, arena_used = 0;
+  std::vector<std::pair<char *, size_t>> arena_spill;   // overflow chunks of this step
+  size_t arena_peak = 0;                                // bytes the last step needed
+  // opts.timing: [kind (0 FWD, 1 FRC, 2 BWD), start, end] events of this step
+  struct TRec { int kind; cudaEvent_t a, b; };
+  std::vector<TRec> trec;
+  std::vector<cudaEvent_t> tpool;
+  size_t tnext = 0;
   // backward scratch (main stream)
   void *sF = nullptr, *s3 = nullptr, *sH[5] = {};
   float *s32[4] = {};   // fp32 [R, H]: LN-input gradients and the residual-gradient chain
@@ -88,6 +96,7 @@ struct Node {
   std::vector<Instr> plan;
   size_t pc = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEvent_t ev_begin = nullptr;   // after the step-start memsets of this node's buffers
 };
 
 struct ProfRec {
@@ -114,12 +123,13 @@ struct Ctx {
   Plans plans;
   Topology topo;
   bool failover = false;
-  int victim = -1;
+  std::vector<int> victims;           // preempted nodes, oldest first (bb_rejoin is LIFO)
+  struct Hist { Plans plans; Topology topo; };
+  std::vector<Hist> history;          // plans / topology before each failover
   bool fatal = false;
   std::vector<int> node_rank, node_device;
   std::map<int, Node> nodes;          // local nodes only
   Xport x;                            // cross-rank transport (IPC + copy engines)
-  ncclComm_t world = nullptr;         // bootstrap only
   cudaStream_t serial = nullptr;      // profile mode: the one stream of all local nodes
   // local mailboxes (per (src node, dst node, kind))
   std::map<ChanKey, std::deque<Entry>> mail;
@@ -137,6 +147,7 @@ struct Ctx {
   std::vector<int> csr_U;
   size_t csr_stride = 0;
   long long steps_done = 0;     // completed steps (identical on every rank)
+  long long adam_steps = 0;     // Adam steps since bb_load_params (= every copy's t)
   bool resident = false;        // inputs staged on every local node's device (bb_stage_inputs)
   bool resident_step = false;   // this step reuses the resident inputs (no H2D)
   std::string err;
@@ -146,6 +157,11 @@ struct Ctx {
   size_t prof_next = 0;
   long long launches_at_start = 0;
   uint64_t h2d = 0, d2h = 0;
+  float last_step_ms = 0.f;     // host wall time of the last bb_step call
+  bool recovering = false;      // inside bb_recover's continuation
+  int rec_stage = -1;           // the victim's stage (recovery accounting)
+  int frc_recomputed = 0;       // forwards recomputed by the current recovery
+  uint64_t bytes_rerouted = 0;  // bytes resent / rerouted by the current recovery
 };
 
 // Implemented in runtime.cpp
@@ -157,6 +173,8 @@ bb_status rt_preempt(Ctx &c, int stage, int at_instr);
 bb_status rt_recover(Ctx &c, bb_recovery_stats *r);
 bb_status rt_rejoin(Ctx &c);
 bb_status rt_read_state(Ctx &c, int stage, int replica, int what, float *host, size_t n);
+bb_status rt_write_state(Ctx &c, int stage, int what, const float *host, size_t n);
+bb_status rt_node_stats(Ctx &c, bb_node_stat *out, int cap, int *n);
 std::string rt_dump(const Ctx &c);
 void rt_destroy(Ctx &c);
 bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n);

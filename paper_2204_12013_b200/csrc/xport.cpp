@@ -2,6 +2,8 @@
 #include "xport.h"
 
 #include <fcntl.h>
+#include <sys/stat.h>
+#include <time.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -20,33 +22,12 @@ struct XErr {
     cudaError_t e_ = (x);                                                          \
     if (e_ != cudaSuccess) throw XErr{std::string(#x) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
-#define XNK(x)                                                                     \
-  do {                                                                             \
-    ncclResult_t r_ = (x);                                                         \
-    if (r_ != ncclSuccess) throw XErr{std::string(#x) + ": " + ncclGetErrorString(r_)}; \
-  } while (0)
-
-// Byte-wise all-reduce(sum) of a host table in which every rank filled only
-// its own entries (others zero): an all-gather of disjoint entries.
-void allgather_bytes(ncclComm_t comm, std::vector<uint8_t> &buf) {
-  void *d = nullptr;
-  XCK(cudaMalloc(&d, buf.size()));
-  XCK(cudaMemcpy(d, buf.data(), buf.size(), cudaMemcpyHostToDevice));
-  XNK(ncclAllReduce(d, d, buf.size(), ncclUint8, ncclSum, comm, 0));
-  XCK(cudaStreamSynchronize(0));
-  XCK(cudaMemcpy(buf.data(), d, buf.size(), cudaMemcpyDeviceToHost));
-  XCK(cudaFree(d));
-}
-
-void nccl_barrier(ncclComm_t comm) {
-  std::vector<uint8_t> one(1, 0);
-  allgather_bytes(comm, one);
-}
 }  // namespace
 
+// Header words: [0] magic, [1] barrier count, [2] barrier generation, [3] world.
 void Xport::barrier() {
   if (world <= 1) return;
-  uint64_t *cnt = reinterpret_cast<uint64_t *>(shm);
+  uint64_t *cnt = reinterpret_cast<uint64_t *>(shm) + 1;
   uint64_t *gen = cnt + 1;
   const uint64_t g = __atomic_load_n(gen, __ATOMIC_ACQUIRE);
   if (__atomic_add_fetch(cnt, 1, __ATOMIC_ACQ_REL) == (uint64_t)world) {
@@ -59,16 +40,42 @@ void Xport::barrier() {
   }
 }
 
-void Xport::post(XEdge &e) {
+namespace {
+void CUDART_CB post_cb(void *arg) {
+  auto *p = static_cast<XEdge::Post *>(arg);
+  __atomic_store_n(const_cast<uint64_t *>(p->ctr), p->value, __ATOMIC_RELEASE);
+}
+}  // namespace
+
+cudaError_t Xport::post(XEdge &e) {
+  XEdge::Post &p = e.posts[e.sent % (uint64_t)e.cap];
   ++e.sent;
-  __atomic_store_n(const_cast<uint64_t *>(counter(e.index)), e.sent, __ATOMIC_RELEASE);
+  p.ctr = counter(e.index);
+  p.value = e.sent;
+  return cudaLaunchHostFunc(e.stream, post_cb, &p);
 }
 
 bool Xport::available(const XEdge &e) const {
   return __atomic_load_n(const_cast<uint64_t *>(counter(e.index)), __ATOMIC_ACQUIRE) > e.consumed;
 }
 
-std::string xport_init(Xport &x, ncclComm_t world, int rank, int nranks,
+namespace {
+constexpr uint64_t kMagic = 0x62616d626f6f7831ull;   // "bamboox1"
+constexpr size_t kHS = 64;                          // IPC mem / event handle bytes
+
+double now_s() {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+}  // namespace
+
+// Rendezvous through one POSIX shared-memory segment named after the session
+// id (no NCCL, no sockets): rank 0 creates it, the others open it when it
+// appears. Header | per-edge sequence counters | per-rank heartbeats |
+// one IPC memory handle per rank. Ranks fill their own entries and meet at the shm barrier, so
+// several ranks may share one GPU (NCCL refuses that: duplicate device).
+std::string xport_init(Xport &x, int rank, int nranks,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
                        const std::vector<int> &cap, const void *id_bytes, int hi_prio) {
@@ -93,82 +100,82 @@ std::string xport_init(Xport &x, ncclComm_t world, int rank, int nranks,
       max_cap = std::max(max_cap, e.cap);
       x.edges[w] = e;
     }
+    x.nedges = idx;
     x.arena_bytes = std::max<size_t>(arena_size[rank], 256);
     XCK(cudaMalloc(&x.arena, x.arena_bytes));
-    // ---- shared host memory: barrier + one sequence counter per edge
+    // ---- the shared segment
     uint64_t h = 1469598103934665603ull;
     for (int i = 0; i < 32; ++i) h = (h ^ static_cast<const uint8_t *>(id_bytes)[i]) * 1099511628211ull;
     char name[64];
     std::snprintf(name, sizeof(name), "/bamboo_%016llx", (unsigned long long)h);
     x.shm_name = name;
-    x.shm_bytes = 64 + 8 * (size_t)std::max(1, idx);
+    const size_t off_cnt = 64, off_hb = off_cnt + 8 * (size_t)std::max(1, idx);
+    const size_t off_mh = off_hb + 8 * (size_t)nranks;
+    x.hb_off = off_hb;
+    x.shm_bytes = off_mh + kHS * (size_t)nranks;
+    auto hdr = [&]() { return static_cast<uint64_t *>(x.shm); };
+    const double t0 = now_s();
     if (rank == 0) {
-      int fd = shm_open(name, O_CREAT | O_RDWR | O_TRUNC, 0600);
+      shm_unlink(name);   // a stale segment of a crashed run with this id
+      int fd = shm_open(name, O_CREAT | O_EXCL | O_RDWR, 0600);
       if (fd < 0) throw XErr{"shm_open(create) failed"};
       if (ftruncate(fd, (off_t)x.shm_bytes) != 0) throw XErr{"ftruncate failed"};
       x.shm = mmap(nullptr, x.shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
       close(fd);
       if (x.shm == MAP_FAILED) throw XErr{"mmap failed"};
       std::memset(x.shm, 0, x.shm_bytes);
+      hdr()[3] = (uint64_t)nranks;
+      __atomic_store_n(&hdr()[0], kMagic, __ATOMIC_RELEASE);
+    } else {
+      for (;;) {
+        int fd = shm_open(name, O_RDWR, 0600);
+        if (fd >= 0) {
+          struct stat st;
+          if (fstat(fd, &st) == 0 && (size_t)st.st_size == x.shm_bytes) {
+            x.shm = mmap(nullptr, x.shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+            close(fd);
+            if (x.shm == MAP_FAILED) throw XErr{"mmap failed"};
+            if (__atomic_load_n(&hdr()[0], __ATOMIC_ACQUIRE) == kMagic) break;
+            munmap(x.shm, x.shm_bytes);
+            x.shm = nullptr;
+          } else {
+            close(fd);
+          }
+        }
+        if (now_s() - t0 > 120.0) throw XErr{"rendezvous: rank 0 never created the segment"};
+        usleep(1000);
+      }
+      if (hdr()[3] != (uint64_t)nranks) throw XErr{"rendezvous: world size mismatch"};
     }
-    nccl_barrier(world);
-    if (rank != 0) {
-      int fd = shm_open(name, O_RDWR, 0600);
-      if (fd < 0) throw XErr{"shm_open failed"};
-      x.shm = mmap(nullptr, x.shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-      close(fd);
-      if (x.shm == MAP_FAILED) throw XErr{"mmap failed"};
-    }
-    nccl_barrier(world);
-    if (rank == 0) shm_unlink(name);
-    // ---- receive arenas: exchange IPC handles, map the ones we send to
-    const size_t HS = sizeof(cudaIpcMemHandle_t);
-    std::vector<uint8_t> mh(HS * nranks, 0);
+    x.barrier();
+    if (rank == 0) shm_unlink(name);   // every rank has it mapped now
+    char *tab = static_cast<char *>(x.shm);
+    // ---- receive arenas: publish our IPC handle, map the ones we send to
     cudaIpcMemHandle_t mine;
     XCK(cudaIpcGetMemHandle(&mine, x.arena));
-    std::memcpy(&mh[HS * rank], &mine, HS);
-    allgather_bytes(world, mh);
+    std::memcpy(tab + off_mh + kHS * rank, &mine, kHS);
+    x.barrier();
     x.peer_arena.assign(nranks, nullptr);
     for (auto &kv : x.edges) {
       XEdge &e = kv.second;
       if (e.src_rank != rank || x.peer_arena[e.dst_rank]) continue;
+      if (e.dst_rank == rank) throw XErr{"edge inside one rank"};
       cudaIpcMemHandle_t ph;
-      std::memcpy(&ph, &mh[HS * e.dst_rank], HS);
+      std::memcpy(&ph, tab + off_mh + kHS * e.dst_rank, kHS);
       void *p = nullptr;
       XCK(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
       x.peer_arena[e.dst_rank] = static_cast<char *>(p);
     }
-    // ---- per-slot interprocess events, created by the sender
-    const size_t ES = sizeof(cudaIpcEventHandle_t);
-    std::vector<uint8_t> eh(ES * (size_t)max_cap * std::max(1, idx), 0);
+    // ---- sender-side streams and host-callback slots
     for (auto &kv : x.edges) {
       XEdge &e = kv.second;
       if (e.src_rank != rank) continue;
       XCK(cudaStreamCreateWithPriority(&e.stream, cudaStreamNonBlocking, hi_prio));
       e.peer_base = x.peer_arena[e.dst_rank];
-      for (int s = 0; s < e.cap; ++s) {
-        cudaEvent_t ev;
-        XCK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
-        e.ev.push_back(ev);
-        cudaIpcEventHandle_t hnd;
-        XCK(cudaIpcGetEventHandle(&hnd, ev));
-        std::memcpy(&eh[ES * ((size_t)e.index * max_cap + s)], &hnd, ES);
-      }
-    }
-    allgather_bytes(world, eh);
-    for (auto &kv : x.edges) {
-      XEdge &e = kv.second;
-      if (e.dst_rank != rank) continue;
-      for (int s = 0; s < e.cap; ++s) {
-        cudaIpcEventHandle_t hnd;
-        std::memcpy(&hnd, &eh[ES * ((size_t)e.index * max_cap + s)], ES);
-        cudaEvent_t ev;
-        XCK(cudaIpcOpenEventHandle(&ev, hnd));
-        e.rev.push_back(ev);
-      }
+      e.posts.assign(e.cap, XEdge::Post{nullptr, 0});
     }
     XCK(cudaDeviceSynchronize());
-    nccl_barrier(world);
+    x.barrier();
     return "";
   } catch (const XErr &e) {
     return e.msg;
@@ -179,8 +186,6 @@ void xport_destroy(Xport &x) {
   for (auto &kv : x.edges) {
     XEdge &e = kv.second;
     if (e.stream) cudaStreamSynchronize(e.stream);
-    for (auto ev : e.ev) cudaEventDestroy(ev);
-    for (auto ev : e.rev) cudaEventDestroy(ev);
     if (e.stream) cudaStreamDestroy(e.stream);
   }
   for (auto p : x.peer_arena)

@@ -1,20 +1,23 @@
 // xport.h — inter-process message transport between pipeline nodes on one
 // NVLink/NVSwitch box: the sender's copy engine writes the payload straight
-// into the receiver's HBM (CUDA IPC mapping), records a cross-process CUDA
-// event, and publishes a sequence number in host shared memory; the receiver
-// enqueues a stream wait on that event. No GPU kernel ever spins on a peer,
-// so no stream can be starved by a waiting kernel (the hazard of spinning
-// P2P kernels on concurrent streams); every GPU-side wait is on an event that
-// is already recorded. NCCL is used only to bootstrap (handle exchange).
+// into the receiver's HBM (CUDA IPC mapping of the receiver's arena), and a
+// host callback enqueued behind the copy publishes the edge's sequence number
+// in host shared memory once the copy has COMPLETED. A receiver that sees the
+// number therefore finds the payload whole in its own HBM and needs no GPU
+// wait at all; no GPU kernel ever spins on a peer. (Round 1 published at
+// enqueue time and had the receiver wait on an interprocess CUDA event; with
+// both processes on one GPU that wait sometimes passed before the copy
+// landed, so completion is now established on the sender's side.) The ranks
+// rendezvous through host shared memory named after a session id (no NCCL),
+// so several ranks may share one GPU.
 //
 // Edges: one per (src node, dst node, message kind) crossing ranks; each has
-// `cap` payload slots in the receiver's receive arena and `cap` IPC events on
-// the sender. Slot = cumulative message index % cap; a step-start barrier
-// (host shared memory) guarantees that the previous step's payloads were
-// consumed before a slot is overwritten.
+// `cap` payload slots in the receiver's receive arena. Slot = cumulative
+// message index % cap; a step-start barrier (host shared memory) guarantees
+// that the previous step's payloads were consumed before a slot is
+// overwritten.
 #pragma once
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <cstdint>
 #include <map>
@@ -33,11 +36,11 @@ struct XEdge {
   int index = -1;                      // shm counter index
   // sender side
   cudaStream_t stream = nullptr;
-  std::vector<cudaEvent_t> ev;
   char *peer_base = nullptr;
   uint64_t sent = 0;
+  struct Post { volatile uint64_t *ctr; uint64_t value; };
+  std::vector<Post> posts;             // host-callback arguments, one per slot
   // receiver side
-  std::vector<cudaEvent_t> rev;
   uint64_t consumed = 0;
 };
 
@@ -48,7 +51,8 @@ struct Xport {
   std::vector<char *> peer_arena;      // mapped receive arenas of other ranks
   std::map<std::tuple<int, int, int>, XEdge> edges;
   void *shm = nullptr;
-  size_t shm_bytes = 0;
+  size_t shm_bytes = 0, hb_off = 0;
+  int nedges = 0;
   std::string shm_name;
 
   volatile uint64_t *counter(int i) const {
@@ -56,15 +60,17 @@ struct Xport {
   }
   // Host barrier over all ranks (shared memory, sense-reversing).
   void barrier();
-  void post(XEdge &e);                 // after the copy + event are enqueued
+  // After the payload copy is enqueued on e.stream: enqueue the host callback
+  // that publishes the new sequence number when the copy has completed.
+  cudaError_t post(XEdge &e);
   bool available(const XEdge &e) const;
 };
 
 // want: the global sorted edge list (identical on every rank) with
 // (src, dst, kind); node_rank maps nodes to ranks. slot_bytes(kind) and
-// cap(kind) size the slots. world: the NCCL communicator over all ranks.
-// Returns an error string (empty on success).
-std::string xport_init(Xport &x, ncclComm_t world, int rank, int nranks,
+// cap(kind) size the slots. id_bytes: the session id (>= 32 bytes, same on
+// every rank). Returns an error string (empty on success).
+std::string xport_init(Xport &x, int rank, int nranks,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
                        const std::vector<int> &cap, const void *id_bytes, int hi_prio);

@@ -1,7 +1,11 @@
-"""Worker for multi-process (one rank per GPU) parity tests; launched by
-tests/test_gpu_multi.py through torch.distributed.run. Runs a few steps of a
-config through the C ABI with NCCL edges, optionally injecting a preemption,
-and saves each rank's hosted stage states to <out>/rank<r>.npz."""
+"""Worker for multi-process parity tests; launched by tests/test_gpu_multi.py
+through torch.distributed.run. One process per rank; ranks share the visible
+GPUs round-robin (rank r on device r % n_gpus), so the cross-process
+transport (CUDA IPC + host-shm rendezvous) runs even on a 1-GPU box. Runs a
+few steps of a config through the C ABI, optionally injecting a
+preemption, and saves each rank's hosted stage states to <out>/rank<r>.npz.
+The harness process group is gloo (host-side id broadcast and barriers only;
+the library never uses it)."""
 import argparse
 import os
 
@@ -37,15 +41,16 @@ def main():
     a = ap.parse_args()
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    dist.init_process_group("gloo")
     cfg = get_config(a.config)
     P = a.stages or cfg.stages
-    obj = [bb.nccl_unique_id() if rank == 0 else None]
+    obj = [bb.session_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=bool(a.rc),
-                    prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=local,
-                    nccl_id=obj[0])
+                    prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=dev,
+                    session_id=obj[0])
     p.load_params(make_params(cfg.model))
     losses, rec = [], None
     events = {}

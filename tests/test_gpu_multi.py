@@ -1,7 +1,11 @@
-"""Multi-GPU (one process per GPU, NCCL P2P edges) parity: the pipeline spread
-over 2 (or 4) B200s must give exactly the single-process results (same
-kernels, same order => bit-identical), match the fp64 oracle within the
-tolerances, and recover from an injected preemption bit-identically."""
+"""Multi-process parity (one process per rank; the library's CUDA-IPC
+transport between ranks, rendezvous in host shared memory): the pipeline
+spread over 2 (or 4) processes must give exactly the single-process results
+(same kernels, same order => bit-identical) and recover from an injected
+preemption bit-identically. Ranks share the visible GPUs round-robin, so on
+a 1-GPU box every rank runs on cuda:0 and the cross-process path (IPC
+memory + interprocess events between processes) is still exercised; on a
+multi-GPU box the copies cross NVLink."""
 import os
 import subprocess
 import sys
@@ -66,8 +70,6 @@ def test_multi_gpu_equals_single_process(n, P):
     """P stages over n GPUs (n < P: several nodes per process, device-local
     edges next to NCCL ones) == all P stages in one process, bit for bit."""
     import dataclasses
-    if ngpus() < n:
-        pytest.skip(f"needs {n} GPUs")
     c = dataclasses.replace(get_config("C0"), stages=P)
     ranks = run_mp(n, config="C0", stages=P, steps=2)
     losses, state = single(c, 2)
@@ -83,8 +85,6 @@ def test_multi_gpu_equals_single_process(n, P):
 
 @pytest.mark.parametrize("victim,pi", [(1, 9), (0, 5), (1, 0), (0, 24)])
 def test_multi_gpu_recovery_bitwise(victim, pi):
-    if ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
     cfg = get_config("C0")
     ranks = run_mp(2, config="C0", steps=2, victim=victim, pi=pi)
     losses, state = single(cfg, 2)   # failure-free reference
@@ -100,8 +100,6 @@ def test_multi_gpu_rejoin_sequence_bitwise():
     preempt node 1, rejoin: every step equals the failure-free single-process
     run bit for bit."""
     import dataclasses
-    if ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
     c = dataclasses.replace(get_config("C0"), stages=4)
     ranks = run_mp(2, config="C0", stages=4, steps=6, events="0:2:13,2:rejoin,3:1:20,5:rejoin")
     losses, state = single(c, 6)

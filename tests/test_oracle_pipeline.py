@@ -165,6 +165,67 @@ def test_second_preemption_is_fatal():
         pp.preempt(0, 0)
 
 
+def test_adjacent_second_preemptions_are_fatal():
+    """After losing v: the double-duty shadow v-1, the dead v itself and the
+    unprotected successor v+1 (its replica was on v) cannot be lost."""
+    cfg = tiny(5, 3)
+    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=True)
+    pp.preempt(2, 4)
+    assert pp.step(*make_tokens(cfg, 0))[0] == "preempted"
+    pp.recover()
+    for v in (1, 2, 3):
+        with pytest.raises(pl.Fatal):
+            pp.preempt(v, 0)
+    for v in (0, 4):
+        pp.preempt(v, 0)      # recoverable: armed (and disarmed by the next line)
+        pp.pending = None
+
+
+def test_non_adjacent_second_preemption_exact():
+    """two non-adjacent preemptions are two independent recoveries.
+    P=4/5: lose v1 at some point of step 0, then a non-adjacent v2 at every
+    point of step 2 (on the failover plan); every step equals the failure-free
+    run exactly; then both rejoin (LIFO) and the run continues exactly."""
+    r = random.Random(3)
+    for P, M in ((4, 3), (5, 4)):
+        cfg = tiny(P, M)
+        flat = make_params(cfg.model)
+        _, ref = _run(cfg, flat, 6)
+        plans = pl.normal_plans(P, M, True)
+        for v1 in range(P):
+            ok = [v for v in range(P) if v not in ((v1 - 1) % P, v1, (v1 + 1) % P)]
+            for v2 in ok:
+                pi1 = r.randint(0, len(plans[v1]))
+                pp = pipeline.Pipeline(cfg, flat, rc=True)
+                pp.preempt(v1, pi1)
+                assert pp.step(*make_tokens(cfg, 0))[0] == "preempted"
+                val, _ = pp.recover()
+                _same((val, pp.full_grads(), pp.full_params(), *pp.full_adam()), ref[0])
+                status, val = pp.step(*make_tokens(cfg, 1))
+                _same((val, pp.full_grads(), pp.full_params(), *pp.full_adam()), ref[1])
+                n2 = len(pp.plans[v2])
+                for pi2 in sorted({0, n2 // 3, n2 // 2, n2, r.randint(0, n2)}):
+                    q = pipeline.Pipeline(cfg, flat, rc=True)
+                    q.preempt(v1, pi1)
+                    q.step(*make_tokens(cfg, 0))
+                    q.recover()
+                    q.step(*make_tokens(cfg, 1))
+                    q.preempt(v2, pi2)
+                    assert q.step(*make_tokens(cfg, 2))[0] == "preempted"
+                    val, info = q.recover()
+                    assert info["victim"] == v2 and q.victims == [v1, v2]
+                    _same((val, q.full_grads(), q.full_params(), *q.full_adam()), ref[2])
+                    _, val = q.step(*make_tokens(cfg, 3))       # double-failover plan
+                    _same((val, q.full_grads(), q.full_params(), *q.full_adam()), ref[3])
+                    q.rejoin()
+                    _, val = q.step(*make_tokens(cfg, 4))
+                    _same((val, q.full_grads(), q.full_params(), *q.full_adam()), ref[4])
+                    q.rejoin()
+                    assert q.mode == "normal"
+                    _, val = q.step(*make_tokens(cfg, 5))
+                    _same((val, q.full_grads(), q.full_params(), *q.full_adam()), ref[5])
+
+
 def test_no_rc_preemption_is_fatal():
     cfg = get_config("C0")
     pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=False)
@@ -200,3 +261,34 @@ def test_rejoin_and_repeated_preemptions_exact():
         for s in range(P):
             for key in ("p", "m", "v"):
                 assert np.array_equal(pp.nodes[s].copies[s][key], pp.nodes[(s - 1) % P].copies[s][key])
+
+
+def test_lflb_injection_sweep_exact():
+    """LFLB: replicas kept in sync, no FRC; a failure recomputes
+    the victim's forward (lazy FRC) and backward (lazy BRC) for the whole
+    step. Every victim / point of a P=3 pipeline equals the failure-free run
+    exactly, and the plans carry no FRC_FWD."""
+    cfg = tiny(3, 4)
+    flat = make_params(cfg.model)
+    _, ref = _run(cfg, flat, 2)
+    plans = pl.normal_plans(3, 4, "lflb")
+    assert not any(i.kind == pl.FRC_FWD for seq in plans.values() for i in seq)
+    for v in range(3):
+        for pi in range(len(plans[v]) + 1):
+            pp = pipeline.Pipeline(cfg, flat, rc="lflb")
+            res = []
+            for t in range(2):
+                tok, tgt = make_tokens(cfg, t)
+                if t == 0:
+                    pp.preempt(v, pi)
+                status, val = pp.step(tok, tgt)
+                if status == "preempted":
+                    val, info = pp.recover()
+                    assert info["frc_done"] == []
+                    if v == 2 and info["commit"]:   # the loss left with the last stage
+                        assert np.isnan(val)
+                        val = ref[0][0]
+                res.append((val, pp.full_grads().copy(), pp.full_params().copy(),
+                            *[a.copy() for a in pp.full_adam()]))
+            _same(res[0], ref[0])
+            _same(res[1], ref[1])

@@ -135,12 +135,37 @@ def _check_failover(P, M, v, plans_new):
         fw = [i.mb for i in plans_new[host] if i.kind == "FWD" and i.stage == X]
         bw = [i.mb for i in plans_new[host] if i.kind == "BWD" and i.stage == X]
         assert fw == list(range(M)) and bw == list(range(M))
-    # rule (4) at merge time: whenever the shadow places a forward, no
-    # backward whose inputs were available was waiting at the other head
-    seq = plans_new[u]
+    # S:535 merge checks on the shadow's list. Provenance is read off the
+    # stage field (the victim's work acts for stage v, the shadow's own for
+    # u or none), so the two sequences are recovered without the merge's
+    # internals; readiness here is data readiness only (local input keys),
+    # so RECV heads (arrival-dependent) are not judged.
+    _check_merge_rules(P, M, u, v, plans_new[u])
+
+
+def _check_merge_rules(P, M, u, v, seq):
+    side = lambda ins: 0 if ins.stage == v else 1          # 0 = victim's, 1 = shadow's
+    A = [i for i in seq if side(i) == 1]
+    B = [i for i in seq if side(i) == 0]
+    heads = {0: 0, 1: 0}
+    lists = {0: B, 1: A}
     avail = set()
-    for idx, ins in enumerate(seq):
+    data_ready = lambda ins: all(k in avail for k in pl.inputs_of(ins, P))
+    for ins in seq:
+        s = side(ins)
         assert all(k in avail for k in pl.inputs_of(ins, P)) or ins.kind in pl.RECVS
+        o = 1 - s
+        other = lists[o][heads[o]] if heads[o] < len(lists[o]) else None
+        if other is not None and other.kind not in pl.RECVS and data_ready(other):
+            if ins.kind not in pl.COMMS:
+                # rule 1: no ready communication left waiting behind a computation
+                assert other.kind not in pl.SENDS, ("rule 1", ins, other)
+                # rule 4: no ready backward left waiting behind a forward
+                assert not (ins.kind == pl.FWD and other.kind == pl.BWD), ("rule 4", ins, other)
+            elif s == 1:
+                # rule 3: the victim's external communication goes first
+                assert other.kind not in pl.SENDS, ("rule 3", ins, other)
+        heads[s] += 1
         avail.update(pl.outputs_of(ins, P, M))
 
 
@@ -169,3 +194,15 @@ def test_recovery_property_suite():
                     assert all(len(q) == 0 for q in ch2.values())
                     if not info["commit"]:
                         assert info["brc_mb"] == list(range(M))
+
+
+def test_failover_goldens_exercise_merge_rules_1_3_4():
+    """P=3, M=2 failover plans derived by hand from the four rules of
+    P:538-545 (tests/golden/README.md walks the derivation): v=1 (shadow 0,
+    rule 1: RECV_GRAD / REPLICA_SEND before ready computations) and v=0
+    (shadow 2 = last stage, the wrap case: rule 3 puts the victim's
+    RECV_GRAD ahead of the shadow's ready RECV_ACT / REPLICA_SEND, rule 4
+    BWD before a ready FWD)."""
+    for v in (0, 1):
+        want = open(os.path.join(GOLD, f"p3_m2_failover_v{v}.txt")).read()
+        assert pl.dump_lines(pl.failover_plans(3, 2, v)) == want, v

@@ -76,3 +76,30 @@ def test_invalid_configs_rejected():
         bbl.plan_dump(cfg.model, 5, 4)              # stages > n_layer
     with pytest.raises(bbl.BambooError):
         bbl.plan_dump(cfg.model, 1, 4, victim=0)    # no replica without RC partner
+
+
+def test_cpp_failover_goldens():
+    """The library's merge reproduces the hand-derived P=3 goldens
+    (tests/golden/p3_m2_failover_v*.txt)."""
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    m = dict(n_layer=3, d_model=64, n_head=2, d_ff=256, vocab=128, seq_len=32, causal=1)
+    for v in (0, 1):
+        text = bbl.plan_dump(m, 3, 2, victim=v, micro_batch=1)
+        lines = "".join(l + "\n" for l in text.splitlines() if not l.startswith("#"))
+        assert lines == open(os.path.join(gold, f"p3_m2_failover_v{v}.txt")).read(), v
+
+
+def test_cpp_lflb_plans_match_oracle():
+    r = random.Random(9)
+    m = dict(n_layer=6, d_model=64, n_head=2, d_ff=256, vocab=128, seq_len=32, causal=1)
+    for _ in range(20):
+        P, M = r.randint(2, 6), r.randint(1, 7)
+        got = bbl.plan_dump(m, P, M, rc="lflb", micro_batch=1)
+        want = pl.dump(P, M, "lflb", pl.partition(6, P), pl.normal_plans(P, M, "lflb"))
+        assert got == want, (P, M)
+        v = r.randrange(P)
+        n = len(pl.normal_plans(P, M, "lflb")[v])
+        pi = r.randint(0, n)
+        assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc="lflb", micro_batch=1) == \
+            pl.recovery_dump(P, M, v, pi, rc="lflb"), (P, M, v, pi)

@@ -56,9 +56,9 @@ def main():
     tok, tgt = make_tokens(cfg, 0)
     # one pipeline for the whole sweep (training simply continues from one k
     # to the next; every k starts and ends on the normal, fully protected plan)
-    nid = bench.bcast_bytes(bb.nccl_unique_id() if rank == 0 else None, ws) if ws > 1 else None
+    nid = bench.bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None
     pipe = bb.Pipeline(m, P, M, micro_batch=mb, rc=True, world_rank=rank, world_size=ws,
-                       device=local, nccl_id=nid)
+                       device=local, session_id=nid)
     pipe.load_params(flat)
     pipe.stage_inputs(tok, tgt)
     for _ in range(3):
