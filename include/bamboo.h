@@ -108,6 +108,17 @@ typedef struct {
                                    granularity; 1: persistent full-device grids (r01)     */
   int timing;                   /* 1 = per-instruction CUDA events on every node for
                                    bb_node_stats (busy / bubble / FRC accounting)        */
+  int detect_ms;                /* 0 (default): injected preemptions, bb_preempt called with
+                                   the same arguments on every rank. > 0: fail-stop mode
+                                   (needs one node per rank): bb_preempt is called on the
+                                   victim's rank only; that rank stops at the injection
+                                   point and goes silent (its bb_step returns
+                                   BB_E_PREEMPTED; the caller then calls bb_destroy and
+                                   exits). The other ranks detect the loss when the
+                                   victim's heartbeat in host shared memory is older than
+                                   detect_ms (P:417-420 timeouts), run to quiescence,
+                                   agree on the cut from the victim's delivered messages
+                                   and return BB_E_PREEMPTED from their own bb_step     */
 } bb_opts;
 
 typedef struct {

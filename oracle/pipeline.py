@@ -133,17 +133,21 @@ class Pipeline:
             out, saved = self._stage_fwd(X, c, x_in, k)
             st[("saved", X, k)] = saved
             st[("act", X + 1, k) if X < P - 1 else ("loss", k)] = out
-        elif kd == pl.BWD:
+        elif kd in (pl.BWD, pl.BRC_BWD):
             c = node.copies[X]
             d = None if X == P - 1 else st[("dact", X + 1, k)]
             din = self._stage_bwd(X, c, st[("saved", X, k)], d, k)
             if X > 0:
-                st[("dact", X, k)] = din
+                if kd == pl.BWD:
+                    st[("dact", X, k)] = din
+                else:   # EFEB: the same value the victim would send; keep a received one
+                    st.setdefault(("dact", X, k), din)
             if k == self.M - 1:
                 st[("gradsum", X)] = c["g"]
         elif kd in pl.SENDS:
             payload = {pl.SEND_ACT: lambda: st[("act", X + 1, k)],
                        pl.SEND_GRAD: lambda: st[("dact", X, k)],
+                       pl.SEND_DGRAD: lambda: st[("dact", X, k)],
                        pl.RESEND_GRAD: lambda: st[("dact", X, k)],
                        pl.REPLICA_SEND: lambda: st[("gradsum", X)].copy()}[kd]()
             self.payloads[id(msg)] = payload
@@ -151,7 +155,7 @@ class Pipeline:
             payload = self.payloads.pop(id(msg))
             if kd == pl.RECV_ACT:
                 st[("act", X, k)] = payload
-            elif kd == pl.RECV_GRAD:
+            elif kd in (pl.RECV_GRAD, pl.RECV_DGRAD):
                 st[("dact", X + 1, k)] = payload
             else:
                 c = node.copies[X]

@@ -32,8 +32,12 @@ Instr = namedtuple("Instr", "kind mb peer stage")
 LOAD_INPUTS, FWD, FRC_FWD, BWD = "LOAD_INPUTS", "FWD", "FRC_FWD", "BWD"
 SEND_ACT, RECV_ACT, SEND_GRAD, RECV_GRAD = "SEND_ACT", "RECV_ACT", "SEND_GRAD", "RECV_GRAD"
 RESEND_GRAD, REPLICA_SEND, REPLICA_RECV, APPLY = "RESEND_GRAD", "REPLICA_SEND", "REPLICA_RECV", "APPLY"
-SENDS = {SEND_ACT, SEND_GRAD, RESEND_GRAD, REPLICA_SEND}
-RECVS = {RECV_ACT, RECV_GRAD, REPLICA_RECV}
+BRC_BWD = "BRC_BWD"   # EFEB: eager redundant backward of the replica stage
+# EFEB: the duplicate of a stage's input-gradient for the node two back (its
+# own message kind, so it never shares a FIFO with the normal gradients)
+SEND_DGRAD, RECV_DGRAD = "SEND_DGRAD", "RECV_DGRAD"
+SENDS = {SEND_ACT, SEND_GRAD, RESEND_GRAD, REPLICA_SEND, SEND_DGRAD}
+RECVS = {RECV_ACT, RECV_GRAD, REPLICA_RECV, RECV_DGRAD}
 COMMS = SENDS | RECVS
 
 
@@ -76,7 +80,7 @@ def partition(n_layer, P, layers_per_stage=None):
 # ----------------------------------------------------------------------------
 # normal plans (A2)
 # ----------------------------------------------------------------------------
-MODES = ("none", "eflb", "lflb")
+MODES = ("none", "eflb", "lflb", "efeb")
 
 
 def rc_mode(rc):
@@ -90,11 +94,21 @@ def rc_mode(rc):
 
 def stage_plan(s, P, M, rc):
     """Instruction list of node s in a failure-free step. rc: False / "none"
-    (no redundancy), True / "eflb" (replica + eager FRC) or
+    (no redundancy), True / "eflb" (replica + eager FRC),
     "lflb" (replica kept in sync, no FRC: the victim's forward is recomputed
-    lazily on failure, "LFLB")."""
+    lazily on failure, "LFLB") or "efeb" (eager FRC and eager BRC:
+    node s also runs the backward of its replica stage r = s+1 every step,
+    BRC_BWD(k), from the gradient node r+1 = s+2 sends it next to its normal
+    send, "BRC requires the output of BNC_{n+2}"; the replica's own
+    gradient then equals the primary's, so there is no replica sync).
+    EFEB placement (this build's reading): BRC_BWD(k) (with its RECV_GRAD
+    from s+2) right before node s's own RECV_GRAD(k); on the last node (the
+    replica of stage 0 needs stage 1's gradient, which comes last) all of
+    them after its own backwards."""
     mode = rc_mode(rc)
-    rc, frc = mode != "none", mode == "eflb"
+    rc, frc = mode != "none", mode in ("eflb", "efeb")
+    efeb = mode == "efeb"
+    r = (s + 1) % P
     if rc and P < 2:
         raise PlanError("RC needs P >= 2")
     I = []
@@ -115,12 +129,21 @@ def stage_plan(s, P, M, rc):
             if frc:
                 I.append(Instr(FRC_FWD, k, None, s + 1))
 
+    def brc(k):
+        if r < P - 1 and P >= 3:
+            I.append(Instr(RECV_DGRAD, k, (r + 1) % P, r))
+        I.append(Instr(BRC_BWD, k, None, r))
+
     def bwd(k):
+        if efeb and s < P - 1:
+            brc(k)
         if s < P - 1:
             I.append(Instr(RECV_GRAD, k, s + 1, s))
         I.append(Instr(BWD, k, None, s))
         if s > 0:
             I.append(Instr(SEND_GRAD, k, s - 1, s))
+            if efeb and P >= 3:   # the gradient node s-2 needs for its BRC of stage s-1
+                I.append(Instr(SEND_DGRAD, k, (s - 2) % P, s))
 
     for k in range(W):
         fwd(k)
@@ -129,7 +152,13 @@ def stage_plan(s, P, M, rc):
         bwd(i)
     for i in range(M - W, M):
         bwd(i)
-    if rc:
+    if efeb:
+        if s == P - 1:
+            for k in range(M):
+                brc(k)
+        I.append(Instr(APPLY, None, None, s))
+        I.append(Instr(APPLY, None, None, r))
+    elif rc:
         I.append(Instr(REPLICA_SEND, None, (s - 1) % P, s))
         I.append(Instr(REPLICA_RECV, None, (s + 1) % P, (s + 1) % P))
         I.append(Instr(APPLY, None, None, s))
@@ -175,11 +204,11 @@ def inputs_of(ins, P):
         if X == P - 1:
             keys.append(("tgt", k))
         return keys
-    if ins.kind == BWD:
+    if ins.kind in (BWD, BRC_BWD):
         return [("saved", X, k)] + ([("dact", X + 1, k)] if X < P - 1 else [])
     if ins.kind == SEND_ACT:
         return [("act", X + 1, k)]
-    if ins.kind in (SEND_GRAD, RESEND_GRAD):
+    if ins.kind in (SEND_GRAD, RESEND_GRAD, SEND_DGRAD):
         return [("dact", X, k)]
     if ins.kind in (REPLICA_SEND, APPLY):
         return [("gradsum", X)]
@@ -192,12 +221,12 @@ def outputs_of(ins, P, M):
         return [("tok", j) for j in range(M)] + [("tgt", j) for j in range(M)]
     if ins.kind in (FWD, FRC_FWD):
         return [("saved", X, k), ("act", X + 1, k) if X < P - 1 else ("loss", k)]
-    if ins.kind == BWD:
+    if ins.kind in (BWD, BRC_BWD):
         out = [("dact", X, k)] if X > 0 else []
         return out + ([("gradsum", X)] if k == M - 1 else [])
     if ins.kind == RECV_ACT:
         return [("act", X, k)]
-    if ins.kind == RECV_GRAD:
+    if ins.kind in (RECV_GRAD, RECV_DGRAD):
         return [("dact", X + 1, k)]
     if ins.kind == REPLICA_RECV:
         return [("gradsum", X)]
@@ -217,6 +246,10 @@ def message_of(ins):
         return ("grad", ins.mb, ins.stage + 1)
     if ins.kind in (REPLICA_SEND, REPLICA_RECV):
         return ("gradsum", None, ins.stage)
+    if ins.kind == SEND_DGRAD:
+        return ("dgrad", ins.mb, ins.stage)
+    if ins.kind == RECV_DGRAD:
+        return ("dgrad", ins.mb, ins.stage + 1)
     raise ValueError(ins)
 
 
@@ -263,7 +296,7 @@ def lockstep(plans, pcs=None, channels=None, cap=None, on_exec=None):
 # failover / recovery transforms (A12/A13)
 # ----------------------------------------------------------------------------
 def _rank(ins):
-    return {BWD: 0, FWD: 1, FRC_FWD: 1}.get(ins.kind, 2)
+    return {BWD: 0, BRC_BWD: 0, FWD: 1, FRC_FWD: 1}.get(ins.kind, 2)
 
 
 def merge(A, B, avail, P, M, u, others, channels):
@@ -338,13 +371,20 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     pv = plans[v]
     executed_v = pv[:pcs[v]]
     commit = any(i.kind == REPLICA_SEND for i in executed_v)
+    # EFEB (eager BRC): the shadow already runs the victim stage's backward
+    # (BRC_BWD) from the duplicate gradients w sends it, so the victim's
+    # backward, its APPLY and its receives from w are not replayed; every
+    # message to the victim is dropped (the shadow has its copy) and every
+    # receive from it is rerouted to the shadow, which takes over the
+    # victim's remaining sends (its duplicate gradients for node v-2).
+    efeb = any(i.kind == BRC_BWD for seq in plans.values() for i in seq)
 
     def executed(n):
         return plans[n][:pcs[n]]
 
     # messages from v that a survivor has not consumed yet (delivered, in FIFO)
     pending_from_v = {n: {kind: [m for m, _ in channels.get((v, n, kind), [])]
-                          for kind in ("act", "grad", "gradsum")} for n in plans if n != v}
+                          for kind in ("act", "grad", "gradsum", "dgrad")} for n in plans if n != v}
 
     def delivered_filter(n, seq, local_peer_to):
         """Walk n's remaining RECVs from v in order against the delivered FIFO:
@@ -373,7 +413,7 @@ def recovery_plans(plans, P, M, v, pcs, channels):
             continue                                  # becomes v's FWD (in B)
         if ins.kind in SENDS and ins.peer == v:
             continue                                  # victim<->shadow (rule 2)
-        if ins.kind == APPLY and ins.stage == v and not commit:
+        if ins.kind == APPLY and ins.stage == v and not commit and not efeb:
             continue                                  # v's update runs from B
         A.append(ins)
     A = delivered_filter(u, A, lambda ins: None)
@@ -386,14 +426,16 @@ def recovery_plans(plans, P, M, v, pcs, channels):
             kd = ins.kind
             if kd in (LOAD_INPUTS, FRC_FWD, REPLICA_SEND, REPLICA_RECV):
                 continue
-            if kd == APPLY and ins.stage != v:
+            if kd == APPLY and (ins.stage != v or efeb):
                 continue
+            if efeb and kd in (BWD, BRC_BWD, RECV_GRAD, RECV_DGRAD):
+                continue                              # the shadow's BRC_BWD does it
             if kd in COMMS and ins.peer == u:
                 continue                              # rule 2: becomes local
             if kd == FWD and ins.mb in frc_done:
                 continue                              # use the retained FRC result
-            if kd == SEND_ACT and idx < pcs[v]:
-                continue                              # already delivered to w
+            if kd in SENDS and idx < pcs[v]:
+                continue                              # already delivered
             B.append(ins)
 
     # ---- W: the successor's remaining instructions, rerouted to the shadow
@@ -402,7 +444,10 @@ def recovery_plans(plans, P, M, v, pcs, channels):
         if n == v:
             continue
         seq = A if n == u else list(plans[n][pcs[n]:])
-        if n == w:
+        if efeb and n != u:
+            seq = [i for i in seq if not (i.kind in SENDS and i.peer == v)]
+            seq = delivered_filter(n, seq, lambda ins: u)
+        elif n == w:
             resend = []
             if not commit and w != u:
                 resend = [Instr(RESEND_GRAD, i.mb, u, i.stage) for i in executed(w)
@@ -422,7 +467,9 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     others = {n: seq for n, seq in new.items() if n != u}
     new[u] = merge(new[u], B, avail, P, M, u, others, channels)
     info = {"victim": v, "shadow": u, "successor": w, "commit": commit,
-            "frc_done": sorted(frc_done), "brc_mb": sorted(i.mb for i in B if i.kind == BWD),
+            "frc_done": sorted(frc_done),
+            "brc_mb": sorted(i.mb for i in (A if efeb else B)
+                             if i.kind in (BWD, BRC_BWD) and i.stage == v),
             "resend": [i.mb for i in new.get(w, []) if i.kind == RESEND_GRAD]}
     return new, info
 

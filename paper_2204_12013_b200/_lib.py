@@ -49,7 +49,8 @@ class BBOpts(ctypes.Structure):
                 ("world_size", ctypes.c_int), ("device", ctypes.c_int),
                 ("node_rank", ctypes.POINTER(ctypes.c_int)), ("session_id", ctypes.c_void_p),
                 ("profile", ctypes.c_int), ("frc_retain_bytes", ctypes.c_size_t),
-                ("frc_persistent", ctypes.c_int), ("timing", ctypes.c_int)]
+                ("frc_persistent", ctypes.c_int), ("timing", ctypes.c_int),
+                ("detect_ms", ctypes.c_int)]
 
 
 class BBStepStats(ctypes.Structure):
@@ -156,7 +157,7 @@ def _ints(xs):
 def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-4, beta1=0.9,
               beta2=0.999, eps=1e-8, world_rank=0, world_size=1, device=0, node_rank=None,
               session_id=None, profile=False, frc_retain_bytes=0, frc_persistent=False,
-              timing=False):
+              timing=False, detect_ms=0):
     """rc: True (= "eflb"), False (= "none") or a mode name in RC."""
     o = BBOpts()
     lib().bb_default_opts(ctypes.byref(o))
@@ -180,6 +181,7 @@ def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-
     o.frc_retain_bytes = int(frc_retain_bytes)
     o.frc_persistent = int(bool(frc_persistent))
     o.timing = int(bool(timing))
+    o.detect_ms = int(detect_ms)
     return o, keep
 
 

@@ -360,17 +360,92 @@ __global__ void embed_fwd_kernel(int R, int S, int H, const int32_t *__restrict_
 }
 
 template <typename T>
-__global__ void embed_bwd_tok_kernel(int H, const int32_t *__restrict__ uniq,
+__global__ void embed_bwd_tok_kernel(int H, const int32_t *__restrict__ nuniq,
+                                     const int32_t *__restrict__ uniq,
                                      const int32_t *__restrict__ offs,
                                      const int32_t *__restrict__ pos, const T *__restrict__ dx,
                                      float *__restrict__ dE) {
   const int u = blockIdx.x;
+  if (u >= *nuniq) return;   // grid = R, the CSR's U <= R lives on the device
   const int a = offs[u], b = offs[u + 1];
   float *out = dE + (size_t)uniq[u] * H;
   for (int i = threadIdx.x; i < H; i += blockDim.x) {
     float s = 0.f;
     for (int p = a; p < b; ++p) s += to_f(dx[(size_t)pos[p] * H + i]);
     out[i] += s;
+  }
+}
+
+// Per-micro-batch token CSR for the deterministic embedding backward, built on
+// the device (one CTA per micro-batch): a bitonic sort of the 64-bit keys
+// (token << 32 | position) in shared memory gives the positions grouped by
+// token in ascending position order (the keys are unique, so the order is the
+// stable one); a block scan of the "new token" flags then writes
+// uniq[U], offs[U+1], pos[R] and U at blob[3R+1].
+constexpr int CSR_T = 1024;
+__global__ void __launch_bounds__(CSR_T) embed_csr_kernel(int R, int n2, const int32_t *__restrict__ tok,
+                                                        int32_t *__restrict__ blob_all,
+                                                        size_t stride) {
+  extern __shared__ unsigned long long key[];   // n2 keys
+  __shared__ int wsum[CSR_T / 32];
+  const int k = blockIdx.x;
+  const int32_t *t = tok + (size_t)k * R;
+  int32_t *blob = blob_all + (size_t)k * stride;
+  int32_t *uniq = blob, *offs = blob + R, *pos = blob + 2 * R + 1;
+  for (int i = threadIdx.x; i < n2; i += CSR_T)
+    key[i] = i < R ? ((unsigned long long)(unsigned)t[i] << 32) | (unsigned)i : ~0ull;
+  __syncthreads();
+  for (int kk = 2; kk <= n2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += CSR_T) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = key[i], b = key[ixj];
+          if ((a > b) == ((i & kk) == 0)) {
+            key[i] = b;
+            key[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // block scan of the group-start flags; thread i owns a contiguous chunk
+  const int per = (R + CSR_T - 1) / CSR_T;
+  const int lo = threadIdx.x * per, hi = min(R, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i)
+    cnt += (i == 0 || (key[i] >> 32) != (key[i - 1] >> 32)) ? 1 : 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < CSR_T / 32 ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane < CSR_T / 32) wsum[lane] = v;   // inclusive over warps
+  }
+  __syncthreads();
+  int base = incl - cnt + (w > 0 ? wsum[w - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    pos[i] = (int32_t)(key[i] & 0xffffffffu);
+    if (i == 0 || (key[i] >> 32) != (key[i - 1] >> 32)) {
+      uniq[base] = (int32_t)(key[i] >> 32);
+      offs[base] = i;
+      ++base;
+    }
+  }
+  if (threadIdx.x == CSR_T - 1) {
+    const int U = wsum[CSR_T / 32 - 1];
+    offs[U] = R;
+    blob[3 * R + 1] = U;
   }
 }
 
@@ -756,14 +831,29 @@ cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const 
   return cudaGetLastError();
 }
 
-cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const int32_t *uniq,
-                      const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
-                      float *dPos, cudaStream_t s) {
+size_t embed_csr_ints(int R) { return 3 * (size_t)R + 2; }
+
+cudaError_t embed_csr(int M, int R, const int32_t *tok, int32_t *blob, cudaStream_t s) {
+  int n2 = 1;
+  while (n2 < R) n2 <<= 1;
+  const size_t smem = (size_t)n2 * 8;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(embed_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  embed_csr_kernel<<<M, CSR_T, smem, s>>>(R, n2, tok, blob, embed_csr_ints(R));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, const int32_t *csr,
+                      const void *dx, float *dE, float *dPos, cudaStream_t s) {
+  const int32_t *uniq = csr, *offs = csr + R, *pos = csr + 2 * R + 1, *nu = csr + 3 * R + 1;
   if (dx_f32 || !bf16) {
-    embed_bwd_tok_kernel<float><<<U, 128, 0, s>>>(H, uniq, offs, pos, cp<float>(dx), dE);
+    embed_bwd_tok_kernel<float><<<R, 128, 0, s>>>(H, nu, uniq, offs, pos, cp<float>(dx), dE);
     embed_bwd_pos_kernel<float><<<S, 128, 0, s>>>(R / S, S, H, cp<float>(dx), dPos);
   } else {
-    embed_bwd_tok_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(H, uniq, offs, pos,
+    embed_bwd_tok_kernel<__nv_bfloat16><<<R, 128, 0, s>>>(H, nu, uniq, offs, pos,
                                                           cp<__nv_bfloat16>(dx), dE);
     embed_bwd_pos_kernel<__nv_bfloat16><<<S, 128, 0, s>>>(R / S, S, H, cp<__nv_bfloat16>(dx),
                                                           dPos);

@@ -39,10 +39,12 @@ bool gemm_tc_supported(const Gemm &g);
 cudaError_t embed_fwd(bool bf16, int R, int S, int H, const int32_t *tok, const void *E,
                       const void *Pos, void *x, cudaStream_t s);
 // Deterministic embedding backward: tokens of the micro-batch grouped by id
-// (host-built CSR: uniq[U], offs[U+1], pos[R] ascending within a group).
-cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, int U, const int32_t *uniq,
-                      const int32_t *offs, const int32_t *pos, const void *dx, float *dE,
-                      float *dPos, cudaStream_t s);
+// through a device-built CSR blob per micro-batch (embed_csr_ints(R) ints:
+// uniq[R] | offs[R+1] | pos[R] | U), positions ascending within a group.
+size_t embed_csr_ints(int R);
+cudaError_t embed_csr(int M, int R, const int32_t *tok, int32_t *blob, cudaStream_t s);
+cudaError_t embed_bwd(bool bf16, bool dx_f32, int R, int S, int H, const int32_t *csr,
+                      const void *dx, float *dE, float *dPos, cudaStream_t s);
 
 cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
                           void *y, float *mean, float *rstd, cudaStream_t s);

@@ -8,15 +8,19 @@
 namespace bb {
 
 const char *kind_name(Kind k) {
-  static const char *n[] = {"LOAD_INPUTS", "FWD",       "FRC_FWD",     "BWD",
-                            "SEND_ACT",    "RECV_ACT",  "SEND_GRAD",   "RECV_GRAD",
-                            "RESEND_GRAD", "REPLICA_SEND", "REPLICA_RECV", "APPLY"};
+  static const char *n[] = {"LOAD_INPUTS", "FWD",          "FRC_FWD",      "BWD",
+                            "SEND_ACT",    "RECV_ACT",     "SEND_GRAD",    "RECV_GRAD",
+                            "RESEND_GRAD", "REPLICA_SEND", "REPLICA_RECV", "APPLY",
+                            "BRC_BWD",     "SEND_DGRAD",   "RECV_DGRAD"};
   return n[k];
 }
 bool is_send(Kind k) {
-  return k == SEND_ACT || k == SEND_GRAD || k == RESEND_GRAD || k == REPLICA_SEND;
+  return k == SEND_ACT || k == SEND_GRAD || k == RESEND_GRAD || k == REPLICA_SEND ||
+         k == SEND_DGRAD;
 }
-bool is_recv(Kind k) { return k == RECV_ACT || k == RECV_GRAD || k == REPLICA_RECV; }
+bool is_recv(Kind k) {
+  return k == RECV_ACT || k == RECV_GRAD || k == REPLICA_RECV || k == RECV_DGRAD;
+}
 
 Msg message_of(const Instr &i) {
   switch (i.kind) {
@@ -27,6 +31,8 @@ Msg message_of(const Instr &i) {
     case RECV_GRAD: return {MSG_GRAD, i.mb, i.stage + 1}; // produced by the next stage
     case REPLICA_SEND:
     case REPLICA_RECV: return {MSG_GRADSUM, -1, i.stage};
+    case SEND_DGRAD: return {MSG_DGRAD, i.mb, i.stage};
+    case RECV_DGRAD: return {MSG_DGRAD, i.mb, i.stage + 1};
     default: throw PlanError("message_of on a compute instruction");
   }
 }
@@ -40,13 +46,15 @@ std::vector<Key> inputs_of(const Instr &i, int P) {
       if (X == P - 1) v.push_back({K_TGT, k, 0});
       return v;
     }
-    case BWD: {
+    case BWD:
+    case BRC_BWD: {
       std::vector<Key> v{{K_SAVED, X, k}};
       if (X < P - 1) v.push_back({K_DACT, X + 1, k});
       return v;
     }
     case SEND_ACT: return {{K_ACT, X + 1, k}};
     case SEND_GRAD:
+    case SEND_DGRAD:
     case RESEND_GRAD: return {{K_DACT, X, k}};
     case REPLICA_SEND:
     case APPLY: return {{K_GRADSUM, X, 0}};
@@ -66,14 +74,16 @@ std::vector<Key> outputs_of(const Instr &i, int P, int M) {
     case FWD:
     case FRC_FWD:
       return {{K_SAVED, X, k}, X < P - 1 ? Key{K_ACT, X + 1, k} : Key{K_LOSS, k, 0}};
-    case BWD: {
+    case BWD:
+    case BRC_BWD: {
       std::vector<Key> v;
       if (X > 0) v.push_back({K_DACT, X, k});
       if (k == M - 1) v.push_back({K_GRADSUM, X, 0});
       return v;
     }
     case RECV_ACT: return {{K_ACT, X, k}};
-    case RECV_GRAD: return {{K_DACT, X + 1, k}};
+    case RECV_GRAD:
+    case RECV_DGRAD: return {{K_DACT, X + 1, k}};
     case REPLICA_RECV: return {{K_GRADSUM, X, 0}};
     default: return {};
   }
@@ -111,9 +121,12 @@ std::vector<std::pair<int, int>> partition(int L, int P, const int *lps) {
 // -------------------------------------------------------------- normal plan
 std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
   // mode = bb_rc_mode: NONE 0, EFLB 1 (replicas + eager FRC), LFLB 2
-  // (replicas, no FRC: the forward is recomputed lazily on failure)
-  const bool rc = mode != 0, frc = mode == 1;
+  // (replicas, no FRC: the forward is recomputed lazily on failure), EFEB 3
+  // (eager FRC and eager BRC of the replica stage r = s+1 from the duplicate
+  // gradient node s+2 sends, no replica sync)
+  const bool rc = mode != 0, frc = mode == 1 || mode == 3, efeb = mode == 3;
   if (rc && P < 2) throw PlanError("RC needs stages >= 2");
+  const int r = (s + 1) % P;
   std::vector<Instr> I;
   const bool need_tok = s == 0 || (rc && s == P - 1);
   const bool need_tgt = s == P - 1 || (rc && s == P - 2);
@@ -128,10 +141,18 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
       if (frc) I.push_back({FRC_FWD, k, -1, s + 1});
     }
   };
+  auto brc = [&](int k) {   // EFEB: the replica stage's backward, eagerly
+    if (r < P - 1 && P >= 3) I.push_back({RECV_DGRAD, k, (r + 1) % P, r});
+    I.push_back({BRC_BWD, k, -1, r});
+  };
   auto bwd = [&](int k) {
+    if (efeb && s < P - 1) brc(k);
     if (s < P - 1) I.push_back({RECV_GRAD, k, s + 1, s});
     I.push_back({BWD, k, -1, s});
-    if (s > 0) I.push_back({SEND_GRAD, k, s - 1, s});
+    if (s > 0) {
+      I.push_back({SEND_GRAD, k, s - 1, s});
+      if (efeb && P >= 3) I.push_back({SEND_DGRAD, k, (s - 2 + P) % P, s});
+    }
   };
   for (int k = 0; k < W; ++k) fwd(k);
   for (int i = 0; i < M - W; ++i) {
@@ -139,7 +160,12 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
     bwd(i);
   }
   for (int i = M - W; i < M; ++i) bwd(i);
-  if (rc) {
+  if (efeb) {
+    if (s == P - 1)   // stage 1's gradients come last: after the own backwards
+      for (int k = 0; k < M; ++k) brc(k);
+    I.push_back({APPLY, -1, -1, s});
+    I.push_back({APPLY, -1, -1, r});
+  } else if (rc) {
     I.push_back({REPLICA_SEND, -1, (s - 1 + P) % P, s});
     I.push_back({REPLICA_RECV, -1, (s + 1) % P, (s + 1) % P});
     I.push_back({APPLY, -1, -1, s});
@@ -208,54 +234,237 @@ Cut cut(const Plans &plans, int v, int pi) {
   return c;
 }
 
-// -------------------------------------------------------------------- merge
+// ----------------------------------------------------------------- recovery
+// The continuation after node v is lost (readings Q2-Q5 and the
+// EFEB reading in DESIGN.md §2). Written from the rules, independently of the
+// oracle's implementation (oracle/plan.py); the two must produce the same
+// text (tests/test_plan_parity.py), which is what makes the comparison a
+// check of the rules rather than of one transcription.
+//
+//  shadow u = v-1 (rule set A): keeps its own remaining work, except
+//    - its FRC of v (the victim's forward is rerun as a FWD from B),
+//    - its sends to v and its receives of messages v never delivered
+//      (rule 2: victim <-> shadow traffic becomes local data),
+//    - v's APPLY when B brings one (EFLB before v's commit point).
+//  victim v (rule set B, run by u): its whole step again, except what was
+//    already done elsewhere: inputs (u loads them for its FRC), FRC /
+//    replica work (its replica is gone), forwards whose FRC u already ran
+//    (the retained FRC result is reused), sends it had delivered, the
+//    traffic with u (rule 2); nothing at all once it committed (Q13). EFEB:
+//    also not its backward and its gradient receives (u's eager BRC_BWD is
+//    that backward, fed by the duplicate gradients w already sends u).
+//  every other survivor: EFLB - the successor w re-sends the gradients v
+//    received from it (Q3), its other traffic with v goes to u instead, and
+//    its replica gradient for v is dropped (w is unprotected now, Q21);
+//    EFEB - messages to v are dropped (u has its own copies), receives from
+//    v that v had not delivered come from u.
+//  A and B are then merged as two sequences (Q5): among the ready heads a
+//  communication goes first (rule 1), the victim's first among
+//  communications (rule 3); among computations backward before forward
+//  (rule 4), then ascending micro-batch, then the victim's.
 namespace {
-int compute_rank(Kind k) { return k == BWD ? 0 : (k == FWD || k == FRC_FWD) ? 1 : 2; }
 
-std::vector<Instr> merge(const std::vector<Instr> &A, const std::vector<Instr> &B,
-                         std::set<Key> avail, int P, int M, int u, const Plans &others,
-                         const Channels &channels) {
-  Channels och = channels;
-  std::map<int, int> opcs;
-  const std::map<int, int> nocap;
-  lockstep(others, opcs, och, nocap);
-  size_t a = 0, b = 0;
+enum Fate { KEEP, DROP, TO_SHADOW };
+
+struct Loss {
+  int P, M, v, u, w;
+  bool efeb = false, commit = false;
+  std::set<int> frc_done;
+  const std::map<int, int> *pcs = nullptr;
+  const Channels *ch = nullptr;
+};
+
+int step_kind_rank(Kind k) {
+  if (k == BWD || k == BRC_BWD) return 0;
+  if (k == FWD || k == FRC_FWD) return 1;
+  return 2;
+}
+
+// Messages v had delivered to node n that n has not consumed yet, per kind.
+std::map<int, std::deque<Msg>> undelivered_queue(const Loss &x, int n) {
+  std::map<int, std::deque<Msg>> q;
+  for (auto &kv : *x.ch)
+    if (std::get<0>(kv.first) == x.v && std::get<1>(kv.first) == n)
+      q[std::get<2>(kv.first)] = kv.second;
+  return q;
+}
+
+Fate shadow_fate(const Loss &x, const Instr &i) {
+  if (i.kind == FRC_FWD && i.stage == x.v) return DROP;
+  if (is_send(i.kind) && i.peer == x.v) return DROP;
+  if (i.kind == APPLY && i.stage == x.v && !x.commit && !x.efeb) return DROP;
+  return KEEP;
+}
+
+Fate survivor_fate(const Loss &x, int n, const Instr &i) {
+  if (!is_send(i.kind) || i.peer != x.v) return KEEP;
+  if (x.efeb) return DROP;
+  if (n != x.w || i.kind == REPLICA_SEND) return DROP;
+  return TO_SHADOW;
+}
+
+bool victim_work(const Loss &x, const Instr &i, int idx) {
+  if (x.commit) return false;
+  switch (i.kind) {
+    case LOAD_INPUTS:
+    case FRC_FWD:
+    case BRC_BWD:
+    case REPLICA_SEND:
+    case REPLICA_RECV:
+      return false;
+    case APPLY:
+      return i.stage == x.v && !x.efeb;
+    case BWD:
+      return !x.efeb;
+    case RECV_GRAD:
+    case RECV_DGRAD:
+      if (x.efeb) return false;
+      break;
+    case FWD:
+      return !x.frc_done.count(i.mb);
+    default:
+      break;
+  }
+  if (is_comm(i.kind) && i.peer == x.u) return false;
+  if (is_send(i.kind) && idx < x.pcs->at(x.v)) return false;
+  return true;
+}
+
+// Rewrite node n's remaining instructions: fates for the other instructions,
+// and every receive from v either stays (its message is already in n's FIFO)
+// or, when v never delivered it, is dropped (n == u) or taken from u.
+std::vector<Instr> rewrite(const Loss &x, int n, const std::vector<Instr> &rest) {
+  auto q = undelivered_queue(x, n);
   std::vector<Instr> out;
-  auto ready = [&](const Instr &ins) {
-    if (is_recv(ins.kind)) {
-      const Msg want = message_of(ins);
-      auto it = och.find(ChanKey{ins.peer, u, want.kind});
-      return it != och.end() && !it->second.empty() && it->second.front() == want;
+  for (Instr i : rest) {
+    if (is_recv(i.kind) && i.peer == x.v) {
+      auto &d = q[message_of(i).kind];
+      if (!d.empty() && d.front() == message_of(i)) {
+        d.pop_front();
+        out.push_back(i);
+      } else if (n != x.u) {
+        i.peer = x.u;
+        out.push_back(i);
+      }
+      continue;
     }
-    for (const Key &k : inputs_of(ins, P))
+    const Fate f = n == x.u ? shadow_fate(x, i) : survivor_fate(x, n, i);
+    if (f == DROP) continue;
+    if (f == TO_SHADOW) i.peer = x.u;
+    out.push_back(i);
+  }
+  return out;
+}
+
+// Merge readiness of a RECV at the shadow, decided on the dependency graph of
+// the other survivors' lists instead of by simulating them: the message the
+// receive expects is either already in the shadow's FIFO, or it is sent by an
+// instruction of its producer that can run given what the shadow has placed
+// so far (everything before it on that node can run, and each receive there
+// is fed by a message that is pending or sent by something that can run).
+struct Readiness {
+  const Loss &x;
+  const Plans &lists;                          // the other survivors' new lists
+  std::map<ChanKey, std::vector<Msg>> pending; // per channel, at the cut
+  std::map<ChanKey, std::vector<Msg>> u_sent;  // the shadow's placed sends
+  std::map<int, std::vector<int>> memo;        // 0 unknown, 1 yes, 2 no, 3 visiting
+
+  Readiness(const Loss &x_, const Plans &l) : x(x_), lists(l) {
+    for (auto &kv : *x.ch) pending[kv.first].assign(kv.second.begin(), kv.second.end());
+  }
+  void placed_send(const Instr &i) {
+    u_sent[ChanKey{x.u, i.peer, message_of(i).kind}].push_back(message_of(i));
+    memo.clear();
+  }
+  // j-th message (0-based, this step's remaining traffic) on channel c, if it
+  // can exist given the shadow's placed prefix
+  bool message(const ChanKey &c, size_t j, Msg *m) {
+    auto p = pending.find(c);
+    const size_t np = p == pending.end() ? 0 : p->second.size();
+    if (j < np) {
+      *m = p->second[j];
+      return true;
+    }
+    j -= np;
+    const int src = std::get<0>(c);
+    if (src == x.u) {
+      auto s = u_sent.find(c);
+      if (s == u_sent.end() || j >= s->second.size()) return false;
+      *m = s->second[j];
+      return true;
+    }
+    auto it = lists.find(src);
+    if (it == lists.end()) return false;
+    size_t seen = 0;
+    for (size_t i = 0; i < it->second.size(); ++i) {
+      const Instr &ins = it->second[i];
+      if (!is_send(ins.kind) || ins.peer != std::get<1>(c) ||
+          (int)message_of(ins).kind != std::get<2>(c))
+        continue;
+      if (seen++ == j) {
+        if (!can_run(src, (int)i)) return false;
+        *m = message_of(ins);
+        return true;
+      }
+    }
+    return false;
+  }
+  bool can_run(int n, int idx) {
+    if (idx < 0) return true;
+    auto &mv = memo[n];
+    if (mv.empty()) mv.assign(lists.at(n).size(), 0);
+    if (mv[idx] == 1) return true;
+    if (mv[idx] >= 2) return false;   // no, or a cycle
+    mv[idx] = 3;
+    bool ok = can_run(n, idx - 1);
+    const Instr &ins = lists.at(n)[idx];
+    if (ok && is_recv(ins.kind)) {
+      const ChanKey c{ins.peer, n, message_of(ins).kind};
+      size_t j = 0;   // ordinal of this receive on its channel
+      for (int i = 0; i < idx; ++i) {
+        const Instr &e = lists.at(n)[i];
+        if (is_recv(e.kind) && e.peer == ins.peer && message_of(e).kind == message_of(ins).kind) ++j;
+      }
+      Msg m;
+      ok = message(c, j, &m) && m == message_of(ins);
+    }
+    memo[n][idx] = ok ? 1 : 2;
+    return ok;
+  }
+};
+
+std::vector<Instr> merge_two(const Loss &x, const std::vector<Instr> &A,
+                             const std::vector<Instr> &B, std::set<Key> avail,
+                             const Plans &others) {
+  Readiness rd(x, others);
+  std::map<ChanKey, size_t> u_recvd;   // receives the shadow has placed, per channel
+  auto ready = [&](const Instr &i) {
+    if (is_recv(i.kind)) {
+      const ChanKey c{i.peer, x.u, message_of(i).kind};
+      Msg m;
+      return rd.message(c, u_recvd[c], &m) && m == message_of(i);
+    }
+    for (const Key &k : inputs_of(i, x.P))
       if (!avail.count(k)) return false;
     return true;
   };
-  // priority key: comm first (victim side first), then backward < forward <
-  // other, ascending micro-batch, victim side first.
-  auto prio = [&](const Instr &ins, int side) {
-    if (is_comm(ins.kind)) return std::make_tuple(0, side, 0, 0);
-    return std::make_tuple(1, compute_rank(ins.kind), ins.mb, side);
+  // side 0 = victim (B), 1 = shadow (A)
+  auto order = [&](const Instr &i, int side) {
+    return is_comm(i.kind) ? std::make_tuple(0, side, 0, 0)
+                           : std::make_tuple(1, step_kind_rank(i.kind), i.mb, side);
   };
+  std::vector<Instr> out;
+  size_t a = 0, b = 0;
   while (a < A.size() || b < B.size()) {
-    bool ra = a < A.size() && ready(A[a]);
-    bool rb = b < B.size() && ready(B[b]);
+    const bool ra = a < A.size() && ready(A[a]);
+    const bool rb = b < B.size() && ready(B[b]);
     if (!ra && !rb) throw PlanError("merge deadlock");
-    bool takeA;
-    if (ra && rb)
-      takeA = prio(A[a], 1) < prio(B[b], 0);
-    else
-      takeA = ra;
-    const Instr ins = takeA ? A[a++] : B[b++];
-    out.push_back(ins);
-    for (const Key &k : outputs_of(ins, P, M)) avail.insert(k);
-    if (is_recv(ins.kind)) {
-      och[ChanKey{ins.peer, u, message_of(ins).kind}].pop_front();
-    } else if (is_send(ins.kind)) {
-      const Msg m = message_of(ins);
-      och[ChanKey{u, ins.peer, m.kind}].push_back(m);
-      lockstep(others, opcs, och, nocap);
-    }
+    const bool pick_a = ra && (!rb || order(A[a], 1) < order(B[b], 0));
+    const Instr i = pick_a ? A[a++] : B[b++];
+    out.push_back(i);
+    for (const Key &k : outputs_of(i, x.P, x.M)) avail.insert(k);
+    if (is_recv(i.kind)) ++u_recvd[ChanKey{i.peer, x.u, message_of(i).kind}];
+    if (is_send(i.kind)) rd.placed_send(i);
   }
   return out;
 }
@@ -263,127 +472,66 @@ std::vector<Instr> merge(const std::vector<Instr> &A, const std::vector<Instr> &
 
 Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int, int> &pcs,
                      const Channels &ch, RecoveryInfo *info) {
-  const int u = (v - 1 + P) % P, w = (v + 1) % P;
-  const auto &pv = plans.at(v);
-  const int pcv = pcs.at(v);
-  bool commit = false;
-  for (int i = 0; i < pcv; ++i)
-    if (pv[i].kind == REPLICA_SEND) commit = true;
+  Loss x;
+  x.P = P;
+  x.M = M;
+  x.v = v;
+  x.u = (v - 1 + P) % P;
+  x.w = (v + 1) % P;
+  x.pcs = &pcs;
+  x.ch = &ch;
+  const std::vector<Instr> &pv = plans.at(v), &pu = plans.at(x.u);
+  for (int i = 0; i < pcs.at(v); ++i) x.commit = x.commit || pv[i].kind == REPLICA_SEND;
+  for (auto &kv : plans)
+    for (const Instr &i : kv.second) x.efeb = x.efeb || i.kind == BRC_BWD;
+  for (int i = 0; i < pcs.at(x.u); ++i)
+    if (pu[i].kind == FRC_FWD && pu[i].stage == v) x.frc_done.insert(pu[i].mb);
 
-  // Remaining RECVs from v are kept iff their message is already delivered
-  // (pending in the per-kind FIFO); otherwise rewritten by `redirect`.
-  auto delivered_filter = [&](int n, const std::vector<Instr> &seq, int redirect) {
-    std::map<int, std::deque<Msg>> qs;
-    for (int kd = 0; kd < 3; ++kd) {
-      auto it = ch.find(ChanKey{v, n, kd});
-      if (it != ch.end()) qs[kd] = it->second;
-    }
-    std::vector<Instr> out;
-    for (const Instr &ins : seq) {
-      if (is_recv(ins.kind) && ins.peer == v) {
-        const Msg m = message_of(ins);
-        auto &q = qs[m.kind];
-        if (!q.empty() && q.front() == m) {
-          q.pop_front();
-          out.push_back(ins);
-        } else if (redirect >= 0) {
-          Instr r = ins;
-          r.peer = redirect;
-          out.push_back(r);
-        }
-        continue;
-      }
-      out.push_back(ins);
-    }
-    return out;
-  };
-
-  // A: the shadow's remaining instructions
-  std::vector<Instr> A;
-  const auto &pu = plans.at(u);
-  for (size_t i = pcs.at(u); i < pu.size(); ++i) {
-    const Instr &ins = pu[i];
-    if (ins.kind == FRC_FWD && ins.stage == v) continue;   // becomes v's FWD in B
-    if (is_send(ins.kind) && ins.peer == v) continue;       // rule 2
-    if (ins.kind == APPLY && ins.stage == v && !commit) continue;
-    A.push_back(ins);
-  }
-  A = delivered_filter(u, A, -1);
-
-  // B: the victim's whole step, rewritten for the shadow
-  std::set<int> frc_done;
-  for (int i = 0; i < pcs.at(u); ++i)
-    if (pu[i].kind == FRC_FWD && pu[i].stage == v) frc_done.insert(pu[i].mb);
-  std::vector<Instr> B;
-  if (!commit) {
-    for (int idx = 0; idx < (int)pv.size(); ++idx) {
-      const Instr &ins = pv[idx];
-      const Kind kd = ins.kind;
-      if (kd == LOAD_INPUTS || kd == FRC_FWD || kd == REPLICA_SEND || kd == REPLICA_RECV) continue;
-      if (kd == APPLY && ins.stage != v) continue;
-      if (is_comm(kd) && ins.peer == u) continue;          // rule 2: local data edge
-      if (kd == FWD && frc_done.count(ins.mb)) continue;    // reuse retained FRC
-      if (kd == SEND_ACT && idx < pcv) continue;            // already delivered
-      B.push_back(ins);
-    }
-  }
-
-  Plans nw;
+  Plans out;
   for (auto &kv : plans) {
     const int n = kv.first;
     if (n == v) continue;
-    std::vector<Instr> seq;
-    if (n == u)
-      seq = A;
-    else
-      seq.assign(kv.second.begin() + pcs.at(n), kv.second.end());
-    if (n == w) {
-      std::vector<Instr> resend;
-      if (!commit && w != u) {
-        for (int i = 0; i < pcs.at(w); ++i) {
-          const Instr &x = plans.at(w)[i];
-          if (x.kind == SEND_GRAD && x.peer == v) resend.push_back({RESEND_GRAD, x.mb, u, x.stage});
-        }
+    std::vector<Instr> rest(kv.second.begin() + pcs.at(n), kv.second.end());
+    std::vector<Instr> seq = rewrite(x, n, rest);
+    if (n == x.w && n != x.u && !x.efeb && !x.commit) {
+      // Q3: the gradients w already gave v, again, now to the shadow
+      std::vector<Instr> again;
+      for (int i = 0; i < pcs.at(n); ++i) {
+        const Instr &e = kv.second[i];
+        if (e.kind == SEND_GRAD && e.peer == v) again.push_back({RESEND_GRAD, e.mb, x.u, e.stage});
       }
-      std::vector<Instr> s2;
-      for (Instr ins : seq) {
-        if (ins.kind == REPLICA_SEND && ins.peer == v) continue;
-        if (is_send(ins.kind) && ins.peer == v) ins.peer = u;
-        s2.push_back(ins);
-      }
-      if (w != u) {
-        auto f = delivered_filter(w, s2, u);
-        seq = resend;
-        seq.insert(seq.end(), f.begin(), f.end());
-      } else {
-        seq = s2;
-      }
+      seq.insert(seq.begin(), again.begin(), again.end());
     }
-    nw[n] = seq;
+    out[n] = seq;
   }
+  std::vector<Instr> B;
+  for (int i = 0; i < (int)pv.size(); ++i)
+    if (victim_work(x, pv[i], i)) B.push_back(pv[i]);
   std::set<Key> avail;
-  for (int i = 0; i < pcs.at(u); ++i)
+  for (int i = 0; i < pcs.at(x.u); ++i)
     for (const Key &k : outputs_of(pu[i], P, M)) avail.insert(k);
   Plans others;
-  for (auto &kv : nw)
-    if (kv.first != u) others[kv.first] = kv.second;
-  nw[u] = merge(nw[u], B, avail, P, M, u, others, ch);
+  for (auto &kv : out)
+    if (kv.first != x.u) others.insert(kv);
+  out[x.u] = merge_two(x, out[x.u], B, avail, others);
 
   if (info) {
     info->victim = v;
-    info->shadow = u;
-    info->successor = w;
-    info->commit = commit;
-    info->frc_done.assign(frc_done.begin(), frc_done.end());
+    info->shadow = x.u;
+    info->successor = x.w;
+    info->commit = x.commit;
+    info->frc_done.assign(x.frc_done.begin(), x.frc_done.end());
     info->brc_mb.clear();
-    for (const Instr &i : B)
-      if (i.kind == BWD) info->brc_mb.push_back(i.mb);
+    // the victim-stage backwards still to run: B's (EFLB / LFLB) or the
+    // shadow's pending eager BRCs (EFEB)
+    for (const Instr &i : x.efeb ? out[x.u] : B)
+      if ((i.kind == BWD || i.kind == BRC_BWD) && i.stage == v) info->brc_mb.push_back(i.mb);
     info->resend.clear();
-    if (nw.count(w))
-      for (const Instr &i : nw[w])
+    if (out.count(x.w))
+      for (const Instr &i : out[x.w])
         if (i.kind == RESEND_GRAD) info->resend.push_back(i.mb);
   }
-  return nw;
+  return out;
 }
 
 Plans failover_plans(int P, int M, int v, const Plans *base) {

@@ -23,7 +23,9 @@ namespace bb {
 
 enum Kind : int8_t {
   LOAD_INPUTS, FWD, FRC_FWD, BWD, SEND_ACT, RECV_ACT, SEND_GRAD, RECV_GRAD, RESEND_GRAD,
-  REPLICA_SEND, REPLICA_RECV, APPLY
+  REPLICA_SEND, REPLICA_RECV, APPLY,
+  BRC_BWD,                 // EFEB: eager redundant backward of the replica stage
+  SEND_DGRAD, RECV_DGRAD   // EFEB: a stage's input-gradient duplicated to the node two back
 };
 const char *kind_name(Kind k);
 bool is_send(Kind k);
@@ -37,7 +39,8 @@ struct Instr {
   int stage;  // logical stage the node acts for, -1 = none
 };
 
-enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2, MSG_STATE = 3 /* rejoin only */ };
+enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2, MSG_STATE = 3 /* rejoin only */,
+                        MSG_DGRAD = 4 /* EFEB duplicate gradients */ };
 struct Msg {
   MsgKind kind;
   int mb;
@@ -70,7 +73,7 @@ struct PlanError : std::exception {
 // Stage unit ranges [a, b] inclusive (units: 0 emb, 1..L blocks, L+1 head).
 std::vector<std::pair<int, int>> partition(int n_layer, int P, const int *layers_per_stage);
 
-// mode = bb_rc_mode (0 none, 1 EFLB, 2 LFLB); a bool converts to none / EFLB.
+// mode = bb_rc_mode (0 none, 1 EFLB, 2 LFLB, 3 EFEB); a bool converts to none / EFLB.
 std::vector<Instr> stage_plan(int s, int P, int M, int mode);
 Plans normal_plans(int P, int M, int mode);
 

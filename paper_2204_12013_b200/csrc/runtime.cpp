@@ -36,7 +36,12 @@ size_t al(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 void *dmalloc(size_t bytes) {
   void *p = nullptr;
   if (bytes == 0) bytes = ALIGN;
-  CK(cudaMalloc(&p, bytes));
+  const cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();   // an allocation failure is not sticky: clear it
+    throw RtError{e == cudaErrorMemoryAllocation ? BB_E_OOM : BB_E_CUDA,
+                  std::string("cudaMalloc: ") + cudaGetErrorString(e)};
+  }
   return p;
 }
 
@@ -156,6 +161,42 @@ static void layout_slots(const Dims &d, size_t tsz, StageInfo &si) {
 
 // ================================================================ helpers
 namespace {
+constexpr int kScratchSlot = -2;   // FRC beyond the retention budget
+char *slot_base(const Copy &cp, int slot) {
+  return slot == kScratchSlot ? cp.scratch : cp.sp.at(slot);
+}
+
+// Append n saved-set slots (one allocation) to a copy's pool.
+void grow_slots(Copy &cp, int n, size_t slot_bytes) {
+  if (n <= 0) return;
+  char *p = (char *)dmalloc(slot_bytes * n);
+  cp.chunks.push_back({p, slot_bytes * n});
+  for (int i = 0; i < n; ++i) {
+    cp.free_slots.insert(cp.free_slots.begin(), cp.nslots());
+    cp.sp.push_back(p + (size_t)i * slot_bytes);
+  }
+}
+
+void free_slots_all(Copy &cp);
+// A copy's pool as bb_init sizes it: the 1F1B stash of its own stage, or the
+// retention slots (+ scratch) of a replica.
+void reset_pool(Ctx &c, Copy &cp, bool scratch) {
+  const size_t sb = c.stages[cp.X].slot_bytes;
+  grow_slots(cp, cp.replica ? cp.retain : std::min(c.d.M, c.d.P - cp.X), sb);
+  if (scratch) {
+    cp.scratch = (char *)dmalloc(sb);
+    cp.chunks.push_back({cp.scratch, sb});
+  }
+}
+
+void free_slots_all(Copy &cp) {
+  for (auto &ch : cp.chunks) cudaFree(ch.first);
+  cp.chunks.clear();
+  cp.sp.clear();
+  cp.free_slots.clear();
+  cp.scratch = nullptr;
+}
+
 cudaEvent_t new_event(Node &nd) {
   if (nd.evnext == nd.evpool.size()) {
     cudaEvent_t e;
@@ -286,7 +327,7 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
                    const void *x_in, void *x_out, float *loss_rows, bool tg = false) {
   const Dims &d = c.d;
   const StageInfo &si = c.stages[X];
-  char *sl = cp.slots + (size_t)slot * si.slot_bytes;
+  char *sl = slot_base(cp, slot);
   const int R = d.R(), H = d.H, F = d.F;
   const bool b16 = c.bf16;
   const void *x = x_in;
@@ -355,10 +396,10 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
 // to its storage-type copy (a GEMM operand); GEMM outputs that only feed a
 // LayerNorm backward are written in fp32.
 void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStream_t s,
-                    const void *x_in, const void *dout, void *dx_out) {
+                    const void *x_in, const void *dout, void *dx_out, Node::Scratch &sc) {
   const Dims &d = c.d;
   const StageInfo &si = c.stages[X];
-  char *sl = cp.slots + (size_t)slot * si.slot_bytes;
+  char *sl = slot_base(cp, slot);
   const int R = d.R(), H = d.H, F = d.F;
   const bool b16 = c.bf16;
   const void *dy = dout;      // storage type
@@ -368,17 +409,16 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
     const UnitP &p = si.up[i];
     const UnitS &u = si.us[i];
     const void *x = i == 0 ? x_in : (const void *)(sl + si.us[i - 1].out);
-    void *dx = i == 0 ? dx_out : nd.sH[3 + flip];
-    float *dx32 = i == 0 ? nullptr : nd.s32[2 + flip];
+    void *dx = i == 0 ? dx_out : sc.sH[3 + flip];
+    float *dx32 = i == 0 ? nullptr : sc.s32[2 + flip];
     flip ^= 1;
     if (p.kind == 0) {
       Prof pf(c, nd, s, PC_EMB, 0);
       const int32_t *csr = nd.d_csr + (size_t)k * c.csr_stride;
-      const int U = c.csr_U[k];
-      CK(k::embed_bwd(b16, dy32 != nullptr, R, d.S, H, U, csr, csr + R, csr + 2 * R + 1,
-                      dy32 ? (const void *)dy32 : dy, pg(cp, p.tok), pg(cp, p.pos), s));
+      CK(k::embed_bwd(b16, dy32 != nullptr, R, d.S, H, csr, dy32 ? (const void *)dy32 : dy,
+                      pg(cp, p.tok), pg(cp, p.pos), s));
     } else if (p.kind == 2) {
-      float *dhf = nd.s32[0];
+      float *dhf = sc.s32[0];
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, d.V, sl + u.dlog, d.V, false, pw(c, cp, p.whead), H, true, k::EPI_STORE_F32,
             dhf, H, nullptr, nullptr, nullptr});
@@ -389,10 +429,10 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
       CK(k::layernorm_bwd_dx(b16, R, H, dhf, x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
                              pw(c, cp, p.lnfg), nullptr, nullptr, dx, dx32, s));
       CK(k::colreduce_ln(b16, R, H, dhf, x, (float *)(sl + u.meanf), (float *)(sl + u.rstdf),
-                         nd.s_part, pg(cp, p.lnfg), pg(cp, p.lnfb), s));
+                         sc.s_part, pg(cp, p.lnfg), pg(cp, p.lnfb), s));
     } else {
-      void *dpre = nd.sF, *dx1 = nd.sH[1], *dO = nd.sH[2], *dqkv = nd.s3;
-      float *dh2 = nd.s32[0], *dx1_32 = nd.s32[1], *dh1 = nd.s32[0];
+      void *dpre = sc.sF, *dx1 = sc.sH[1], *dO = sc.sH[2], *dqkv = sc.s3;
+      float *dh2 = sc.s32[0], *dx1_32 = sc.s32[1], *dh1 = sc.s32[0];
       gemm(c, nd, s, PC_GEMM_DX,
            {R, F, H, dy, H, false, pw(c, cp, p.w2), F, true, k::EPI_GELU_BWD, dpre, F, nullptr,
             nullptr, sl + u.pre});
@@ -402,7 +442,7 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
         CK(k::colreduce(b16, dy32 != nullptr, 0, R, H, dy32 ? (const void *)dy32 : dy, nullptr,
-                        nullptr, nullptr, nd.s_part, pg(cp, p.b2), s));
+                        nullptr, nullptr, sc.s_part, pg(cp, p.b2), s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, F, dpre, F, false, pw(c, cp, p.w1), H, true, k::EPI_STORE_F32, dh2, H, nullptr,
@@ -412,7 +452,7 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
             nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, false, 0, R, F, dpre, nullptr, nullptr, nullptr, nd.s_part,
+        CK(k::colreduce(b16, false, 0, R, F, dpre, nullptr, nullptr, nullptr, sc.s_part,
                         pg(cp, p.b1), s));
       }
       {
@@ -421,7 +461,7 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
                                (float *)(sl + u.rstd2), pw(c, cp, p.ln2g), dy32,
                                dy32 ? nullptr : dy, dx1, dx1_32, s));
         CK(k::colreduce_ln(b16, R, H, dh2, sl + u.x1, (float *)(sl + u.mean2),
-                           (float *)(sl + u.rstd2), nd.s_part, pg(cp, p.ln2g), pg(cp, p.ln2b), s));
+                           (float *)(sl + u.rstd2), sc.s_part, pg(cp, p.ln2g), pg(cp, p.ln2b), s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, H, dx1, H, false, pw(c, cp, p.wo), H, true, k::EPI_STORE, dO, H, nullptr,
@@ -431,13 +471,13 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
             nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, true, 0, R, H, dx1_32, nullptr, nullptr, nullptr, nd.s_part,
+        CK(k::colreduce(b16, true, 0, R, H, dx1_32, nullptr, nullptr, nullptr, sc.s_part,
                         pg(cp, p.bo), s));
       }
       {
         Prof pf(c, nd, s, PC_ATTN_BWD, 0);
         CK(k::attention_bwd(b16, d.mb, d.S, H, d.nh, d.causal, sl + u.qkv, sl + u.o,
-                            (float *)(sl + u.lse), dO, dqkv, nd.s_attn, s));
+                            (float *)(sl + u.lse), dO, dqkv, sc.s_attn, s));
       }
       gemm(c, nd, s, PC_GEMM_DX,
            {R, H, 3 * H, dqkv, 3 * H, false, pw(c, cp, p.wqkv), H, true, k::EPI_STORE_F32, dh1, H,
@@ -447,7 +487,7 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
             nullptr, nullptr, nullptr});
       {
         Prof pf(c, nd, s, PC_REDUCE, 0);
-        CK(k::colreduce(b16, false, 0, R, 3 * H, dqkv, nullptr, nullptr, nullptr, nd.s_part,
+        CK(k::colreduce(b16, false, 0, R, 3 * H, dqkv, nullptr, nullptr, nullptr, sc.s_part,
                         pg(cp, p.bqkv), s));
       }
       {
@@ -456,7 +496,7 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
                                (float *)(sl + u.rstd1), pw(c, cp, p.ln1g), dx1_32, nullptr, dx,
                                dx32, s));
         CK(k::colreduce_ln(b16, R, H, dh1, x, (float *)(sl + u.mean1),
-                           (float *)(sl + u.rstd1), nd.s_part, pg(cp, p.ln1g), pg(cp, p.ln1b), s));
+                           (float *)(sl + u.rstd1), sc.s_part, pg(cp, p.ln1g), pg(cp, p.ln1b), s));
       }
     }
     dy = dx;
@@ -482,6 +522,7 @@ Key payload_key(const Instr &ins) {
   switch (ins.kind) {
     case SEND_ACT: return {K_ACT, ins.stage + 1, ins.mb};
     case SEND_GRAD:
+    case SEND_DGRAD:
     case RESEND_GRAD: return {K_DACT, ins.stage, ins.mb};
     default: return {K_GRADSUM, ins.stage, 0};
   }
@@ -529,9 +570,8 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       if (!c.resident_step) {   // the last node fetches its inputs itself
         CK(cudaMemcpyAsync(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice, nd.main));
         CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice, nd.main));
-        CK(cudaMemcpyAsync(nd.d_csr, c.h_csr, (size_t)M * c.csr_stride * 4,
-                           cudaMemcpyHostToDevice, nd.main));
-        c.h2d += 2 * n * 4 + (size_t)M * c.csr_stride * 4;
+        if (nd.needs_csr) CK(k::embed_csr(M, d.R(), nd.d_tok, nd.d_csr, nd.main));
+        c.h2d += 2 * n * 4;
       }
       cudaEvent_t e = record(nd, nd.main);
       for (int j = 0; j < M; ++j) {
@@ -546,19 +586,19 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       const bool frc = ins.kind == FRC_FWD;
       cudaStream_t s = frc ? nd.frc : nd.main;
       const void *x_in = stage_input(c, nd, s, X, k);
-      // FRC retention budget (Q10): the first cp.retain FRC saved sets
-      // of a step stay in the pool for a lazy BRC; later ones run in the
-      // scratch slot and keep only their input and output (BRC recomputes).
+      // FRC retention budget (Q10): an FRC keeps its saved set for a
+      // lazy BRC while the replica's pool (cp.retain slots) has a free slot;
+      // beyond that it runs in the scratch slot and keeps only its input and
+      // output (the BRC recomputes the forward).
       bool keep = true;
       int slot;
-      if (frc && cp.retain_left <= 0) {
+      if (frc && cp.free_slots.empty() && cp.scratch) {
         keep = false;
-        slot = cp.nslots;
+        slot = kScratchSlot;
       } else {
         if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
         slot = cp.free_slots.back();
         cp.free_slots.pop_back();
-        if (frc) --cp.retain_left;
       }
       void *out = X < P - 1 ? arena_alloc(nd, msg_bytes(c, MSG_ACT, X)) : nullptr;
       {
@@ -576,19 +616,25 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         nd.store[{K_LOSS, k, 0}] = {cp.loss + k, e};
       return true;
     }
-    case BWD: {
+    case BWD:
+    case BRC_BWD: {
+      // BRC_BWD (EFEB): the replica stage's backward, eagerly, on the FRC
+      // stream with its own scratch; it accumulates the replica's gradient and
+      // its input-gradient stands in for the victim's only if none arrived
       Copy &cp = nd.copies.at(X);
+      const bool brc = ins.kind == BRC_BWD;
+      cudaStream_t s = brc ? nd.frc : nd.main;
       const Entry sv = need(nd, {K_SAVED, X, k});
-      wait_ev(nd.main, sv.ev);
+      wait_ev(s, sv.ev);
       const void *dout = nullptr;
       if (X < P - 1) {
         const Entry &e = need(nd, {K_DACT, X + 1, k});
-        wait_ev(nd.main, e.ev);
+        wait_ev(s, e.ev);
         dout = e.p;
       }
       const void *x_in = X == 0 ? nullptr : need(nd, {K_ACT, X, k}).p;
       void *dx = X > 0 ? arena_alloc(nd, msg_bytes(c, MSG_GRAD, X)) : nullptr;
-      TMark tm(c, nd, nd.main, 2);
+      TMark tm(c, nd, s, brc ? 1 : 2);
       int slot = sv.slot;
       if (slot < 0) {
         // an FRC saved set beyond the retention budget: recompute the forward
@@ -597,20 +643,21 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
         slot = cp.free_slots.back();
         cp.free_slots.pop_back();
-        const void *xi = stage_input(c, nd, nd.main, X, k);
+        const void *xi = stage_input(c, nd, s, X, k);
         void *tmp = X < P - 1 ? arena_alloc(nd, msg_bytes(c, MSG_ACT, X)) : nullptr;
-        stage_forward(c, nd, cp, X, k, slot, nd.main, xi, tmp, nd.s_loss_main);
+        stage_forward(c, nd, cp, X, k, slot, s, xi, tmp, brc ? nd.s_loss_frc : nd.s_loss_main);
         if (c.recovering) ++c.frc_recomputed;
       }
-      stage_backward(c, nd, cp, X, k, slot, nd.main, x_in, dout, dx);
-      cudaEvent_t e = record(nd, nd.main);
+      stage_backward(c, nd, cp, X, k, slot, s, x_in, dout, dx, nd.sc[brc ? 1 : 0]);
+      cudaEvent_t e = record(nd, s);
       cp.free_slots.push_back(slot);
-      if (X > 0) nd.store[{K_DACT, X, k}] = {dx, e};
+      if (X > 0 && (!brc || !nd.store.count({K_DACT, X, k}))) nd.store[{K_DACT, X, k}] = {dx, e};
       if (k == M - 1) nd.store[{K_GRADSUM, X, 0}] = {cp.grad, e};
       return true;
     }
     case SEND_ACT:
     case SEND_GRAD:
+    case SEND_DGRAD:
     case RESEND_GRAD:
     case REPLICA_SEND: {
       const Msg m = message_of(ins);
@@ -647,6 +694,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
     }
     case RECV_ACT:
     case RECV_GRAD:
+    case RECV_DGRAD:
     case REPLICA_RECV: {
       const Msg m = message_of(ins);
       const ChanKey ck{ins.peer, nd.n, (int)m.kind};
@@ -660,7 +708,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         XEdge &e = c.x.edges.at(std::make_tuple(ins.peer, nd.n, (int)m.kind));
         if (!c.x.available(e)) return false;       // the sender has not posted it yet
         const int slot = (int)(e.consumed % (uint64_t)e.cap);
-        ++e.consumed;
+        c.x.consume(e);
         char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
         // the sequence number is published after the payload landed: no wait
         if (m.kind == MSG_GRADSUM) {
@@ -673,7 +721,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       }
       if (ins.kind == RECV_ACT)
         nd.store[{K_ACT, X, k}] = got;
-      else if (ins.kind == RECV_GRAD)
+      else if (ins.kind == RECV_GRAD || ins.kind == RECV_DGRAD)
         nd.store[{K_DACT, X + 1, k}] = got;
       else
         nd.store[{K_GRADSUM, X, 0}] = {nd.copies.at(X).grad, got.ev};
@@ -810,12 +858,12 @@ void begin_step(Ctx &c) {
     nd.tnext = 0;
     for (auto &cc : nd.copies) {
       Copy &cp = cc.second;
-      cp.retain_left = cp.retain;
+
       // a loss nobody computes this step reads NaN (LFLB: the last stage
       // lost after its commit point took the only copy of its losses)
       if (cp.loss) CK(k::fill_nan(cp.loss, (size_t)c.d.M * 4, nd.main));
       cp.free_slots.clear();
-      for (int i = cp.nslots - 1; i >= 0; --i) cp.free_slots.push_back(i);
+      for (int i = cp.nslots() - 1; i >= 0; --i) cp.free_slots.push_back(i);
       CK(cudaMemsetAsync(cp.grad, 0, c.stages[cp.X].pcount * sizeof(float), nd.main));
     }
     CK(cudaEventRecord(nd.ev_begin, nd.main));
@@ -835,25 +883,6 @@ void stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
       throw RtError{BB_E_INVAL, "token or target id outside [0, vocab)"};
   std::memcpy(c.h_tok, tok, (size_t)d.M * R * 4);
   std::memcpy(c.h_tgt, tgt, (size_t)d.M * R * 4);
-  std::vector<int32_t> idx(R);
-  for (int k = 0; k < d.M; ++k) {
-    const int32_t *t = tok + (size_t)k * R;
-    int32_t *blob = c.h_csr + (size_t)k * c.csr_stride;
-    int32_t *uniq = blob, *offs = blob + R, *pos = blob + 2 * R + 1;
-    std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return t[a] < t[b]; });
-    int U = 0;
-    for (size_t i = 0; i < R; ++i) {
-      if (i == 0 || t[idx[i]] != t[idx[i - 1]]) {
-        uniq[U] = t[idx[i]];
-        offs[U] = (int)i;
-        ++U;
-      }
-      pos[i] = idx[i];
-    }
-    offs[U] = (int)R;
-    c.csr_U[k] = U;
-  }
 }
 
 float read_loss(Ctx &c) {
@@ -885,16 +914,19 @@ void poison_node(Ctx &c, Node &nd) {
     CK(k::fill_nan(cp.v, n * 4, nd.main));
     CK(k::fill_nan(cp.grad, n * 4, nd.main));
     if (c.bf16) CK(k::fill_nan(cp.work, n * 2, nd.main));
-    CK(k::fill_nan(cp.slots, c.stages[cp.X].slot_bytes * cp.nslots, nd.main));
+    for (auto &ch : cp.chunks) CK(k::fill_nan(ch.first, ch.second, nd.main));
     if (cp.loss) CK(k::fill_nan(cp.loss, (size_t)c.d.M * 4, nd.main));
   }
   CK(k::fill_nan(nd.arena, nd.arena_bytes, nd.main));
   for (auto &ch : nd.arena_spill) CK(k::fill_nan(ch.first, ch.second, nd.main));
   const size_t R = c.d.R(), H = c.d.H, F = c.d.F;
-  CK(k::fill_nan(nd.sF, R * F * c.act_bytes, nd.main));
-  CK(k::fill_nan(nd.s3, R * 3 * H * c.act_bytes, nd.main));
-  for (auto p : nd.sH) CK(k::fill_nan(p, R * H * c.act_bytes, nd.main));
-  for (auto p : nd.s32) CK(k::fill_nan(p, R * H * 4, nd.main));
+  for (auto &sc : nd.sc) {
+    if (!sc.sF) continue;
+    CK(k::fill_nan(sc.sF, R * F * c.act_bytes, nd.main));
+    CK(k::fill_nan(sc.s3, R * 3 * H * c.act_bytes, nd.main));
+    for (auto p : sc.sH) CK(k::fill_nan(p, R * H * c.act_bytes, nd.main));
+    for (auto p : sc.s32) CK(k::fill_nan(p, R * H * 4, nd.main));
+  }
   CK(cudaStreamSynchronize(nd.main));
   nd.alive = false;
 }
@@ -925,6 +957,166 @@ void finish_stats(Ctx &c, bb_step_stats *st, double t0) {
 }
 }  // namespace
 
+// ========================================================== fail-stop mode
+// opts.detect_ms > 0: a preempted rank goes silent; the others
+// notice that its heartbeat stopped, run to quiescence, agree on the cut from
+// the messages it delivered, and recover as in the injected mode.
+namespace {
+// Messages each cross-rank edge carries when `plans` run for `lim` (or all)
+// instructions: every rank derives the same counts from the same plans.
+void add_edge_sends(Ctx &c, const Plans &plans, const std::map<int, int> *lim) {
+  for (auto &kv : plans) {
+    const int n = kv.first;
+    size_t cap = kv.second.size();
+    if (lim && lim->count(n)) cap = std::min(cap, (size_t)lim->at(n));
+    for (size_t i = 0; i < cap; ++i) {
+      const Instr &ins = kv.second[i];
+      if (!is_send(ins.kind) || c.node_rank[ins.peer] == c.node_rank[n]) continue;
+      auto it = c.x.edges.find(std::make_tuple(n, ins.peer, (int)message_of(ins).kind));
+      if (it != c.x.edges.end()) ++c.edge_prior[it->second.index];
+    }
+  }
+}
+
+uint64_t hb_now(Ctx &c, int r) { return *c.x.rank_word(0, r); }
+
+// Ranks whose heartbeat has not moved for detect_ms are flagged dead in shm
+// (every survivor applies the same rule; the flag makes the verdict shared).
+void detect(Ctx &c, std::vector<uint64_t> &seen, std::vector<double> &since) {
+  const double t = now_ms();
+  for (int r = 0; r < c.o.world_size; ++r) {
+    if (r == c.o.world_rank || c.x.dead(r)) continue;
+    const uint64_t h = hb_now(c, r);
+    if (h != seen[r]) {
+      seen[r] = h;
+      since[r] = t;
+    } else if (t - since[r] > c.o.detect_ms) {
+      __atomic_store_n(const_cast<uint64_t *>(c.x.rank_word(1, r)), 1ull, __ATOMIC_RELEASE);
+      c.detect_ms_seen = t - since[r];
+    }
+  }
+}
+
+uint64_t inbound_sum(Ctx &c, int rank) {
+  uint64_t s = 0;
+  for (auto &kv : c.x.edges)
+    if (kv.second.dst_rank == rank) s += *c.x.counter(kv.second.index);
+  return s;
+}
+
+// Quiescent: every live rank is blocked on what it last saw arrive, and every
+// copy enqueued between live ranks has completed.
+bool quiescent(Ctx &c) {
+  for (int r = 0; r < c.o.world_size; ++r) {
+    if (c.x.dead(r)) continue;
+    const uint64_t b = *c.x.rank_word(2, r);
+    if (b == 0 || b - 1 != inbound_sum(c, r)) return false;
+  }
+  for (auto &kv : c.x.edges) {
+    const XEdge &e = kv.second;
+    if (c.x.dead(e.src_rank) || c.x.dead(e.dst_rank)) continue;
+    if (*c.x.intent(e.index) != *c.x.counter(e.index)) return false;
+  }
+  return true;
+}
+
+// Survivor side of a fail-stop step. Returns -1 when the step completed on
+// every live rank, else the dead node (the local lists stopped at quiescence;
+// pcs holds how far each local node got).
+int run_failstop(Ctx &c, std::map<int, size_t> &pc) {
+  const int W = c.o.world_size, me = c.o.world_rank;
+  std::vector<uint64_t> seen(W, 0);
+  std::vector<double> since(W, now_ms());
+  for (int r = 0; r < W; ++r) seen[r] = hb_now(c, r);
+  for (auto &kv : c.nodes)
+    if (kv.second.alive && c.plans.count(kv.first)) pc[kv.first] = 0;
+  auto flag = [&](int f) { return const_cast<uint64_t *>(c.x.rank_word(f, me)); };
+  bool arrived = false;
+  double stable_since = -1;
+  for (;;) {
+    bool progress = false, done = true;
+    for (auto &kv : pc) {
+      Node &nd = c.nodes.at(kv.first);
+      const auto &seq = c.plans.at(kv.first);
+      while (kv.second < seq.size() && exec(c, nd, seq[kv.second], Phase{})) {
+        ++kv.second;
+        progress = true;
+      }
+      if (kv.second < seq.size()) done = false;
+    }
+    if (done && !arrived) {
+      mark_end(c);
+      sync_all(c, true);
+      __atomic_store_n(flag(4), c.step_id, __ATOMIC_RELEASE);
+      arrived = true;
+    }
+    int dead = -1;   // a rank lost in THIS step (earlier victims stay flagged)
+    for (int r = 0; r < W; ++r)
+      if (c.x.dead(r) && std::find(c.victims.begin(), c.victims.end(), r) == c.victims.end())
+        dead = r;
+    if (arrived && dead < 0) {
+      bool all = true;
+      for (int r = 0; r < W; ++r)
+        if (!c.x.dead(r) && *c.x.rank_word(4, r) < c.step_id) all = false;
+      if (all) return -1;
+    }
+    if (progress) {
+      __atomic_store_n(flag(2), 0ull, __ATOMIC_RELEASE);
+      stable_since = -1;
+      continue;
+    }
+    if (dead < 0) {
+      detect(c, seen, since);
+      std::this_thread::yield();
+      continue;
+    }
+    // a rank is gone: block here, publish what we have seen, wait for the
+    // live ranks to settle
+    __atomic_store_n(flag(2), 1 + inbound_sum(c, me), __ATOMIC_RELEASE);
+    if (quiescent(c)) {
+      if (stable_since < 0) stable_since = now_ms();
+      if (now_ms() - stable_since > 20.0) {
+        if (!arrived) {
+          mark_end(c);
+          sync_all(c, true);
+        }
+        return dead;   // dead RANK; with one node per rank it is the node id
+      }
+    } else {
+      stable_since = -1;
+    }
+    std::this_thread::yield();
+  }
+}
+
+// The victim's instruction count as seen from outside: just past the last
+// send whose message was delivered (its later instructions left no trace).
+int observed_cut(Ctx &c, int v) {
+  std::map<int, uint64_t> ordinal;   // per edge index, sends of v so far this step
+  const auto &seq = c.plans.at(v);
+  int pi = 0;
+  for (size_t i = 0; i < seq.size(); ++i) {
+    const Instr &ins = seq[i];
+    if (!is_send(ins.kind)) continue;
+    auto it = c.x.edges.find(std::make_tuple(v, ins.peer, (int)message_of(ins).kind));
+    if (it == c.x.edges.end()) continue;
+    const int e = it->second.index;
+    const uint64_t delivered = *c.x.counter(e) - c.edge_prior[e];
+    if (ordinal[e]++ < delivered) pi = (int)i + 1;
+  }
+  return pi;
+}
+
+void heartbeat(Ctx *c) {
+  volatile uint64_t *h = c->x.rank_word(0, c->o.world_rank);
+  while (!c->hb_stop.load()) {
+    __atomic_add_fetch(const_cast<uint64_t *>(h), 1ull, __ATOMIC_RELEASE);
+    struct timespec ts{0, 5000000};
+    nanosleep(&ts, nullptr);
+  }
+}
+}  // namespace
+
 // ================================================================= API
 bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
   try {
@@ -936,14 +1128,16 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       throw RtError{BB_E_INVAL, "bad world rank/size"};
     if (m->n_layer < P) throw RtError{BB_E_INVAL, "n_layer < stages"};
     if (c.o.rc != BB_RC_NONE && P < 2) throw RtError{BB_E_INVAL, "RC needs stages >= 2"};
-    if (c.o.rc != BB_RC_NONE && c.o.rc != BB_RC_EFLB && c.o.rc != BB_RC_LFLB)
-      throw RtError{BB_E_UNSUPPORTED, "RC mode not built"};
+    if (c.o.rc < BB_RC_NONE || c.o.rc > BB_RC_EFEB) throw RtError{BB_E_INVAL, "unknown RC mode"};
     if (m->n_head <= 0 || m->d_model % m->n_head) throw RtError{BB_E_INVAL, "d_model % n_head"};
     if (m->d_model % 8 || m->d_ff % 8 || m->vocab % 8)
       throw RtError{BB_E_INVAL, "d_model, d_ff, vocab must be multiples of 8"};
     if (m->d_model / m->n_head != 64 && m->d_model / m->n_head != 32)
       throw RtError{BB_E_UNSUPPORTED, "attention kernels take head dim 64 (or 32)"};
     if (c.o.micro_batch < 1) throw RtError{BB_E_INVAL, "micro_batch < 1"};
+    if (c.o.detect_ms > 0 && (c.o.world_size != P || c.o.node_rank))
+      // a process death takes all its nodes: only one node per rank is recoverable
+      throw RtError{BB_E_INVAL, "fail-stop mode needs one node per rank (world_size == stages)"};
     if (c.o.prec == BB_PREC_BF16 && m->d_model < 64)
       // the transposed (MN-major) operands of dX / dW need >= 64 rows
       throw RtError{BB_E_UNSUPPORTED, "bf16 path needs d_model >= 64"};
@@ -977,11 +1171,9 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     for (int n = 0; n < P; ++n) c.node_device[n] = c.node_rank[n];
     CK(cudaSetDevice(c.o.device));
     const size_t R = c.d.R();
-    c.csr_stride = 3 * R + 1;
+    c.csr_stride = k::embed_csr_ints((int)R);
     CK(cudaMallocHost(&c.h_tok, (size_t)M * R * 4));
     CK(cudaMallocHost(&c.h_tgt, (size_t)M * R * 4));
-    CK(cudaMallocHost(&c.h_csr, (size_t)M * c.csr_stride * 4));
-    c.csr_U.assign(M, 0);
     int lo_prio = 0, hi_prio = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     const size_t act = R * c.d.H * c.act_bytes;
@@ -1015,8 +1207,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         cp.grad = (float *)dmalloc(si.pcount * 4);
         cp.work = c.bf16 ? dmalloc(si.pcount * 2) : (void *)cp.master;
         if (!h.second) {   // 1F1B stash of the node's own stage: min(M, P - X) in flight
-          cp.nslots = std::min(M, P - X);
-          cp.slots = (char *)dmalloc(si.slot_bytes * cp.nslots);
+          grow_slots(cp, std::min(M, P - X), si.slot_bytes);
         }
         if (X == P - 1) cp.loss = (float *)dmalloc(M * 4);
       }
@@ -1024,29 +1215,32 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.arena_bytes = (size_t)(6 * M + 8) * al(act);
       nd.arena = (char *)dmalloc(nd.arena_bytes);
       const size_t F = c.d.F, H = c.d.H;
-      nd.sF = dmalloc(R * F * c.act_bytes);
-      nd.s3 = dmalloc(R * 3 * H * c.act_bytes);
-      for (auto &p : nd.sH) p = dmalloc(R * H * c.act_bytes);
-      for (auto &p : nd.s32) p = (float *)dmalloc(R * H * 4);
-      {
+      for (int si = 0; si < (c.o.rc == BB_RC_EFEB ? 2 : 1); ++si) {
+        Node::Scratch &sc = nd.sc[si];
+        sc.sF = dmalloc(R * F * c.act_bytes);
+        sc.s3 = dmalloc(R * 3 * H * c.act_bytes);
+        for (auto &p : sc.sH) p = dmalloc(R * H * c.act_bytes);
+        for (auto &p : sc.s32) p = (float *)dmalloc(R * H * 4);
         const size_t pb = k::colreduce_partial_floats((int)R, (int)std::max(F, 3 * H)) * 4;
-        nd.s_part = (float *)dmalloc(pb);
-        CK(cudaMemset(nd.s_part, 0, pb));   // colreduce tickets start at zero
+        sc.s_part = (float *)dmalloc(pb);
+        CK(cudaMemset(sc.s_part, 0, pb));   // colreduce tickets start at zero
+        sc.s_attn = (float *)dmalloc(
+            k::attention_bwd_scratch_floats(c.d.mb, c.d.S, (int)H, c.d.nh) * 4);
       }
-      nd.s_attn = (float *)dmalloc(
-          k::attention_bwd_scratch_floats(c.d.mb, c.d.S, (int)H, c.d.nh) * 4);
       nd.s_loss_main = (float *)dmalloc(R * 4);
       nd.s_loss_frc = (float *)dmalloc(R * 4);
       nd.d_tok = (int32_t *)dmalloc((size_t)M * R * 4);
       nd.d_tgt = (int32_t *)dmalloc((size_t)M * R * 4);
       nd.d_csr = (int32_t *)dmalloc((size_t)M * c.csr_stride * 4);
+      // the embedding backward runs where a copy of stage 0 lives (its own
+      // node, the replica holder for a lazy BRC)
+      nd.needs_csr = n == 0 || (rc && n == P - 1);
     }
     // FRC retention pools of the replicas (Q10), allocated last so an
-    // automatic budget can take what the rest left free. A replica keeps
-    // `retain` FRC saved sets per step; its pool also has to serve as the 1F1B
-    // stash once promoted (min(M, P - X) in flight) plus one slot for a BRC
-    // re-forward, and one extra scratch slot (index nslots) for the FRCs
-    // beyond the budget.
+    // automatic budget can take what the rest left free: `retain` slots (the
+    // FRC saved sets kept per step) plus a scratch slot for the FRCs beyond
+    // them. A promoted replica's pool grows in bb_recover (the 1F1B stash of
+    // the victim's stage, min(M, P - X) in flight, plus one BRC re-forward).
     if (rc) {
       size_t budget = c.o.frc_retain_bytes;
       int nrep = 0;
@@ -1063,12 +1257,15 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           Copy &cp = cc.second;
           if (!cp.replica) continue;
           const StageInfo &si = c.stages[cp.X];
-          const bool frc = c.o.rc == BB_RC_EFLB;   // LFLB keeps no FRC saved sets
+          const bool frc = c.o.rc == BB_RC_EFLB || c.o.rc == BB_RC_EFEB;   // LFLB: no FRC
           const int full = !frc ? 0 : budget == 0 ? M
                                     : (int)std::min<size_t>(M, budget / si.slot_bytes);
           cp.retain = full;
-          cp.nslots = full >= M ? M : std::min(M, full + std::min(M, P - cp.X) + 1);
-          cp.slots = (char *)dmalloc(si.slot_bytes * (cp.nslots + (frc && full < M ? 1 : 0)));
+          grow_slots(cp, full, si.slot_bytes);
+          if (frc && full < M) {
+            cp.scratch = (char *)dmalloc(si.slot_bytes);
+            cp.chunks.push_back({cp.scratch, si.slot_bytes});
+          }
         }
     }
     // Cross-rank edges: one per (src node, dst node, kind) whose endpoints
@@ -1090,16 +1287,22 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         add(a, a - 1, MSG_GRADSUM);
         add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
         add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
+        if (c.o.rc == BB_RC_EFEB) add(a, a - 2, MSG_DGRAD);   // eager-BRC gradients
       }
       size_t gmax = 0;
       for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
       const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float),
-                                           3 * gmax * sizeof(float)};
-      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, 2};
+                                           3 * gmax * sizeof(float), act};
+      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, 2, 2 * M + 4};
       const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
-      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, wl, c.node_rank,
+      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, P, wl, c.node_rank,
                                         slot_bytes, caps, c.o.session_id, hi_prio);
       if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
+      c.edge_prior.assign(c.x.nedges, 0);
+      if (c.o.detect_ms > 0) {
+        c.failstop = true;
+        c.hb_thread = std::thread(heartbeat, &c);
+      }
     }
     CK(cudaDeviceSynchronize());
     return BB_OK;
@@ -1140,6 +1343,69 @@ bb_status rt_load_params(Ctx &c, const float *host, size_t n) {
   }
 }
 
+namespace {
+bb_status step_failstop(Ctx &c, bb_step_stats *st, double t0) {
+  if (c.self_dead) throw RtError{BB_E_STATE, "this rank was preempted"};
+  ++c.step_id;
+  begin_step(c);
+  if (c.armed) {
+    // this rank is the victim: run its first pi instructions, let what it sent
+    // land, then go silent (no heartbeat, no step-end arrival)
+    c.armed = false;
+    std::map<int, int> lim{{c.inj_v, c.inj_pi}};
+    run(c, c.plans, &lim, Phase{});
+    sync_all(c, true);
+    c.hb_stop = true;
+    if (c.hb_thread.joinable()) c.hb_thread.join();
+    c.self_dead = true;
+    c.nodes.at(c.inj_v).alive = false;
+    finish_stats(c, st, t0);
+    if (st) st->loss = NAN;
+    return BB_E_PREEMPTED;
+  }
+  std::map<int, size_t> pc;
+  const int dead = run_failstop(c, pc);
+  if (dead < 0) {   // every live rank finished the step
+    add_edge_sends(c, c.plans, nullptr);
+    ++c.steps_done;
+    ++c.adam_steps;
+    finish_stats(c, st, t0);
+    if (st) st->loss = read_loss(c);
+    return BB_OK;
+  }
+  // a node died: agree on the cut. Publish how far our nodes got, meet the
+  // other survivors, infer the victim's point from what it delivered.
+  for (auto &kv : pc) *const_cast<uint64_t *>(c.x.node_pc(kv.first)) = kv.second;
+  c.x.barrier();
+  const int v = dead;
+  if (c.o.rc == BB_RC_NONE || !recoverable(c.d.P, c.topo, c.victims, v)) {
+    c.fatal = true;
+    throw RtError{BB_E_FATAL, "lost node " + std::to_string(v) + " has no redundancy left"};
+  }
+  c.inj_v = v;
+  c.inj_pi = observed_cut(c, v);
+  try {
+    c.cut = cut(c.plans, v, c.inj_pi);
+  } catch (const PlanError &e) {
+    throw RtError{BB_E_STATE, e.msg};
+  }
+  for (auto &kv : c.cut.pcs) {
+    if (kv.first == v) continue;
+    const uint64_t got = *c.x.node_pc(kv.first);
+    if ((uint64_t)kv.second != got)
+      throw RtError{BB_E_STATE, "fail-stop: node " + std::to_string(kv.first) + " stopped at " +
+                                    std::to_string(got) + ", the cut says " +
+                                    std::to_string(kv.second)};
+  }
+  std::map<int, int> lim = c.cut.pcs;
+  add_edge_sends(c, c.plans, &lim);
+  c.interrupted = true;
+  finish_stats(c, st, t0);
+  if (st) st->loss = NAN;
+  return BB_E_PREEMPTED;
+}
+}  // namespace
+
 bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats *st) {
   const double t0 = now_ms();
   try {
@@ -1153,6 +1419,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
       c.resident = false;          // LOAD_INPUTS overwrites the device copies
     }
     c.resident_step = tok == nullptr;
+    if (c.failstop) return step_failstop(c, st, t0);
     c.x.barrier();   // every rank finished the previous step: receive slots are free
     // profile mode: park the serialised stream while the host enqueues the
     // step, so host launch latency never sits inside a kernel's event bracket
@@ -1217,7 +1484,8 @@ bb_status rt_stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
       Node &nd = kv.second;
       CK(cudaMemcpy(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(nd.d_csr, c.h_csr, (size_t)c.d.M * c.csr_stride * 4, cudaMemcpyHostToDevice));
+      if (nd.needs_csr) CK(k::embed_csr(c.d.M, c.d.R(), nd.d_tok, nd.d_csr, nd.main));
+      CK(cudaStreamSynchronize(nd.main));
     }
     c.resident = true;
     return BB_OK;
@@ -1242,6 +1510,10 @@ bb_status rt_preempt(Ctx &c, int stage, int at_instr) {
     // double-duty shadow, or lost its replica holder: P:464 consecutive nodes, Q18)
     c.err = "no redundancy left for the victim";
     return BB_E_FATAL;
+  }
+  if (c.failstop && !is_local(c, stage)) {
+    c.err = "fail-stop mode: arm the preemption on the victim's rank only";
+    return BB_E_INVAL;
   }
   if (at_instr < 0 || at_instr > (int)c.plans.at(stage).size()) {
     c.err = "injection point beyond the victim's list";
@@ -1272,8 +1544,24 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
       o << '\n' << dump_lines(c.continuation);
       c.recovery_text = o.str();
     }
-    // promote the replica on the shadow; the victim stops
-    if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = false;
+    // promote the replica on the shadow; the victim stops. The
+    // promoted pool must also hold the victim stage's 1F1B stash (min(M, P-v)
+    // in flight) and one BRC re-forward next to the retained FRC saved sets.
+    if (c.nodes.count(u)) {
+      Copy &cp = c.nodes.at(u).copies.at(v);
+      cp.replica = false;
+      const int need = std::min(M, cp.retain + std::min(M, P - v) + 1);
+      const size_t sb = c.stages[v].slot_bytes;
+      try {
+        grow_slots(cp, need - cp.nslots(), sb);
+      } catch (const RtError &e) {
+        // one GPU hosts the victim too (stages > GPUs): its pools are dead
+        // memory now, hand them to the shadow
+        if (e.st != BB_E_OOM || !c.nodes.count(v)) throw;
+        for (auto &cc : c.nodes.at(v).copies) free_slots_all(cc.second);
+        grow_slots(cp, need - cp.nslots(), sb);
+      }
+    }
     Phase ph;
     c.recovering = true;
     c.rec_stage = v;
@@ -1282,6 +1570,11 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
     run(c, c.continuation, nullptr, ph);
     c.recovering = false;
     sync_all(c, true);
+    if (c.failstop) {
+      add_edge_sends(c, c.continuation, nullptr);
+      // the victim's rank may now release its memory (our copies into it are done)
+      *const_cast<uint64_t *>(c.x.rank_word(3, c.o.world_rank)) = 1;
+    }
     c.history.push_back({c.plans, c.topo});
     c.topo = lose_node(P, c.topo, v);
     try {
@@ -1325,6 +1618,7 @@ bb_status rt_rejoin(Ctx &c) {
   try {
     if (c.fatal) return BB_E_FATAL;
     if (!c.failover || c.interrupted) throw RtError{BB_E_STATE, "rejoin needs a recovered failover pipeline"};
+    if (c.failstop) throw RtError{BB_E_UNSUPPORTED, "fail-stop mode: the lost process is gone"};
     CK(cudaSetDevice(c.o.device));
     c.x.barrier();
     // the most recent victim returns first (LIFO): the plans and topology
@@ -1372,7 +1666,7 @@ bb_status rt_rejoin(Ctx &c) {
             std::this_thread::yield();
           }
           const int slot = (int)(e.consumed % (uint64_t)e.cap);
-          ++e.consumed;
+          c.x.consume(e);
           const char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
           auto dp = parts(dc);
           for (int i = 0; i < 3; ++i)
@@ -1385,7 +1679,17 @@ bb_status rt_rejoin(Ctx &c) {
       }
       nd.alive = true;
     }
-    if (c.nodes.count(u)) c.nodes.at(u).copies.at(v).replica = true;
+    if (c.nodes.count(u)) {
+      // the shadow's copy is a replica again: back to its retention pool
+      Copy &cp = c.nodes.at(u).copies.at(v);
+      cp.replica = true;
+      const bool scr = cp.scratch != nullptr;
+      free_slots_all(cp);
+      reset_pool(c, cp, scr);
+    }
+    if (c.nodes.count(v))   // pools the returning node gave up under memory pressure
+      for (auto &cc : c.nodes.at(v).copies)
+        if (cc.second.chunks.empty()) reset_pool(c, cc.second, cc.second.replica && c.o.rc != BB_RC_LFLB && cc.second.retain < c.d.M);
     sync_all(c, true);
     c.plans = c.history.back().plans;
     c.topo = c.history.back().topo;
@@ -1534,6 +1838,20 @@ bb_status rt_kernel_stats(Ctx &c, bb_kernel_stat *out, int cap, int *n) {
 }
 
 void rt_destroy(Ctx &c) {
+  c.hb_stop = true;
+  if (c.hb_thread.joinable()) c.hb_thread.join();
+  if (c.self_dead && c.x.shm) {
+    // a silent victim keeps its memory mapped until every survivor finished
+    // the recovery that may still write into it (bounded wait)
+    const double t0 = now_ms();
+    for (;;) {
+      bool all = true;
+      for (int r = 0; r < c.o.world_size; ++r)
+        if (r != c.o.world_rank && !*c.x.rank_word(3, r) && !c.x.dead(r)) all = false;
+      if (all || now_ms() - t0 > 120000.0) break;
+      std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+  }
   cudaDeviceSynchronize();
   xport_destroy(c.x);
   for (auto &kv : c.nodes) {
@@ -1545,16 +1863,19 @@ void rt_destroy(Ctx &c) {
       cudaFree(cp.v);
       cudaFree(cp.grad);
       if (c.bf16) cudaFree(cp.work);
-      cudaFree(cp.slots);
+      free_slots_all(cp);
       if (cp.loss) cudaFree(cp.loss);
     }
     cudaFree(nd.arena);
-    cudaFree(nd.sF);
-    cudaFree(nd.s3);
-    for (auto p : nd.sH) cudaFree(p);
-    for (auto p : nd.s32) cudaFree(p);
-    cudaFree(nd.s_part);
-    cudaFree(nd.s_attn);
+    for (auto &sc : nd.sc) {
+      if (!sc.sF) continue;
+      cudaFree(sc.sF);
+      cudaFree(sc.s3);
+      for (auto p : sc.sH) cudaFree(p);
+      for (auto p : sc.s32) cudaFree(p);
+      cudaFree(sc.s_part);
+      cudaFree(sc.s_attn);
+    }
     cudaFree(nd.s_loss_main);
     cudaFree(nd.s_loss_frc);
     cudaFree(nd.d_tok);
@@ -1573,7 +1894,6 @@ void rt_destroy(Ctx &c) {
   if (c.serial) cudaStreamDestroy(c.serial);
   if (c.h_tok) cudaFreeHost(c.h_tok);
   if (c.h_tgt) cudaFreeHost(c.h_tgt);
-  if (c.h_csr) cudaFreeHost(c.h_csr);
 }
 
 }  // namespace bb

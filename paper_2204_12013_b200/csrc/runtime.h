@@ -12,7 +12,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <map>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -63,11 +65,15 @@ struct Copy {
   float *master = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
   void *work = nullptr;   // bf16 working copy (== master in fp32 check mode)
   int t = 0;
-  char *slots = nullptr;
-  int nslots = 0;              // pool slots; slot index nslots is the FRC scratch slot
+  // saved-set slot pool: slot i at sp[i]; the FRC scratch slot (saved sets
+  // beyond the retention budget) is `scratch`. Chunks are cudaMalloc'ed at
+  // init, grown when a replica is promoted, freed when the node dies.
+  std::vector<char *> sp;
+  char *scratch = nullptr;
+  std::vector<std::pair<char *, size_t>> chunks;
+  int nslots() const { return (int)sp.size(); }
   std::vector<int> free_slots;
   int retain = 0;              // FRC saved sets kept per step (replica; budget, Q10)
-  int retain_left = 0;         // ... still to keep in the current step
   float *loss = nullptr;  // [M] per-micro-batch losses (stage P-1 only)
 };
 
@@ -86,11 +92,17 @@ struct Node {
   std::vector<TRec> trec;
   std::vector<cudaEvent_t> tpool;
   size_t tnext = 0;
-  // backward scratch (main stream)
-  void *sF = nullptr, *s3 = nullptr, *sH[5] = {};
-  float *s32[4] = {};   // fp32 [R, H]: LN-input gradients and the residual-gradient chain
-  float *s_part = nullptr, *s_attn = nullptr, *s_loss_main = nullptr, *s_loss_frc = nullptr;
+  // backward scratch: [0] for the main stream, [1] for the FRC stream (EFEB's
+  // eager BRC); column-reduction tickets and attention partials are per
+  // stream because both streams may run backwards concurrently
+  struct Scratch {
+    void *sF = nullptr, *s3 = nullptr, *sH[5] = {};
+    float *s32[4] = {};   // fp32 [R, H]: LN-input gradients and the residual-gradient chain
+    float *s_part = nullptr, *s_attn = nullptr;
+  } sc[2];
+  float *s_loss_main = nullptr, *s_loss_frc = nullptr;
   int32_t *d_tok = nullptr, *d_tgt = nullptr, *d_csr = nullptr;
+  bool needs_csr = false;   // hosts a copy of stage 0: builds the token CSR on the device
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   std::vector<Instr> plan;
@@ -143,8 +155,7 @@ struct Ctx {
   RecoveryInfo rinfo;
   std::string recovery_text;
   // host staging
-  int32_t *h_tok = nullptr, *h_tgt = nullptr, *h_csr = nullptr;
-  std::vector<int> csr_U;
+  int32_t *h_tok = nullptr, *h_tgt = nullptr;
   size_t csr_stride = 0;
   long long steps_done = 0;     // completed steps (identical on every rank)
   long long adam_steps = 0;     // Adam steps since bb_load_params (= every copy's t)
@@ -158,6 +169,14 @@ struct Ctx {
   long long launches_at_start = 0;
   uint64_t h2d = 0, d2h = 0;
   float last_step_ms = 0.f;     // host wall time of the last bb_step call
+  // fail-stop mode (opts.detect_ms > 0)
+  bool failstop = false;
+  bool self_dead = false;       // this rank's node was preempted (silent from now on)
+  std::thread hb_thread;
+  std::atomic<bool> hb_stop{false};
+  std::vector<uint64_t> edge_prior;   // messages per cross-rank edge in completed steps
+  uint64_t step_id = 0;
+  double detect_ms_seen = 0;    // detection latency of the last loss (ms)
   bool recovering = false;      // inside bb_recover's continuation
   int rec_stage = -1;           // the victim's stage (recovery accounting)
   int frc_recomputed = 0;       // forwards recomputed by the current recovery

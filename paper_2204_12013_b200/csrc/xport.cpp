@@ -24,13 +24,24 @@ struct XErr {
   } while (0)
 }  // namespace
 
+int Xport::live() const {
+  int n = 0;
+  for (int r = 0; r < world; ++r) n += dead(r) ? 0 : 1;
+  return n;
+}
+
+void Xport::consume(XEdge &e) {
+  ++e.consumed;
+  __atomic_store_n(const_cast<uint64_t *>(consumed_ctr(e.index)), e.consumed, __ATOMIC_RELEASE);
+}
+
 // Header words: [0] magic, [1] barrier count, [2] barrier generation, [3] world.
 void Xport::barrier() {
   if (world <= 1) return;
   uint64_t *cnt = reinterpret_cast<uint64_t *>(shm) + 1;
   uint64_t *gen = cnt + 1;
   const uint64_t g = __atomic_load_n(gen, __ATOMIC_ACQUIRE);
-  if (__atomic_add_fetch(cnt, 1, __ATOMIC_ACQ_REL) == (uint64_t)world) {
+  if (__atomic_add_fetch(cnt, 1, __ATOMIC_ACQ_REL) == (uint64_t)live()) {
     __atomic_store_n(cnt, 0, __ATOMIC_RELAXED);
     __atomic_store_n(gen, g + 1, __ATOMIC_RELEASE);
   } else {
@@ -50,6 +61,7 @@ void CUDART_CB post_cb(void *arg) {
 cudaError_t Xport::post(XEdge &e) {
   XEdge::Post &p = e.posts[e.sent % (uint64_t)e.cap];
   ++e.sent;
+  __atomic_store_n(const_cast<uint64_t *>(intent(e.index)), e.sent, __ATOMIC_RELEASE);
   p.ctr = counter(e.index);
   p.value = e.sent;
   return cudaLaunchHostFunc(e.stream, post_cb, &p);
@@ -75,13 +87,14 @@ double now_s() {
 // appears. Header | per-edge sequence counters | per-rank heartbeats |
 // one IPC memory handle per rank. Ranks fill their own entries and meet at the shm barrier, so
 // several ranks may share one GPU (NCCL refuses that: duplicate device).
-std::string xport_init(Xport &x, int rank, int nranks,
+std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
                        const std::vector<int> &cap, const void *id_bytes, int hi_prio) {
   try {
     x.rank = rank;
     x.world = nranks;
+    x.nnodes = nnodes;
     // ---- edge table and receive-arena layout (identical on every rank)
     std::vector<size_t> arena_size(nranks, 0);
     int idx = 0, max_cap = 0;
@@ -109,9 +122,7 @@ std::string xport_init(Xport &x, int rank, int nranks,
     char name[64];
     std::snprintf(name, sizeof(name), "/bamboo_%016llx", (unsigned long long)h);
     x.shm_name = name;
-    const size_t off_cnt = 64, off_hb = off_cnt + 8 * (size_t)std::max(1, idx);
-    const size_t off_mh = off_hb + 8 * (size_t)nranks;
-    x.hb_off = off_hb;
+    const size_t off_mh = 64 + 8 * x.words();
     x.shm_bytes = off_mh + kHS * (size_t)nranks;
     auto hdr = [&]() { return static_cast<uint64_t *>(x.shm); };
     const double t0 = now_s();

@@ -44,22 +44,41 @@ struct XEdge {
   uint64_t consumed = 0;
 };
 
+// Shared segment layout (uint64 words after a 64-byte header): per edge the
+// published (completed) count, the intent count (bumped when a send is
+// enqueued) and the receiver's consumed count; per rank a heartbeat, a dead
+// flag, a blocked flag, a released flag and a step-end arrival stamp; per
+// node its published instruction counter (fail-stop cut agreement); then one
+// IPC memory handle per rank.
 struct Xport {
-  int rank = 0, world = 1;
+  int rank = 0, world = 1, nnodes = 0;
   char *arena = nullptr;
   size_t arena_bytes = 0;
   std::vector<char *> peer_arena;      // mapped receive arenas of other ranks
   std::map<std::tuple<int, int, int>, XEdge> edges;
   void *shm = nullptr;
-  size_t shm_bytes = 0, hb_off = 0;
+  size_t shm_bytes = 0;
   int nedges = 0;
   std::string shm_name;
 
-  volatile uint64_t *counter(int i) const {
-    return reinterpret_cast<volatile uint64_t *>(static_cast<char *>(shm) + 64 + 8 * i);
+  volatile uint64_t *word(size_t i) const {
+    return reinterpret_cast<volatile uint64_t *>(static_cast<char *>(shm) + 64) + i;
   }
-  // Host barrier over all ranks (shared memory, sense-reversing).
+  volatile uint64_t *counter(int e) const { return word(e); }
+  volatile uint64_t *intent(int e) const { return word(nedges + e); }
+  volatile uint64_t *consumed_ctr(int e) const { return word(2 * nedges + e); }
+  volatile uint64_t *rank_word(int field, int r) const {   // 0 hb 1 dead 2 blocked 3 released 4 arrive
+    return word(3 * nedges + field * world + r);
+  }
+  volatile uint64_t *node_pc(int n) const { return word(3 * nedges + 5 * world + n); }
+  size_t words() const { return 3 * nedges + 5 * world + nnodes; }
+
+  // Host barrier over the live ranks (shared memory, sense-reversing).
   void barrier();
+  int live() const;                    // ranks not flagged dead
+  bool dead(int r) const { return shm && *rank_word(1, r) != 0; }
+  // the receiver consumed one message of e (published for quiescence checks)
+  void consume(XEdge &e);
   // After the payload copy is enqueued on e.stream: enqueue the host callback
   // that publishes the new sequence number when the copy has completed.
   cudaError_t post(XEdge &e);
@@ -70,7 +89,7 @@ struct Xport {
 // (src, dst, kind); node_rank maps nodes to ranks. slot_bytes(kind) and
 // cap(kind) size the slots. id_bytes: the session id (>= 32 bytes, same on
 // every rank). Returns an error string (empty on success).
-std::string xport_init(Xport &x, int rank, int nranks,
+std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
                        const std::vector<int> &cap, const void *id_bytes, int hi_prio);

@@ -36,8 +36,10 @@ def main():
     ap.add_argument("--pi", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--out", required=True)
-    ap.add_argument("--rc", type=int, default=1)
+    ap.add_argument("--rc", default="eflb", help="none / eflb / lflb / efeb")
     ap.add_argument("--events", default="", help="t:v:pi or t:rejoin, comma separated")
+    ap.add_argument("--failstop", default="", help="t:v:pi — fail-stop loss armed on v's rank only")
+    ap.add_argument("--detect", type=int, default=0, help="bb_opts.detect_ms")
     a = ap.parse_args()
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -48,9 +50,9 @@ def main():
     P = a.stages or cfg.stages
     obj = [bb.session_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=bool(a.rc),
+    p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=a.rc,
                     prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=dev,
-                    session_id=obj[0])
+                    session_id=obj[0], detect_ms=a.detect)
     p.load_params(make_params(cfg.model))
     losses, rec = [], None
     events = {}
@@ -59,8 +61,15 @@ def main():
         events[int(f[0])] = "rejoin" if f[1] == "rejoin" else (int(f[1]), int(f[2]))
     if a.victim >= 0:
         events[0] = (a.victim, a.pi)
+    fs = tuple(int(x) for x in a.failstop.split(":")) if a.failstop else None
     for t in range(a.steps):
         tok, tgt = make_tokens(cfg, t)
+        if fs is not None and fs[0] == t and fs[1] == rank:   # one node per rank
+            p.preempt(fs[1], fs[2])
+            status, st = p.step(tok, tgt)
+            assert status == "preempted"
+            p.close()          # waits until the survivors released our memory
+            os._exit(0)        # the victim process is gone
         ev = events.get(t)
         if ev == "rejoin":
             p.rejoin()
@@ -72,10 +81,14 @@ def main():
             r = p.recover()
             loss, rec = r.loss, r
         losses.append(loss)
-        dist.barrier()
+        if fs is None:
+            dist.barrier()
     out = {"losses": np.array(losses, np.float32), "dump": np.array(p.schedule_dump())}
     if rec is not None:
         out["recovery_dump"] = np.array(p.recovery_dump())
+        out["rec"] = np.array([rec.victim, rec.shadow, rec.commit, rec.brc_mb, rec.frc_done_mb,
+                               rec.resent_mb, rec.frc_recomputed_mb], np.int64)
+        out["rec_loss"] = np.float32(rec.loss)
     for s in range(P):
         for what in ("params", "grads", "adam_m", "adam_v"):
             try:
@@ -84,8 +97,9 @@ def main():
                 pass
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), **out)
     p.close()
-    dist.barrier()
-    dist.destroy_process_group()
+    if fs is None:   # gloo cannot barrier over a dead rank
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

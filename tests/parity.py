@@ -67,20 +67,27 @@ def check_update(lay, lo, hi, p_gpu, p0, g_gpu, m0, v0, t, hp):
     """Adam update gate: the GPU's new parameters equal the oracle's Adam
     (oracle.model.adam_update, fp64, Q8) applied to the GPU's OWN
     gradient from the same (p0, m0, v0, t), up to the fp32 representation of
-    the result: |p_gpu - p_exp| <= 2 ulp_fp32(p_exp) + 1e-5 |p_exp - p0|.
+    the result: |p_gpu - p_exp| <= 2 ulp_fp32(p_exp) + 1e-5 |p_exp - p0|
+    + the fp32 rounding of m' under cancellation (8 ulp of its terms).
     A wrong lr / beta / bias correction, a missing or sign-flipped update
     fails by orders of magnitude. (Comparing the update against the oracle's
     gradient instead would gate an ill-conditioned quantity: where the
     gradient history is small the update amplifies the gradient's error.)"""
     from oracle.model import adam_update
     lr, b1, b2, eps = hp
-    p_exp, _, _ = adam_update(p0.astype(np.float64), g_gpu.astype(np.float64),
-                              m0.astype(np.float64), v0.astype(np.float64), t, lr, b1, b2, eps)
+    g64, m64 = g_gpu.astype(np.float64), m0.astype(np.float64)
+    p_exp, _, v_exp = adam_update(p0.astype(np.float64), g64, m64, v0.astype(np.float64), t,
+                                  lr, b1, b2, eps)
+    # fp32 rounding of m' = b1*m + (1-b1)*g is relative to the TERMS (they can
+    # cancel): ~8 ulp of their magnitude, carried through lr/(sqrt(v_hat)+eps)
+    bc1, bc2 = 1 - b1 ** t, 1 - b2 ** t
+    m_terms = (b1 * np.abs(m64) + (1 - b1) * np.abs(g64)) / bc1
+    m_round = lr * 1e-6 * m_terms / (np.sqrt(v_exp / bc2) + eps)
     errs = {}
     for name, a, b in tensor_slices(lay, lo, hi):
         pe = p_exp[a:b]
         bound = 2 * np.spacing(np.abs(pe).astype(np.float32)).astype(np.float64) + \
-            1e-5 * np.abs(pe - p0[a:b])
+            1e-5 * np.abs(pe - p0[a:b]) + m_round[a:b]
         d = np.abs(p_gpu[a:b] - pe)
         bad = d > bound
         assert not bad.any(), f"update {name}: {int(bad.sum())} elements, worst {d.max():.3e}"

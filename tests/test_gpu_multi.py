@@ -35,7 +35,8 @@ def run_mp(n, **kw):
         args += [f"--{k}", str(v)]
     r = subprocess.run(args, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    return [dict(np.load(os.path.join(d, f"rank{i}.npz"))) for i in range(n)]
+    return [dict(np.load(os.path.join(d, f"rank{i}.npz"))) if
+            os.path.exists(os.path.join(d, f"rank{i}.npz")) else None for i in range(n)]
 
 
 def merged(ranks, P, what):
@@ -106,3 +107,44 @@ def test_multi_gpu_rejoin_sequence_bitwise():
     assert [float(x) for x in ranks[-1]["losses"]] == [float(x) for x in losses]
     for w in state:
         assert np.array_equal(merged(ranks, 4, w), state[w]), w
+
+
+@pytest.mark.parametrize("n,victim,pi", [(2, 1, 9), (4, 2, 13), (4, 0, 7), (4, 3, 16)])
+def test_failstop_detection_and_recovery_bitwise(n, victim, pi):
+    """Fail-stop mode (bb_opts.detect_ms): bb_preempt is called on
+    the victim's rank ONLY; that process stops at instruction pi, goes silent
+    and exits. The survivors notice the stopped heartbeat after detect_ms,
+    run to quiescence, agree on the cut from the messages the victim had
+    delivered, recover without it, and keep training: the survivors' state
+    after the interrupted step and two failover steps equals the failure-free
+    single-process run bit for bit."""
+    import dataclasses
+    c = dataclasses.replace(get_config("C0"), stages=n)
+    ranks = run_mp(n, config="C0", stages=n, steps=3, failstop=f"1:{victim}:{pi}", detect=300)
+    assert ranks[victim] is None                      # the victim left no output
+    losses, state = single(c, 3)
+    live = [r for r in ranks if r is not None]
+    for t in range(3):   # whichever survivor hosted the last stage at step t
+        got = [float(r["losses"][t]) for r in live if not np.isnan(r["losses"][t])]
+        assert got and all(g == float(losses[t]) for g in got), (
+            t, got, losses[t], [(r.get("rec"), r["losses"], str(r.get("recovery_dump", ""))[:3000])
+                                for r in live])
+    for w in state:
+        assert np.array_equal(merged(live, n, w), state[w]), w
+
+
+@pytest.mark.parametrize("mode", ["efeb", "lflb"])
+def test_multi_process_modes_bitwise(mode):
+    """EFEB's duplicate gradients (node s -> s-2) and LFLB cross process
+    boundaries (3 ranks, one node each): a failure-free step and an injected
+    preemption of node 1 both equal the single-process failure-free run."""
+    import dataclasses
+    c = dataclasses.replace(get_config("C0"), stages=3)
+    losses, state = single(c, 2)
+    for extra in ({}, {"victim": 1, "pi": 12}):
+        ranks = run_mp(3, config="C0", stages=3, steps=2, rc=mode, **extra)
+        for t in range(2):
+            got = [float(r["losses"][t]) for r in ranks if not np.isnan(r["losses"][t])]
+            assert got and all(g == float(losses[t]) for g in got), (mode, extra, t)
+        for w in state:
+            assert np.array_equal(merged(ranks, 3, w), state[w]), (mode, extra, w)

@@ -450,7 +450,7 @@ def test_non_adjacent_second_preemption_bitwise():
     cfg = dataclasses.replace(get_config("C0"), model=dataclasses.replace(
         get_config("C0").model, n_layer=5), stages=5, microbatches=4)
     flat = make_params(cfg.model)
-    _, ref, _ = _run(cfg, flat, 6)
+    _, ref, _ = _run(cfg, flat, "bf16", 6)
     for v2 in (3, 4):
         n2 = len(opl.failover_plans(5, 4, 1)[v2])
         for pi2 in (0, n2 // 2, n2):
@@ -491,7 +491,7 @@ def test_lflb_recovery_bitwise_and_plans():
     recovery dumps equal the oracle's."""
     cfg = dataclasses.replace(get_config("C0"), stages=3, microbatches=4)
     flat = make_params(cfg.model)
-    _, ref, _ = _run(cfg, flat, 2)
+    _, ref, _ = _run(cfg, flat, "bf16", 2)
     p0 = _gpu(cfg, flat, "bf16", rc="lflb")
     assert p0.schedule_dump() == opl.dump(3, 4, "lflb", opl.partition(4, 3),
                                           opl.normal_plans(3, 4, "lflb"))
@@ -510,3 +510,60 @@ def test_lflb_recovery_bitwise_and_plans():
                 for w in sa:
                     assert np.array_equal(sa[w], sb[w]), (v, pi, w)
             p.close()
+
+
+def test_zipf_tokens_embedding_backward_matches_oracle():
+    """Zipf(1.1) tokens: many repeated ids per micro-batch
+    stress the device-built token CSR of the deterministic embedding
+    backward; gradients match the oracle and two runs are bit-identical."""
+    cfg = get_config("C0")
+    flat = make_params(cfg.model)
+    tok, tgt = make_tokens(cfg, 0, zipf=True)
+    assert len(np.unique(tok[:cfg.micro_batch])) < tok[:cfg.micro_batch].size * 3 // 4
+    outs = []
+    for _ in range(2):
+        p = _gpu(cfg, flat, "bf16")
+        ref = opipe.Pipeline(cfg, flat, rc=True, lr=LR)
+        s0 = _state0(ref)
+        _, st = p.step(tok, tgt)
+        _, rl = ref.step(tok, tgt)
+        _compare_step(cfg, p, ref, "bf16", st.loss, rl, s0)
+        outs.append(_flat_state(p, cfg.stages, "grads"))
+        p.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_efeb_eager_brc_bitwise(P):
+    """EFEB: every node runs its replica stage's backward
+    eagerly on the FRC stream from the duplicate gradient of node s+2, so the
+    replica's gradient and state equal the primary's with no replica sync.
+    Results equal the failure-free EFLB run bit for bit; a preemption at
+    several points of every victim recovers bit for bit with plans equal to
+    the oracle's, and the recovery reuses the eager BRC (few or no
+    re-computed backwards)."""
+    cfg = dataclasses.replace(get_config("C0"), stages=P, microbatches=4)
+    flat = make_params(cfg.model)
+    _, ref, _ = _run(cfg, flat, "bf16", 2)
+    p, got, _ = _run(cfg, flat, "bf16", 2, rc="efeb")
+    assert p.schedule_dump() == opl.dump(P, 4, "efeb", opl.partition(4, P),
+                                         opl.normal_plans(P, 4, "efeb"))
+    for s in range(P):
+        for w in STATES:
+            assert np.array_equal(p.read_state(s, w), p.read_state(s, w, replica=True)), (s, w)
+    p.close()
+    for (la, sa), (lb, sb) in zip(got, ref):
+        assert la == lb
+        for w in sa:
+            assert np.array_equal(sa[w], sb[w]), w
+    plans = opl.normal_plans(P, 4, "efeb")
+    for v in range(P):
+        n = len(plans[v])
+        for pi in sorted({1, n // 3, n // 2, (2 * n) // 3, n}):
+            q, got2, rec = _run(cfg, flat, "bf16", 2, inject=(0, v, pi), rc="efeb")
+            assert q.recovery_dump() == opl.recovery_dump(P, 4, v, pi, rc="efeb"), (v, pi)
+            for (la, sa), (lb, sb) in zip(got2, ref):
+                assert la == lb, (v, pi)
+                for w in sa:
+                    assert np.array_equal(sa[w], sb[w]), (v, pi, w)
+            q.close()

@@ -292,3 +292,41 @@ def test_lflb_injection_sweep_exact():
                             *[a.copy() for a in pp.full_adam()]))
             _same(res[0], ref[0])
             _same(res[1], ref[1])
+
+
+@pytest.mark.parametrize("P,M", [(2, 3), (3, 4), (4, 5), (5, 3)])
+def test_efeb_injection_sweep_exact(P, M):
+    """EFEB: eager FRC and eager BRC (from the duplicate
+    gradient of node s+2), no replica sync. The replica's own gradient and
+    state equal the primary's exactly every step; a preemption at every point
+    of every victim leaves the run exactly equal to the failure-free one, and
+    the following failover step too."""
+    cfg = tiny(P, M)
+    flat = make_params(cfg.model)
+    _, ref = _run(cfg, flat, 2)
+    plans = pl.normal_plans(P, M, "efeb")
+    assert not any(i.kind in (pl.REPLICA_SEND, pl.REPLICA_RECV) for q in plans.values() for i in q)
+    pp = pipeline.Pipeline(cfg, flat, rc="efeb")
+    for t in range(2):
+        pp.step(*make_tokens(cfg, t))
+        for s in range(P):
+            prim, rep = pp.nodes[s].copies[s], pp.nodes[(s - 1) % P].copies[s]
+            for key in ("p", "m", "v", "g"):
+                assert np.array_equal(prim[key], rep[key]), (t, s, key)
+    for v in range(P):
+        for pi in range(len(plans[v]) + 1):
+            pp = pipeline.Pipeline(cfg, flat, rc="efeb")
+            res = []
+            for t in range(2):
+                tok, tgt = make_tokens(cfg, t)
+                if t == 0:
+                    pp.preempt(v, pi)
+                status, val = pp.step(tok, tgt)
+                if status == "preempted":
+                    val, info = pp.recover()
+                    if v == P - 1 and np.isnan(val):
+                        val = ref[0][0]
+                res.append((val, pp.full_grads().copy(), pp.full_params().copy(),
+                            *[a.copy() for a in pp.full_adam()]))
+            _same(res[0], ref[0])
+            _same(res[1], ref[1])

@@ -103,3 +103,27 @@ def test_cpp_lflb_plans_match_oracle():
         pi = r.randint(0, n)
         assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc="lflb", micro_batch=1) == \
             pl.recovery_dump(P, M, v, pi, rc="lflb"), (P, M, v, pi)
+
+
+@pytest.mark.parametrize("mode", ["eflb", "lflb", "efeb"])
+def test_cpp_recovery_matches_oracle_every_point(mode):
+    """The library's recovery planner (plan.cpp, written from the rules with a
+    dependency-graph merge) and the oracle's (co-simulating merge) agree on
+    the cut and continuation text of every injection point of every victim,
+    for P = 2..5 and several M, in every RC mode; and on the static failover
+    plans."""
+    m = dict(n_layer=6, d_model=64, n_head=2, d_ff=256, vocab=128, seq_len=32, causal=1)
+    for P in (2, 3, 4, 5):
+        for M in (1, 2, 3, 6):
+            plans = pl.normal_plans(P, M, mode)
+            assert bbl.plan_dump(m, P, M, rc=mode, micro_batch=1) == \
+                pl.dump(P, M, mode, pl.partition(6, P), plans)
+            for v in range(P):
+                host, rep = pl.failover_topology(P, v)
+                assert bbl.plan_dump(m, P, M, victim=v, rc=mode, micro_batch=1) == \
+                    pl.dump(P, M, mode, pl.partition(6, P), pl.failover_plans(P, M, v, plans),
+                            host, rep, mode="failover", victim=v), (P, M, v)
+                for pi in range(len(plans[v]) + 1):
+                    assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc=mode,
+                                         micro_batch=1) == \
+                        pl.recovery_dump(P, M, v, pi, rc=mode), (P, M, v, pi)
