@@ -26,6 +26,21 @@ static bb_status copy_text(const std::string &s, char *buf, size_t cap, size_t *
   return (buf && cap < s.size() + 1) ? BB_E_INVAL : BB_OK;
 }
 
+// No C++ exception may cross the ABI: anything the runtime did not map to a
+// status (a library exception) becomes BB_E_STATE with its message.
+template <typename F>
+static bb_status guarded(void *ctx, F &&f) {
+  try {
+    return f();
+  } catch (const std::exception &e) {
+    static_cast<Ctx *>(ctx)->err = std::string("internal: ") + e.what();
+    return BB_E_STATE;
+  } catch (...) {
+    static_cast<Ctx *>(ctx)->err = "internal: unknown exception";
+    return BB_E_STATE;
+  }
+}
+
 extern "C" {
 
 void bb_default_opts(bb_opts *o) {
@@ -70,54 +85,54 @@ bb_status bb_init(const bb_model *m, int stages, int microbatches, const bb_opts
   *ctx_out = nullptr;
   Ctx *c = new (std::nothrow) Ctx();
   if (!c) return BB_E_OOM;
-  bb_status st = bb::rt_init(*c, m, stages, microbatches, o);
+  bb_status st = guarded(c, [&] { return bb::rt_init(*c, m, stages, microbatches, o); });
   *ctx_out = c;   // returned even on failure so bb_last_error works; caller destroys
   return st;
 }
 
 bb_status bb_load_params(void *ctx, const float *host, size_t n) {
   if (!ctx || !host) return BB_E_INVAL;
-  return bb::rt_load_params(*static_cast<Ctx *>(ctx), host, n);
+  return guarded(ctx, [&] { return bb::rt_load_params(*static_cast<Ctx *>(ctx), host, n); });
 }
 
 bb_status bb_step(void *ctx, const int32_t *tokens, const int32_t *targets, bb_step_stats *st) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_step(*static_cast<Ctx *>(ctx), tokens, targets, st);
+  return guarded(ctx, [&] { return bb::rt_step(*static_cast<Ctx *>(ctx), tokens, targets, st); });
 }
 
 bb_status bb_stage_inputs(void *ctx, const int32_t *tokens, const int32_t *targets) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_stage_inputs(*static_cast<Ctx *>(ctx), tokens, targets);
+  return guarded(ctx, [&] { return bb::rt_stage_inputs(*static_cast<Ctx *>(ctx), tokens, targets); });
 }
 
 bb_status bb_preempt(void *ctx, int stage, int at_instr) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_preempt(*static_cast<Ctx *>(ctx), stage, at_instr);
+  return guarded(ctx, [&] { return bb::rt_preempt(*static_cast<Ctx *>(ctx), stage, at_instr); });
 }
 
 bb_status bb_recover(void *ctx, bb_recovery_stats *r) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_recover(*static_cast<Ctx *>(ctx), r);
+  return guarded(ctx, [&] { return bb::rt_recover(*static_cast<Ctx *>(ctx), r); });
 }
 
 bb_status bb_rejoin(void *ctx) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_rejoin(*static_cast<Ctx *>(ctx));
+  return guarded(ctx, [&] { return bb::rt_rejoin(*static_cast<Ctx *>(ctx)); });
 }
 
 bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n) {
   if (!ctx || !host) return BB_E_INVAL;
-  return bb::rt_read_state(*static_cast<Ctx *>(ctx), stage, replica, what, host, n);
+  return guarded(ctx, [&] { return bb::rt_read_state(*static_cast<Ctx *>(ctx), stage, replica, what, host, n); });
 }
 
 bb_status bb_write_state(void *ctx, int stage, int what, const float *host, size_t n) {
   if (!ctx || !host) return BB_E_INVAL;
-  return bb::rt_write_state(*static_cast<Ctx *>(ctx), stage, what, host, n);
+  return guarded(ctx, [&] { return bb::rt_write_state(*static_cast<Ctx *>(ctx), stage, what, host, n); });
 }
 
 bb_status bb_node_stats(void *ctx, bb_node_stat *out, int cap, int *n) {
   if (!ctx) return BB_E_INVAL;
-  return bb::rt_node_stats(*static_cast<Ctx *>(ctx), out, cap, n);
+  return guarded(ctx, [&] { return bb::rt_node_stats(*static_cast<Ctx *>(ctx), out, cap, n); });
 }
 
 bb_status bb_stage_memory(void *ctx, int stage, size_t *slot_bytes, int *retained) {
@@ -241,16 +256,33 @@ bb_status bb_op_attention_fwd(int prec, int B, int S, int H, int nh, int causal,
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 
+// Op-level scratch (single-op entry points only: tests and kernel timing):
+// one growing device buffer per kind, kept for the process, so a timed call
+// measures the kernels, not an allocation. Not thread-safe (like the ops).
+static float *op_scratch(int kind, size_t bytes, bool zero, cudaStream_t s) {
+  static float *buf[2] = {nullptr, nullptr};
+  static size_t cap[2] = {0, 0};
+  if (bytes > cap[kind]) {
+    cudaStreamSynchronize(s);
+    if (buf[kind]) cudaFree(buf[kind]);
+    buf[kind] = nullptr;
+    cap[kind] = 0;
+    if (cudaMalloc((void **)&buf[kind], bytes) != cudaSuccess) return nullptr;
+    cap[kind] = bytes;
+    zero = true;
+  }
+  if (zero && cudaMemsetAsync(buf[kind], 0, cap[kind], s) != cudaSuccess) return nullptr;
+  return buf[kind];
+}
+
 bb_status bb_op_attention_bwd(int prec, int B, int S, int H, int nh, int causal, const void *qkv,
                               const void *o, const float *lse, const void *dout, void *dqkv,
                               void *stream) {
-  float *scratch = nullptr;
-  if (cudaMallocAsync((void **)&scratch, bb::k::attention_bwd_scratch_floats(B, S, H, nh) * 4,
-                      static_cast<cudaStream_t>(stream)) != cudaSuccess)
-    return BB_E_OOM;
+  float *scratch = op_scratch(0, bb::k::attention_bwd_scratch_floats(B, S, H, nh) * 4, false,
+                              static_cast<cudaStream_t>(stream));
+  if (!scratch) return BB_E_OOM;
   cudaError_t e = bb::k::attention_bwd(prec == BB_PREC_BF16, B, S, H, nh, causal != 0, qkv, o, lse,
                                        dout, dqkv, scratch, static_cast<cudaStream_t>(stream));
-  cudaFreeAsync(scratch, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported) return BB_E_UNSUPPORTED;
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
@@ -267,14 +299,12 @@ bb_status bb_op_layernorm_bwd(int prec, int R, int H, const float *dy, const voi
                               const float *dres, void *dx, float *dg, float *db, void *stream) {
   const bool b16 = prec == BB_PREC_BF16;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  float *part = nullptr;
-  const size_t pb = bb::k::colreduce_partial_floats(R, H) * 4;
-  if (cudaMallocAsync((void **)&part, pb, s) != cudaSuccess) return BB_E_OOM;
-  cudaError_t e = cudaMemsetAsync(part, 0, pb, s);
-  if (e == cudaSuccess)
-    e = bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, nullptr, dx, nullptr, s);
+  // colreduce tickets must start at zero; they reset themselves after a call
+  float *part = op_scratch(1, bb::k::colreduce_partial_floats(R, H) * 4, false, s);
+  if (!part) return BB_E_OOM;
+  cudaError_t e =
+      bb::k::layernorm_bwd_dx(b16, R, H, dy, x, mean, rstd, g, dres, nullptr, dx, nullptr, s);
   if (e == cudaSuccess) e = bb::k::colreduce_ln(b16, R, H, dy, x, mean, rstd, part, dg, db, s);
-  cudaFreeAsync(part, s);
   return e == cudaSuccess ? BB_OK : BB_E_CUDA;
 }
 

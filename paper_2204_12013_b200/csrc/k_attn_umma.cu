@@ -92,8 +92,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t o_done = bars + 8u * (4 + 4 * ST);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + L::BAR + 8 * (5 + 4 * ST));
 
-  // heaviest (causal: last) query blocks first
-  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // heaviest (causal: last) query blocks first, across the whole grid: the
+  // query block is the slowest grid dimension, so the block scheduler hands
+  // out every (head, sequence) of the last query block before any lighter one
+  // (longest-processing-time-first packing of the 2-per-SM slots)
+  const int qb = gridDim.z - 1 - blockIdx.z, h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = qb * BQ;
   const int row_base = b * S;            // first qkv row of this sequence
@@ -304,7 +307,7 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((S + BQ - 1) / BQ, nh, B);
+  dim3 grid(nh, B, (S + BQ - 1) / BQ);
   static const bool tr = [] {
     const char *e = std::getenv("BB_ATTN_DBG");
     return e && (std::atoi(e) & 8);

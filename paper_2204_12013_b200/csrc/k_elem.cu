@@ -249,6 +249,166 @@ __global__ void ln_bwd_vec_kernel(int R, int H, const float *__restrict__ dy,
   }
 }
 
+// bf16 LayerNorm, register-lean: a warp per row keeps the row as raw 16-byte
+// vectors (4 registers per 8 elements instead of 8 floats) and converts on
+// use, so 128-thread CTAs fit ~8 per SM and every row of a call is in flight
+// in one wave (the float-array version needed ~100-160 registers, two CTAs of
+// 256 per SM and two waves at C3: 1.6 TB/s). Same arithmetic, same order
+// (chunk, then element) as the generic kernels above: identical results.
+__device__ __forceinline__ void bf8(const uint4 &u, float f[8]) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float f[8]) {
+  uint4 u;
+  __nv_bfloat162 *h = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+constexpr int LNL_ROWS = 4;   // rows (warps) per 128-thread CTA
+template <int NC>
+__global__ void __launch_bounds__(128) ln_fwd_lean_kernel(int R, int H,
+                                                         const __nv_bfloat16 *__restrict__ x,
+                                                         const __nv_bfloat16 *__restrict__ g,
+                                                         const __nv_bfloat16 *__restrict__ b,
+                                                         __nv_bfloat16 *__restrict__ y,
+                                                         float *__restrict__ mean,
+                                                         float *__restrict__ rstd) {
+  const int row = blockIdx.x * LNL_ROWS + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const int nc = H / 8;
+  const uint4 *xr = reinterpret_cast<const uint4 *>(x + (size_t)row * H);
+  uint4 v[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    if (lane + 32 * c < nc) v[c] = xr[lane + 32 * c];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    if (lane + 32 * c < nc) {
+      float f[8];
+      bf8(v[c], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += f[i];
+    }
+  const float mu = warp_sum(s) / H;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    if (lane + 32 * c < nc) {
+      float f[8];
+      bf8(v[c], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = f[i] - mu;
+        q += d * d;
+      }
+    }
+  const float rs = rsqrtf(warp_sum(q) / H + LN_EPS);
+  uint4 *yr = reinterpret_cast<uint4 *>(y + (size_t)row * H);
+  const uint4 *g4 = reinterpret_cast<const uint4 *>(g), *b4 = reinterpret_cast<const uint4 *>(b);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      float f[8], gg[8], bb[8], o[8];
+      bf8(v[c], f);
+      bf8(g4[ch], gg);
+      bf8(b4[ch], bb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (f[i] - mu) * rs * gg[i] + bb[i];
+      yr[ch] = pack8(o);
+    }
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// The backward keeps only dy (fp32, needed twice) in registers and re-reads
+// x and g in its second pass (L1 hits: the warp read them a moment ago).
+template <int NC>
+__global__ void __launch_bounds__(128, 5) ln_bwd_lean_kernel(
+    int R, int H, const float *__restrict__ dy, const __nv_bfloat16 *__restrict__ x,
+    const float *__restrict__ mean, const float *__restrict__ rstd,
+    const __nv_bfloat16 *__restrict__ g, const float *__restrict__ dres32,
+    const __nv_bfloat16 *__restrict__ dresT, __nv_bfloat16 *__restrict__ dxT,
+    float *__restrict__ dx32) {
+  const int row = blockIdx.x * LNL_ROWS + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (row >= R) return;
+  const int nc = H / 8;
+  const size_t off = (size_t)row * H;
+  const float4 *dr = reinterpret_cast<const float4 *>(dy + off);
+  const uint4 *xr = reinterpret_cast<const uint4 *>(x + off);
+  const uint4 *g4 = reinterpret_cast<const uint4 *>(g);
+  float4 d[NC][2];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      d[c][0] = dr[2 * ch];
+      d[c][1] = dr[2 * ch + 1];
+    }
+  }
+  const float mu = mean[row], rs = rstd[row];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      float xx[8], gg[8];
+      const float dd[8] = {d[c][0].x, d[c][0].y, d[c][0].z, d[c][0].w,
+                           d[c][1].x, d[c][1].y, d[c][1].z, d[c][1].w};
+      bf8(__ldg(xr + ch), xx);
+      bf8(__ldg(g4 + ch), gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gd = dd[i] * gg[i], xh = (xx[i] - mu) * rs;
+        s1 += gd;
+        s2 += gd * xh;
+      }
+    }
+  }
+  const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ch = lane + 32 * c;
+    if (ch < nc) {
+      float xx[8], gg[8], r[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, o[8];
+      const float dd[8] = {d[c][0].x, d[c][0].y, d[c][0].z, d[c][0].w,
+                           d[c][1].x, d[c][1].y, d[c][1].z, d[c][1].w};
+      bf8(__ldg(xr + ch), xx);
+      bf8(__ldg(g4 + ch), gg);
+      if (dres32) {
+        const float4 a = reinterpret_cast<const float4 *>(dres32 + off)[2 * ch];
+        const float4 bq = reinterpret_cast<const float4 *>(dres32 + off)[2 * ch + 1];
+        r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+        r[4] = bq.x; r[5] = bq.y; r[6] = bq.z; r[7] = bq.w;
+      } else if (dresT) {
+        bf8(reinterpret_cast<const uint4 *>(dresT + off)[ch], r);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gd = dd[i] * gg[i], xh = (xx[i] - mu) * rs;
+        o[i] = rs * (gd - m1 - xh * m2) + r[i];
+      }
+      reinterpret_cast<uint4 *>(dxT + off)[ch] = pack8(o);
+      if (dx32) {
+        reinterpret_cast<float4 *>(dx32 + off)[2 * ch] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4 *>(dx32 + off)[2 * ch + 1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+}
+
 // Column reduction over 64-column x (row group) tiles: thread t owns the 8
 // columns 8 (t % 8).. of rows t / 8 + 32 k of its group; the 32 row groups are
 // added in a fixed order through shared memory and written to part[row
@@ -695,8 +855,46 @@ int grid_for(size_t n, int tpb) {
 template <typename T> static const T *cp(const void *p) { return reinterpret_cast<const T *>(p); }
 template <typename T> static T *mp(void *p) { return reinterpret_cast<T *>(p); }
 
+template <int NC>
+static void lean_fwd(int R, int H, const void *x, const void *g, const void *b, void *y,
+                     float *mean, float *rstd, cudaStream_t s) {
+  ln_fwd_lean_kernel<NC><<<(R + LNL_ROWS - 1) / LNL_ROWS, 128, 0, s>>>(
+      R, H, static_cast<const __nv_bfloat16 *>(x), static_cast<const __nv_bfloat16 *>(g),
+      static_cast<const __nv_bfloat16 *>(b), static_cast<__nv_bfloat16 *>(y), mean, rstd);
+}
+template <int NC>
+static void lean_bwd(int R, int H, const float *dy, const void *x, const float *mean,
+                     const float *rstd, const void *g, const float *dres32, const void *dresT,
+                     void *dxT, float *dx32, cudaStream_t s) {
+  ln_bwd_lean_kernel<NC><<<(R + LNL_ROWS - 1) / LNL_ROWS, 128, 0, s>>>(
+      R, H, dy, static_cast<const __nv_bfloat16 *>(x), mean, rstd,
+      static_cast<const __nv_bfloat16 *>(g), dres32, static_cast<const __nv_bfloat16 *>(dresT),
+      static_cast<__nv_bfloat16 *>(dxT), dx32);
+}
+#define BB_LEAN_SWITCH(F, NEED, ...)                               \
+  switch (NEED) {                                                  \
+    case 1: F<1>(__VA_ARGS__); break;                              \
+    case 2: F<2>(__VA_ARGS__); break;                              \
+    case 3: F<3>(__VA_ARGS__); break;                              \
+    case 4: F<4>(__VA_ARGS__); break;                              \
+    case 5: F<5>(__VA_ARGS__); break;                              \
+    case 6: F<6>(__VA_ARGS__); break;                              \
+    case 7: F<7>(__VA_ARGS__); break;                              \
+    default: F<8>(__VA_ARGS__); break;                             \
+  }
+
+static bool lean_ok(int H, const void *a, const void *b) {
+  return H % 8 == 0 && H <= 256 * LN_MAXC_MAX &&
+         ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
 cudaError_t layernorm_fwd(bool bf16, int R, int H, const void *x, const void *g, const void *b,
                           void *y, float *mean, float *rstd, cudaStream_t s) {
+  if (bf16 && lean_ok(H, x, y)) {
+    BB_LEAN_SWITCH(lean_fwd, (H / 8 + 31) / 32, R, H, x, g, b, y, mean, rstd, s);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const int grid = (R + 7) / 8;
   if (H % 8 == 0 && H <= 256 * LN_MAXC_MAX) {
 #define BB_LNF(T, C)                                                                          \
@@ -727,6 +925,12 @@ cudaError_t layernorm_bwd_dx(bool bf16, int R, int H, const float *dy, const voi
                              const float *mean, const float *rstd, const void *g,
                              const float *dres32, const void *dresT, void *dxT, float *dx32,
                              cudaStream_t s) {
+  if (bf16 && lean_ok(H, x, dxT)) {
+    BB_LEAN_SWITCH(lean_bwd, (H / 8 + 31) / 32, R, H, dy, x, mean, rstd, g, dres32, dresT, dxT,
+                   dx32, s);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const int grid = (R + 7) / 8;
   if (H % 8 == 0 && H <= 256 * LN_MAXC_MAX) {
 #define BB_LNB(T, C)                                                                          \

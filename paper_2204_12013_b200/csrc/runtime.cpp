@@ -510,6 +510,14 @@ void stage_backward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStre
 namespace {
 bool is_local(const Ctx &c, int n) { return c.node_rank[n] == c.o.world_rank; }
 
+XEdge &xedge(Ctx &c, int src, int dst, int kind) {
+  auto it = c.x.edges.find(std::make_tuple(src, dst, kind));
+  if (it == c.x.edges.end())
+    throw RtError{BB_E_STATE, "no transport edge " + std::to_string(src) + " -> " +
+                                  std::to_string(dst) + " kind " + std::to_string(kind)};
+  return it->second;
+}
+
 size_t msg_count(const Ctx &c, MsgKind kind, int stage) {
   if (kind == MSG_GRADSUM) return c.stages[stage].pcount;
   return (size_t)c.d.R() * c.d.H;
@@ -682,7 +690,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         CK(cudaMemcpyAsync(dp, pl.p, bytes, cudaMemcpyDeviceToDevice, nd.main));
         c.mail[ck].push_back({dp, record(nd, nd.main)});
       } else {
-        XEdge &e = c.x.edges.at(std::make_tuple(nd.n, ins.peer, (int)m.kind));
+        XEdge &e = xedge(c, nd.n, ins.peer, m.kind);
         const int slot = (int)(e.sent % (uint64_t)e.cap);
         if (bytes > e.slot_bytes) throw RtError{BB_E_STATE, "message larger than its slot"};
         char *dst = e.peer_base + e.recv_off + (size_t)slot * e.slot_bytes;
@@ -705,7 +713,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         got = it->second.front();
         it->second.pop_front();
       } else {
-        XEdge &e = c.x.edges.at(std::make_tuple(ins.peer, nd.n, (int)m.kind));
+        XEdge &e = xedge(c, ins.peer, nd.n, m.kind);
         if (!c.x.available(e)) return false;       // the sender has not posted it yet
         const int slot = (int)(e.consumed % (uint64_t)e.cap);
         c.x.consume(e);
@@ -892,6 +900,13 @@ float read_loss(Ctx &c) {
   Node &nd = c.nodes.at(n);
   Copy &cp = nd.copies.at(X);
   float *tmp = nd.s_loss_main;   // scratch: loss rows are no longer needed
+  if (std::getenv("BB_DEBUG_LOSS")) {
+    std::vector<float> h(c.d.M);
+    CK(cudaMemcpy(h.data(), cp.loss, c.d.M * 4, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[bb rank %d] loss of stage %d on node %d:", c.o.world_rank, X, n);
+    for (float f : h) std::fprintf(stderr, " %g", f);
+    std::fprintf(stderr, "\n");
+  }
   CK(k::sum_fixed(c.d.M, cp.loss, tmp, nd.main));
   float h = NAN;
   CK(cudaMemcpyAsync(&h, tmp, 4, cudaMemcpyDeviceToHost, nd.main));
@@ -1287,7 +1302,10 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
         add(a, a - 1, MSG_GRADSUM);
         add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
         add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
-        if (c.o.rc == BB_RC_EFEB) add(a, a - 2, MSG_DGRAD);   // eager-BRC gradients
+        if (c.o.rc == BB_RC_EFEB) {   // eager-BRC gradients; after a loss the shadow
+          add(a, a - 2, MSG_DGRAD);    // takes over the victim's (one hop back)
+          add(a, a - 1, MSG_DGRAD);
+        }
       }
       size_t gmax = 0;
       for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
@@ -1384,6 +1402,9 @@ bb_status step_failstop(Ctx &c, bb_step_stats *st, double t0) {
   }
   c.inj_v = v;
   c.inj_pi = observed_cut(c, v);
+  if (std::getenv("BB_DEBUG_LOSS"))
+    std::fprintf(stderr, "[bb rank %d] fail-stop: node %d lost, observed cut %d\n", c.o.world_rank, v,
+                 c.inj_pi);
   try {
     c.cut = cut(c.plans, v, c.inj_pi);
   } catch (const PlanError &e) {
@@ -1640,7 +1661,7 @@ bb_status rt_rejoin(Ctx &c) {
         for (int i = 0; i < 3; ++i)
           CK(cudaMemcpyAsync(dp[i], sp[i], n * 4, cudaMemcpyDeviceToDevice, src.main));
       } else {
-        XEdge &e = c.x.edges.at(std::make_tuple(from, v, (int)MSG_STATE));
+        XEdge &e = xedge(c, from, v, MSG_STATE);
         const int slot = (int)(e.sent % (uint64_t)e.cap);
         char *dst = e.peer_base + e.recv_off + (size_t)slot * e.slot_bytes;
         wait_ev(e.stream, record(src, src.main));
@@ -1659,7 +1680,7 @@ bb_status rt_rejoin(Ctx &c) {
         Copy &dc = nd.copies.at(X);
         const size_t n = c.stages[X].pcount;
         if (!is_local(c, from)) {
-          XEdge &e = c.x.edges.at(std::make_tuple(from, v, (int)MSG_STATE));
+          XEdge &e = xedge(c, from, v, MSG_STATE);
           const double t0 = now_ms();
           while (!c.x.available(e)) {
             if (now_ms() - t0 > 300000.0) throw RtError{BB_E_STATE, "rejoin: state never arrived"};
