@@ -271,6 +271,14 @@ bb_status bb_kernel_stats(void *ctx, bb_kernel_stat *out, int cap, int *n_classe
 bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb_opts *o,
                        int victim, int at_instr, char *buf, size_t cap, size_t *needed);
 
+/* Transport microbenchmark (no context): two processes (rank 0 / 1, device
+ * ordinals of their own, same 32-byte session id) ping-pong `iters`
+ * messages of `bytes` through the library's transport (copy-engine write into
+ * the peer's HBM, completion published by a host callback, receiver polling
+ * host shared memory). *us = mean one-way time per message, on rank 0. */
+bb_status bb_xport_pingpong(int rank, int world, int device, const void *session_id,
+                            size_t bytes, int iters, float *us);
+
 bb_status bb_last_error(const void *ctx, char *buf, size_t cap);
 void bb_destroy(void *ctx);
 

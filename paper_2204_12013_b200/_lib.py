@@ -26,6 +26,7 @@ EXPORTED = ["bb_default_opts", "bb_session_id", "bb_init", "bb_load_params", "bb
             "bb_stage_inputs", "bb_preempt", "bb_recover", "bb_rejoin", "bb_read_state",
             "bb_write_state", "bb_stage_memory", "bb_stage_params", "bb_schedule_dump", "bb_recovery_dump",
             "bb_kernel_stats", "bb_node_stats", "bb_plan_dump", "bb_last_error", "bb_destroy",
+            "bb_xport_pingpong",
             "bb_op_gemm", "bb_op_attention_fwd", "bb_op_attention_bwd", "bb_op_layernorm_fwd",
             "bb_op_layernorm_bwd", "bb_op_cross_entropy", "bb_op_adam"]
 
@@ -124,6 +125,9 @@ def lib():
         _lib.bb_default_opts.argtypes = [ctypes.POINTER(BBOpts)]
         _lib.bb_default_opts.restype = None
         _lib.bb_session_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        _lib.bb_xport_pingpong.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_float)]
         _lib.bb_plan_dump.argtypes = [ctypes.POINTER(BBModel), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(BBOpts), ctypes.c_int, ctypes.c_int,
                                       ctypes.c_char_p, ctypes.c_size_t,
@@ -192,6 +196,16 @@ def session_id():
     if st != BB_OK:
         raise BambooError(st, "bb_session_id")
     return buf.raw
+
+
+def xport_pingpong(rank, world, device, session, nbytes, iters):
+    """Mean one-way microseconds per message over the library's transport."""
+    us = ctypes.c_float(0)
+    buf = ctypes.create_string_buffer(bytes(session), len(session))
+    st = lib().bb_xport_pingpong(rank, world, device, buf, nbytes, iters, ctypes.byref(us))
+    if st != BB_OK:
+        raise BambooError(st, "bb_xport_pingpong")
+    return us.value
 
 
 def _text(fn, *args):

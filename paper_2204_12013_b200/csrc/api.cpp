@@ -4,6 +4,7 @@
 #include <unistd.h>
 #include <time.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -13,6 +14,7 @@
 #include "kernels.h"
 #include "plan.h"
 #include "runtime.h"
+#include "xport.h"
 
 using bb::Ctx;
 
@@ -228,6 +230,57 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
   } catch (const bb::PlanError &) {
     return BB_E_INVAL;
   }
+}
+
+// Transport microbenchmark: two ranks ping-pong `iters` messages of `bytes`
+// over the library's transport (copy into the peer's HBM + completion
+// published by a host callback, the receiver polls host shared memory);
+// *us = mean one-way latency per message (host wall time), measured on rank
+// 0. Compare with NCCL send/recv of the same bytes (tools/xport_vs_nccl.py).
+bb_status bb_xport_pingpong(int rank, int world, int device, const void *session_id,
+                            size_t bytes, int iters, float *us) {
+  if (world != 2 || rank < 0 || rank > 1 || !session_id || bytes == 0 || iters < 1)
+    return BB_E_INVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return BB_E_CUDA;
+  bb::Xport x;
+  const std::vector<std::tuple<int, int, int>> want{{0, 1, 0}, {1, 0, 0}};
+  const std::vector<int> node_rank{0, 1};
+  const std::string e = bb::xport_init(x, rank, 2, 2, want, node_rank, {bytes}, {2},
+                                       session_id, 0);
+  if (!e.empty()) return BB_E_CUDA;
+  void *src = nullptr;
+  if (cudaMalloc(&src, bytes) != cudaSuccess) return BB_E_OOM;
+  bb::XEdge &out = x.edges.at(std::make_tuple(rank, 1 - rank, 0));
+  bb::XEdge &in = x.edges.at(std::make_tuple(1 - rank, rank, 0));
+  auto send = [&] {
+    char *dst = out.peer_base + out.recv_off + (out.sent % out.cap) * out.slot_bytes;
+    cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, out.stream);
+    x.post(out);
+  };
+  auto recv = [&] {
+    while (!x.available(in)) {
+    }
+    x.consume(in);
+  };
+  x.barrier();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < iters; ++i) {
+    if (rank == 0) {
+      send();
+      recv();
+    } else {
+      recv();
+      send();
+    }
+  }
+  cudaStreamSynchronize(out.stream);
+  const double ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  x.barrier();
+  if (us) *us = (float)(1e3 * ms / (2.0 * iters));
+  cudaFree(src);
+  bb::xport_destroy(x);
+  return BB_OK;
 }
 
 // ------------------------------------------------------------ single ops

@@ -688,7 +688,10 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
       if (std::getenv("BB_DEBUG")) fprintf(stderr, "[bb] gemm pair slots %d\n", slots);
     }
   }
-  // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU.
+  // Split K for fp32-accumulating GEMMs (dW) whose tiles cannot fill the GPU
+  // twice over. (A general rounds-minimising split count was measured slower
+  // at C3: the serialised split adds cost more than the quantisation they
+  // remove, gemm_dw 476 -> 642 ms per serialised step.)
   const int nk = (g.K + BK - 1) / BK;
   int ksplit = 1;
   if (EPI == EPI_ACC_F32 && tiles * 2 <= slots && !g.tile_grid)
@@ -811,11 +814,12 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
     return te ? launch_bn<128, 1, true>(g, s) : launch_bn<128, 1, false>(g, s);
   if (force == 256) return te ? launch_bn<256, 1, true>(g, s) : launch_bn<256, 1, false>(g, s);
   if (force == 3 && te) return launch_bn<128, 2, true>(g, s);
-  // 256 x 192 pair tiles (K-major B only: 96 B rows per CTA, N % 192 == 0):
-  // fewer tile rounds at N = 768, but measured no faster than 256 x 256 there
-  // (18.7 vs 18.9 us, 44.4 vs 43.7 us), so only on request (BB_GEMM_TILE=pair192)
-  if (force == 4 && te && !g.b_mn && g.epi != EPI_ACC_F32 && g.N % 192 == 0)
-    return launch_bn<192, 2, true>(g, s);
+  // 256 x 192 pair tiles (K-major B only: 96 B rows per CTA; ragged N is
+  // clipped by TMA): fewer tile rounds at N = 768 / 1600, but per flop they
+  // move ~17% more operand bytes, and measured no faster (C1: 18.7 vs 18.9 us;
+  // C3 step: gemm_fwd 828 vs 819 ms serialised), so only on request
+  // (BB_GEMM_TILE=pair192).
+  if (force == 4 && te && !g.b_mn && g.epi != EPI_ACC_F32) return launch_bn<192, 2, true>(g, s);
   if (!te) return launch_bn<256, 1, false>(g, s);
   // fp32-accumulating dW with few output tiles: the serialised split-K chain
   // (up to 8 links of a few us each on pairs) costs more than the smaller

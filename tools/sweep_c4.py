@@ -58,7 +58,9 @@ def main():
     # to the next; every k starts and ends on the normal, fully protected plan)
     nid = bench.bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None
     pipe = bb.Pipeline(m, P, M, micro_batch=mb, rc=True, world_rank=rank, world_size=ws,
-                       device=local, session_id=nid)
+                       device=local, session_id=nid,
+                       layers_per_stage=bench.balanced_partition(m, P),
+                       frc_retain_bytes=bench.AUTO)   # bench.py's partition and FRC budget
     pipe.load_params(flat)
     pipe.stage_inputs(tok, tgt)
     for _ in range(3):
