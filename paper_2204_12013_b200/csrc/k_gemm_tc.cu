@@ -149,6 +149,15 @@ struct Smem {
 // is bound by L2 -> SM bandwidth, not by the tensor pipe.
 constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 
+// BB_GEMM_TRACE: progress words per CTA in mapped host memory (readable by
+// the host while a kernel hangs). Word 0 stage (1 running, 2 past the tile
+// loops, 3 done), 1/2 producer iteration before / after its empty wait,
+// 3/4 MMA iteration waiting for full / tile waiting for tempty, 5/6 epilogue
+// tile waiting for tfull / released.
+__device__ __forceinline__ void trw(unsigned *t, int i, unsigned v) {
+  if (t) *(volatile unsigned *)(t + i) = v;
+}
+
 template <int BN, int EPI, int CG, bool TE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -218,6 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  unsigned *tr = g.trace ? g.trace + 8 * blockIdx.x : nullptr;
+  if (threadIdx.x == 0) trw(tr, 0, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -230,8 +241,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nb0 = (tile % tiles_n) * BN + rank * BNH;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
-        auto n_boxes_a = [&](int r) { return max(0, min(BM / 64, (g.M - (m0 + (r - rank) * BM) + 63) / 64)); };
-        auto n_boxes_b = [&](int r) { return max(0, min(BNH / 64, (g.N - (nb0 + (r - rank) * BNH) + 63) / 64)); };
+        // Except: CTA 1 of a pair must load at least one box per K slab. Its
+        // bytes are what makes CTA 0's full barrier wait for it; with none
+        // (the corner tile of C3's 1600 x 1600 dW: rank 1 past both M and N)
+        // the MMA can run STAGES slabs ahead, CTA 1's empty barriers flip
+        // twice while its producer lags, its parity wait aliases and the
+        // kernel hangs (seen intermittently under concurrent kernels; the
+        // round-1 C4 stall). One fully out-of-bounds box (zeros) restores
+        // the lockstep.
+        auto n_boxes_a_raw = [&](int r) { return max(0, min(BM / 64, (g.M - (m0 + (r - rank) * BM) + 63) / 64)); };
+        auto n_boxes_b_raw = [&](int r) { return max(0, min(BNH / 64, (g.N - (nb0 + (r - rank) * BNH) + 63) / 64)); };
+        auto dummy = [&](int r) {
+          return CG == 2 && r == 1 && g.a_mn && g.b_mn && n_boxes_a_raw(r) == 0 &&
+                 n_boxes_b_raw(r) == 0;
+        };
+        auto n_boxes_a = [&](int r) { return n_boxes_a_raw(r) + (dummy(r) ? 1 : 0); };
+        auto n_boxes_b = [&](int r) { return n_boxes_b_raw(r); };
         auto bytes_of = [&](int r) {
           return (uint32_t)((g.a_mn ? n_boxes_a(r) * 64 * BK * 2 : L::A_BYTES) +
                             (g.b_mn ? n_boxes_b(r) * 64 * BK * 2 : L::B_BYTES));
@@ -245,7 +270,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
+          trw(tr, 1, it + 1);
           mbar_wait(empty_bar(s), ph ^ 1);
+          trw(tr, 2, it + 1);
           const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
           const int k0 = kb * BK;
           if (CG == 1) {
@@ -290,14 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int split = unit % ksplit;
         const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
         const int acc = j & 1;
+        trw(tr, 4, 0x80000000u | (unsigned)j);
         if (CG == 2) mbar_wait_cluster(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
         else mbar_wait(tempty_bar(acc), ((j >> 1) & 1) ^ 1);
+        trw(tr, 4, (unsigned)j);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % L::STAGES;
           const uint32_t ph = (it / L::STAGES) & 1;
+          trw(tr, 3, 0x80000000u | (unsigned)it);
           mbar_wait(full_bar(s), ph);
+          trw(tr, 3, (unsigned)it);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = base + s * L::STAGE, sb = sa + L::A_BYTES;
 #pragma unroll
@@ -355,7 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(in_bar(ew, bsel), 4096);
         tma_load_2d(box0 + bsel * 4096, &map_x, in_bar(ew, bsel), nw, mr);
       }
+      if (threadIdx.x == 64) trw(tr, 5, 0x80000000u | (unsigned)j);
       mbar_wait(tfull_bar(acc), (j >> 1) & 1);
+      if (threadIdx.x == 64) trw(tr, 5, (unsigned)j);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (ksplit > 1 && split > 0) {
         if (threadIdx.x == 64) {
@@ -481,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (CG == 2) mbar_arrive_cluster(my_tempty0 + 8u * acc);
         else mbar_arrive(tempty_bar(acc));
       }
+      if (threadIdx.x == 64) trw(tr, 6, (unsigned)j + 1);
       if (ksplit > 1) {
         if (lane == 0) {
           bulk_wait<0>();                                 // this warp's adds are performed
@@ -539,7 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) trw(tr, 0, 2);
   if (CG == 2) cluster_sync();          // peer MMAs / remote arrives done before dealloc / exit
+  if (threadIdx.x == 0) trw(tr, 0, 3);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (CG == 2)
@@ -630,8 +666,32 @@ int num_sms() {
   return sms;
 }
 
+// ---- BB_GEMM_TRACE ring: one region of per-CTA words per launch
+constexpr int kTrLaunches = 2048, kTrCtas = 296;
+struct TraceRec { int M, N, K, epi, bn, cg, grid, ksplit; };
+unsigned *g_tr_host = nullptr, *g_tr_dev = nullptr;
+TraceRec g_tr_rec[kTrLaunches];
+long long g_tr_n = 0;
+std::mutex g_tr_mu;
+unsigned *trace_slot(const Gemm &g, int bn, int cg, int grid, int ksplit) {
+  static const bool on = std::getenv("BB_GEMM_TRACE") != nullptr;
+  if (!on || grid > kTrCtas) return nullptr;
+  std::lock_guard<std::mutex> lk(g_tr_mu);
+  if (!g_tr_host) {
+    const size_t bytes = (size_t)kTrLaunches * kTrCtas * 8 * 4;
+    if (cudaHostAlloc(&g_tr_host, bytes, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+    std::memset(g_tr_host, 0, bytes);
+    if (cudaHostGetDevicePointer(&g_tr_dev, g_tr_host, 0) != cudaSuccess) return nullptr;
+  }
+  const int i = (int)(g_tr_n++ % kTrLaunches);
+  std::memset(g_tr_host + (size_t)i * kTrCtas * 8, 0, kTrCtas * 8 * 4);
+  g_tr_rec[i] = {g.M, g.N, g.K, g.epi, bn, cg, grid, ksplit};
+  return g_tr_dev + (size_t)i * kTrCtas * 8;
+}
+
 template <int BN, int EPI, int CG, bool TE>
-cudaError_t launch(const Gemm &g, cudaStream_t s) {
+cudaError_t launch(const Gemm &g_in, cudaStream_t s) {
+  Gemm g = g_in;
   constexpr int BNH = BN / CG;
   using L = Smem<BN, CG, TE>;
   auto kern = gemm_tc_kernel<BN, EPI, CG, TE>;
@@ -711,6 +771,7 @@ cudaError_t launch(const Gemm &g, cudaStream_t s) {
   int pids = units < slots || g.tile_grid ? units : slots;
   if (ksplit > 1) pids = std::max(ksplit, pids / ksplit * ksplit);
   const int grid = pids * CG;
+  g.trace = trace_slot(g, BN, CG, grid, ksplit);
   if (CG == 1) {
     kern<<<grid, kThreads, L::BYTES, s>>>(ma, mb, mc, mx, g, ksplit, flags, epoch);
   } else {
@@ -828,6 +889,27 @@ cudaError_t gemm_tc(const Gemm &g, cudaStream_t s) {
       (long)((g.M + 255) / 256) * ((g.N + 255) / 256) < 16)
     return launch_bn<128, 1, true>(g, s);
   return launch_bn<256, 2, true>(g, s);
+}
+
+void gemm_trace_dump() {
+  if (!g_tr_host) return;
+  const long long n = g_tr_n;
+  for (long long l = std::max(0LL, n - kTrLaunches); l < n; ++l) {
+    const int i = (int)(l % kTrLaunches);
+    const TraceRec &r = g_tr_rec[i];
+    const unsigned *t = g_tr_host + (size_t)i * kTrCtas * 8;
+    int unfinished = 0;
+    for (int c = 0; c < r.grid; ++c) unfinished += t[8 * c] != 3;
+    if (!unfinished) continue;
+    std::fprintf(stderr, "[bb] gemm launch %lld: %dx%dx%d epi %d BN %d CG %d grid %d ksplit %d, "
+                 "%d CTAs unfinished:\n", l, r.M, r.N, r.K, r.epi, r.bn, r.cg, r.grid, r.ksplit,
+                 unfinished);
+    for (int c = 0; c < r.grid; ++c)
+      if (t[8 * c] != 3)
+        std::fprintf(stderr, "  cta %d: st %u prod %u/%u mma full %x tempty %x epi tfull %x rel %u\n", c,
+                     t[8 * c], t[8 * c + 1], t[8 * c + 2], t[8 * c + 3], t[8 * c + 4], t[8 * c + 5],
+                     t[8 * c + 6]);
+  }
 }
 
 }  // namespace k

@@ -24,7 +24,11 @@ struct Gemm {
   void *aux;          // pre-activation [M][ldc] storage type (BIAS_GELU out, GELU_BWD in)
   bool tile_grid = false;   // one CTA (pair) per output tile instead of a persistent grid:
                             // a low-priority stream's GEMM then yields SMs tile by tile
+  unsigned *trace = nullptr;   // BB_GEMM_TRACE: per-CTA progress words (mapped host memory)
 };
+
+// BB_GEMM_TRACE diagnostics: print the GEMM launches that have not finished.
+void gemm_trace_dump();
 
 // Profile mode: park a stream for `ns` of device time (not counted as a launch).
 cudaError_t gpu_sleep(unsigned long long ns, cudaStream_t s);

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <sstream>
 #include <thread>
+#include <unistd.h>
 
 namespace bb {
 
@@ -161,6 +162,7 @@ static void layout_slots(const Dims &d, size_t tsz, StageInfo &si) {
 
 // ================================================================ helpers
 namespace {
+double watch_s();
 constexpr int kScratchSlot = -2;   // FRC beyond the retention budget
 char *slot_base(const Copy &cp, int slot) {
   return slot == kScratchSlot ? cp.scratch : cp.sp.at(slot);
@@ -279,7 +281,7 @@ struct Prof {
   double work;
   cudaEvent_t a = nullptr;
   Prof(Ctx &c_, Node &nd_, cudaStream_t s_, int cls_, double w) : c(c_), nd(nd_), s(s_), cls(cls_), work(w) {
-    if (c.o.profile) a = take();
+    if (c.o.profile || watch_s() > 0) a = take();
     if (a) CK(cudaEventRecord(a, s));
   }
   cudaEvent_t take() {
@@ -294,7 +296,7 @@ struct Prof {
     if (!a) return;
     cudaEvent_t b = take();
     CK(cudaEventRecord(b, s));
-    c.prof.push_back({cls, a, b, work});
+    c.prof.push_back({cls, a, b, work, nd.n});
   }
 };
 
@@ -548,6 +550,16 @@ bool debug_on() {
   }();
   return on;
 }
+// BB_WATCH=<seconds>: record an event pair per instruction and, when a step's
+// device work has not finished after that long, report the first unfinished
+// instruction of every node and fail the call (diagnosing device hangs).
+double watch_s() {
+  static const double w = [] {
+    const char *e = std::getenv("BB_WATCH");
+    return e ? std::atof(e) : 0.0;
+  }();
+  return w;
+}
 
 // Input of stage X for micro-batch k on node nd: tokens (X = 0) or the
 // activation key; makes stream s wait for it (and for the targets on the last
@@ -766,7 +778,7 @@ void run(Ctx &c, const Plans &lists, const std::map<int, int> *lim, const Phase 
       if (lim) cap = std::min(cap, (size_t)lim->at(kv.first));
       if (kv.second < cap) pending = true;
       while (kv.second < cap && exec(c, nd, seq[kv.second], ph)) {
-        if (debug_on()) {
+        if (debug_on() || watch_s() > 0) {
           cudaEvent_t e1, e2;
           cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
           cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
@@ -831,8 +843,92 @@ void debug_wait(Ctx &c, bool comm_too) {
   }
 }
 
+void watch_wait(Ctx &c, bool comm_too) {
+  const double t0 = now_ms();
+  for (;;) {
+    bool busy = false;
+    for (auto &kv : c.nodes)
+      busy = busy || cudaStreamQuery(kv.second.main) == cudaErrorNotReady ||
+             cudaStreamQuery(kv.second.frc) == cudaErrorNotReady;
+    if (comm_too)
+      for (auto &kv : c.x.edges)
+        busy = busy || (kv.second.stream && cudaStreamQuery(kv.second.stream) == cudaErrorNotReady);
+    if (!busy) return;
+    if (now_ms() - t0 > 1000.0 * watch_s()) {
+      std::ostringstream o;
+      o << "device watchdog: step not finished after " << watch_s() << " s;";
+      std::map<int, int> shown;
+      for (auto &d : c.dbg) {
+        const bool m_ok = cudaEventQuery(d.main_ev) == cudaSuccess;
+        const bool f_ok = cudaEventQuery(d.frc_ev) == cudaSuccess;
+        if ((!m_ok || !f_ok) && shown[d.node]++ < 1)
+          o << " node " << d.node << " #" << d.idx << ' ' << kind_name(d.ins.kind) << " mb "
+            << d.ins.mb << " stage " << d.ins.stage << (m_ok ? "" : " main") << (f_ok ? "" : " frc")
+            << ';';
+      }
+      std::fprintf(stderr, "[bb rank %d] %s\n", c.o.world_rank, o.str().c_str());
+      throw RtError{BB_E_CUDA, o.str()};
+    }
+    struct timespec ts{0, 20000000};
+    nanosleep(&ts, nullptr);
+  }
+}
+
+// BB_WATCH: a host thread that outlives a hung device. When the launch
+// queue fills behind a kernel that never finishes, the step's own thread
+// blocks inside a launch and cannot report; this one prints the first
+// unfinished instruction of every node and ends the process.
+struct Watchdog {
+  Ctx &c;
+  std::atomic<bool> done{false};
+  std::thread t;
+  explicit Watchdog(Ctx &c_) : c(c_) {
+    if (watch_s() <= 0) return;
+    t = std::thread([this] {
+      const double t0 = now_ms();
+      while (!done.load()) {
+        if (now_ms() - t0 > 1000.0 * (watch_s() + 5.0)) {
+          std::fprintf(stderr, "[bb rank %d] watchdog: step running for %.0f s; first unfinished:",
+                       c.o.world_rank, (now_ms() - t0) / 1000.0);
+          std::map<int, int> shown;
+          for (size_t i = 0; i < c.dbg.size(); ++i) {
+            const DbgRec d = c.dbg[i];
+            const bool m_ok = cudaEventQuery(d.main_ev) == cudaSuccess;
+            const bool f_ok = cudaEventQuery(d.frc_ev) == cudaSuccess;
+            if ((!m_ok || !f_ok) && shown[d.node]++ < 1)
+              std::fprintf(stderr, " node %d #%d %s mb %d stage %d%s%s;", d.node, d.idx,
+                           kind_name(d.ins.kind), d.ins.mb, d.ins.stage, m_ok ? "" : " main",
+                           f_ok ? "" : " frc");
+          }
+          std::fprintf(stderr, " (%zu instructions issued); first unfinished kernel:",
+                       c.dbg.size());
+          std::map<int, int> shown_k;
+          for (size_t i = 0; i < c.prof.size(); ++i) {
+            const ProfRec r = c.prof[i];
+            if (cudaEventQuery(r.b) != cudaSuccess && shown_k[r.node]++ < 1)
+              std::fprintf(stderr, " node %d %s %.3g flop (%s, record %zu);", r.node,
+                           prof_names[r.cls], r.work,
+                           cudaEventQuery(r.a) == cudaSuccess ? "started" : "not started", i);
+          }
+          std::fprintf(stderr, "\n");
+          k::gemm_trace_dump();
+          std::fflush(stderr);
+          _exit(3);
+        }
+        struct timespec ts{0, 50000000};
+        nanosleep(&ts, nullptr);
+      }
+    });
+  }
+  ~Watchdog() {
+    done = true;
+    if (t.joinable()) t.join();
+  }
+};
+
 void sync_all(Ctx &c, bool comm_too) {
   if (debug_on()) debug_wait(c, comm_too);
+  else if (watch_s() > 0) watch_wait(c, comm_too);
   for (auto &kv : c.nodes) {
     CK(cudaStreamSynchronize(kv.second.main));
     CK(cudaStreamSynchronize(kv.second.frc));
@@ -843,6 +939,15 @@ void sync_all(Ctx &c, bool comm_too) {
 }
 
 void begin_step(Ctx &c) {
+  for (auto &d : c.dbg) {
+    cudaEventDestroy(d.main_ev);
+    cudaEventDestroy(d.frc_ev);
+  }
+  c.dbg.clear();
+  if (watch_s() > 0) {   // the watchdog thread reads these: no reallocation
+    c.dbg.reserve(1 << 18);
+    c.prof.reserve(1 << 20);
+  }
   c.mail.clear();
   c.prof.clear();
   c.prof_next = 0;
@@ -1440,6 +1545,7 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
       c.resident = false;          // LOAD_INPUTS overwrites the device copies
     }
     c.resident_step = tok == nullptr;
+    Watchdog dog(c);
     if (c.failstop) return step_failstop(c, st, t0);
     c.x.barrier();   // every rank finished the previous step: receive slots are free
     // profile mode: park the serialised stream while the host enqueues the

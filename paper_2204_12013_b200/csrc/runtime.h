@@ -115,6 +115,7 @@ struct ProfRec {
   int cls;
   cudaEvent_t a, b;
   double work;
+  int node;
 };
 
 struct DbgRec {
