@@ -730,13 +730,16 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         const int slot = (int)(e.consumed % (uint64_t)e.cap);
         c.x.consume(e);
         char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
-        // the sequence number is published after the payload landed: no wait
+        // event mode: consumers wait on the sender's event for this slot;
+        // callback mode: the number was published after the payload landed
+        cudaEvent_t ready = c.x.wait_event(e, slot);
         if (m.kind == MSG_GRADSUM) {
+          wait_ev(nd.main, ready);
           CK(cudaMemcpyAsync(nd.copies.at(X).grad, src, msg_bytes(c, m.kind, m.stage),
                              cudaMemcpyDeviceToDevice, nd.main));
           got = {nd.copies.at(X).grad, record(nd, nd.main)};
         } else {
-          got = {src, nullptr};
+          got = {src, ready};
         }
       }
       if (ins.kind == RECV_ACT)
@@ -1356,6 +1359,45 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       // node, the replica holder for a lazy BRC)
       nd.needs_csr = n == 0 || (rc && n == P - 1);
     }
+    // Cross-rank edges, set up before the retention pools so an automatic
+    // FRC budget sees the receive arenas: one per (src node, dst node, kind) whose endpoints
+    // live on different ranks; ring distance <= 2 covers the normal pipeline,
+    // the replica ring and the failover skip edges (xport.h).
+    if (c.o.world_size > 1) {
+      if (!c.o.session_id) throw RtError{BB_E_INVAL, "session_id required for world_size > 1"};
+      std::set<std::tuple<int, int, int>> want;
+      auto add = [&](int a, int b, int kind) {
+        a = (a % P + P) % P;
+        b = (b % P + P) % P;
+        if (a != b && c.node_rank[a] != c.node_rank[b]) want.insert({a, b, kind});
+      };
+      for (int a = 0; a < P; ++a) {
+        if (a < P - 1) add(a, a + 1, MSG_ACT);
+        add(a, a + 2, MSG_ACT);
+        if (a > 0) add(a, a - 1, MSG_GRAD);
+        add(a, a - 2, MSG_GRAD);
+        add(a, a - 1, MSG_GRADSUM);
+        add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
+        add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
+        if (c.o.rc == BB_RC_EFEB) {   // eager-BRC gradients; after a loss the shadow
+          add(a, a - 2, MSG_DGRAD);    // takes over the victim's (one hop back)
+          add(a, a - 1, MSG_DGRAD);
+        }
+      }
+      size_t gmax = 0;
+      for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
+      const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float),
+                                           3 * gmax * sizeof(float), act};
+      // rejoin sends one state message per edge, two when P == 2 (the shadow
+      // and the successor are the same node)
+      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, P == 2 ? 2 : 1, 2 * M + 4};
+      const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
+      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, P, wl, c.node_rank,
+                                        slot_bytes, caps, c.o.session_id, hi_prio,
+                                        /*callback_mode=*/c.o.detect_ms > 0);
+      if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
+      c.edge_prior.assign(c.x.nedges, 0);
+    }
     // FRC retention pools of the replicas (Q10), allocated last so an
     // automatic budget can take what the rest left free: `retain` slots (the
     // FRC saved sets kept per step) plus a scratch slot for the FRCs beyond
@@ -1388,44 +1430,9 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           }
         }
     }
-    // Cross-rank edges: one per (src node, dst node, kind) whose endpoints
-    // live on different ranks; ring distance <= 2 covers the normal pipeline,
-    // the replica ring and the failover skip edges (xport.h).
-    if (c.o.world_size > 1) {
-      if (!c.o.session_id) throw RtError{BB_E_INVAL, "session_id required for world_size > 1"};
-      std::set<std::tuple<int, int, int>> want;
-      auto add = [&](int a, int b, int kind) {
-        a = (a % P + P) % P;
-        b = (b % P + P) % P;
-        if (a != b && c.node_rank[a] != c.node_rank[b]) want.insert({a, b, kind});
-      };
-      for (int a = 0; a < P; ++a) {
-        if (a < P - 1) add(a, a + 1, MSG_ACT);
-        add(a, a + 2, MSG_ACT);
-        if (a > 0) add(a, a - 1, MSG_GRAD);
-        add(a, a - 2, MSG_GRAD);
-        add(a, a - 1, MSG_GRADSUM);
-        add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
-        add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
-        if (c.o.rc == BB_RC_EFEB) {   // eager-BRC gradients; after a loss the shadow
-          add(a, a - 2, MSG_DGRAD);    // takes over the victim's (one hop back)
-          add(a, a - 1, MSG_DGRAD);
-        }
-      }
-      size_t gmax = 0;
-      for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
-      const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float),
-                                           3 * gmax * sizeof(float), act};
-      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, 2, 2 * M + 4};
-      const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
-      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, P, wl, c.node_rank,
-                                        slot_bytes, caps, c.o.session_id, hi_prio);
-      if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
-      c.edge_prior.assign(c.x.nedges, 0);
-      if (c.o.detect_ms > 0) {
-        c.failstop = true;
-        c.hb_thread = std::thread(heartbeat, &c);
-      }
+    if (c.o.world_size > 1 && c.o.detect_ms > 0) {
+      c.failstop = true;
+      c.hb_thread = std::thread(heartbeat, &c);
     }
     CK(cudaDeviceSynchronize());
     return BB_OK;
@@ -1795,6 +1802,7 @@ bb_status rt_rejoin(Ctx &c) {
           const int slot = (int)(e.consumed % (uint64_t)e.cap);
           c.x.consume(e);
           const char *src = c.x.arena + e.recv_off + (size_t)slot * e.slot_bytes;
+          wait_ev(nd.main, c.x.wait_event(e, slot));
           auto dp = parts(dc);
           for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(dp[i], src + (size_t)i * n * 4, n * 4, cudaMemcpyDeviceToDevice, nd.main));

@@ -59,6 +59,14 @@ void CUDART_CB post_cb(void *arg) {
 }  // namespace
 
 cudaError_t Xport::post(XEdge &e) {
+  if (!callback_mode) {
+    const cudaError_t r = cudaEventRecord(e.ev[e.sent % (uint64_t)e.cap], e.stream);
+    if (r != cudaSuccess) return r;
+    ++e.sent;
+    __atomic_store_n(const_cast<uint64_t *>(intent(e.index)), e.sent, __ATOMIC_RELEASE);
+    __atomic_store_n(const_cast<uint64_t *>(counter(e.index)), e.sent, __ATOMIC_RELEASE);
+    return cudaSuccess;
+  }
   XEdge::Post &p = e.posts[e.sent % (uint64_t)e.cap];
   ++e.sent;
   __atomic_store_n(const_cast<uint64_t *>(intent(e.index)), e.sent, __ATOMIC_RELEASE);
@@ -90,8 +98,10 @@ double now_s() {
 std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
-                       const std::vector<int> &cap, const void *id_bytes, int hi_prio) {
+                       const std::vector<int> &cap, const void *id_bytes, int hi_prio,
+                       bool callback_mode) {
   try {
+    x.callback_mode = callback_mode;
     x.rank = rank;
     x.world = nranks;
     x.nnodes = nnodes;
@@ -123,7 +133,8 @@ std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
     std::snprintf(name, sizeof(name), "/bamboo_%016llx", (unsigned long long)h);
     x.shm_name = name;
     const size_t off_mh = 64 + 8 * x.words();
-    x.shm_bytes = off_mh + kHS * (size_t)nranks;
+    const size_t off_eh = off_mh + kHS * (size_t)nranks;
+    x.shm_bytes = off_eh + kHS * (size_t)max_cap * std::max(1, idx);
     auto hdr = [&]() { return static_cast<uint64_t *>(x.shm); };
     const double t0 = now_s();
     if (rank == 0) {
@@ -177,13 +188,34 @@ std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
       XCK(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
       x.peer_arena[e.dst_rank] = static_cast<char *>(p);
     }
-    // ---- sender-side streams and host-callback slots
+    // ---- sender-side streams, host-callback slots and per-slot
+    // interprocess events (created by the sender, opened by the receiver)
     for (auto &kv : x.edges) {
       XEdge &e = kv.second;
       if (e.src_rank != rank) continue;
       XCK(cudaStreamCreateWithPriority(&e.stream, cudaStreamNonBlocking, hi_prio));
       e.peer_base = x.peer_arena[e.dst_rank];
       e.posts.assign(e.cap, XEdge::Post{nullptr, 0});
+      for (int sl = 0; sl < e.cap; ++sl) {
+        cudaEvent_t ev;
+        XCK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
+        e.ev.push_back(ev);
+        cudaIpcEventHandle_t hnd;
+        XCK(cudaIpcGetEventHandle(&hnd, ev));
+        std::memcpy(tab + off_eh + kHS * ((size_t)e.index * max_cap + sl), &hnd, kHS);
+      }
+    }
+    x.barrier();
+    for (auto &kv : x.edges) {
+      XEdge &e = kv.second;
+      if (e.dst_rank != rank) continue;
+      for (int sl = 0; sl < e.cap; ++sl) {
+        cudaIpcEventHandle_t hnd;
+        std::memcpy(&hnd, tab + off_eh + kHS * ((size_t)e.index * max_cap + sl), kHS);
+        cudaEvent_t ev;
+        XCK(cudaIpcOpenEventHandle(&ev, hnd));
+        e.rev.push_back(ev);
+      }
     }
     XCK(cudaDeviceSynchronize());
     x.barrier();
@@ -197,6 +229,8 @@ void xport_destroy(Xport &x) {
   for (auto &kv : x.edges) {
     XEdge &e = kv.second;
     if (e.stream) cudaStreamSynchronize(e.stream);
+    for (auto ev : e.ev) cudaEventDestroy(ev);
+    for (auto ev : e.rev) cudaEventDestroy(ev);
     if (e.stream) cudaStreamDestroy(e.stream);
   }
   for (auto p : x.peer_arena)

@@ -38,9 +38,11 @@ struct XEdge {
   cudaStream_t stream = nullptr;
   char *peer_base = nullptr;
   uint64_t sent = 0;
+  std::vector<cudaEvent_t> ev;         // per-slot interprocess events (event mode)
   struct Post { volatile uint64_t *ctr; uint64_t value; };
-  std::vector<Post> posts;             // host-callback arguments, one per slot
+  std::vector<Post> posts;             // host-callback arguments, one per slot (callback mode)
   // receiver side
+  std::vector<cudaEvent_t> rev;        // the sender's events, opened here (event mode)
   uint64_t consumed = 0;
 };
 
@@ -79,9 +81,20 @@ struct Xport {
   bool dead(int r) const { return shm && *rank_word(1, r) != 0; }
   // the receiver consumed one message of e (published for quiescence checks)
   void consume(XEdge &e);
-  // After the payload copy is enqueued on e.stream: enqueue the host callback
-  // that publishes the new sequence number when the copy has completed.
+  // After the payload copy is enqueued on e.stream, publish the message.
+  // Event mode (default): record the slot's interprocess event behind the
+  // copy and publish the sequence number at once; the receiver's stream
+  // waits on that event (no host in the data path's latency). Callback mode
+  // (fail-stop, opts.detect_ms): a host callback behind the copy publishes
+  // the number once the copy completed, so the receiver never depends on an
+  // event of a process that may have gone silent.
   cudaError_t post(XEdge &e);
+  bool callback_mode = false;
+  // the event the receiver's stream must wait on before reading slot
+  // `slot` of e (nullptr in callback mode: the payload is already there)
+  cudaEvent_t wait_event(const XEdge &e, int slot) const {
+    return callback_mode ? nullptr : e.rev[slot];
+  }
   bool available(const XEdge &e) const;
 };
 
@@ -92,7 +105,8 @@ struct Xport {
 std::string xport_init(Xport &x, int rank, int nranks, int nnodes,
                        const std::vector<std::tuple<int, int, int>> &want,
                        const std::vector<int> &node_rank, const std::vector<size_t> &slot_bytes,
-                       const std::vector<int> &cap, const void *id_bytes, int hi_prio);
+                       const std::vector<int> &cap, const void *id_bytes, int hi_prio,
+                       bool callback_mode = false);
 void xport_destroy(Xport &x);
 
 }  // namespace bb
