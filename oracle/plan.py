@@ -36,8 +36,15 @@ BRC_BWD = "BRC_BWD"   # EFEB: eager redundant backward of the replica stage (P:4
 # EFEB: the duplicate of a stage's input-gradient for the node two back (its
 # own message kind, so it never shares a FIFO with the normal gradients)
 SEND_DGRAD, RECV_DGRAD = "SEND_DGRAD", "RECV_DGRAD"
-SENDS = {SEND_ACT, SEND_GRAD, RESEND_GRAD, REPLICA_SEND, SEND_DGRAD}
-RECVS = {RECV_ACT, RECV_GRAD, REPLICA_RECV, RECV_DGRAD}
+# D > 1 data-parallel pipelines: each node sends its stage's
+# gradient sum to the nodes of the same stage in the other pipelines, receives
+# theirs and adds all D in ascending pipeline order (deterministic; the same
+# bits on every pipeline). Message kind "ar"; AR_SUM is the local addition.
+# AR_SUM leaves the local sum in place (the update reads the total), so a
+# contribution the victim consumed can be sent again to its shadow (RESEND_AR).
+AR_SEND, AR_RECV, AR_SUM, RESEND_AR = "AR_SEND", "AR_RECV", "AR_SUM", "RESEND_AR"
+SENDS = {SEND_ACT, SEND_GRAD, RESEND_GRAD, REPLICA_SEND, SEND_DGRAD, AR_SEND, RESEND_AR}
+RECVS = {RECV_ACT, RECV_GRAD, REPLICA_RECV, RECV_DGRAD, AR_RECV}
 COMMS = SENDS | RECVS
 
 
@@ -92,7 +99,7 @@ def rc_mode(rc):
     return "eflb" if rc else "none"
 
 
-def stage_plan(s, P, M, rc):
+def stage_plan(s, P, M, rc, d=0, D=1):
     """Instruction list of node s in a failure-free step. rc: False / "none"
     (no redundancy), True / "eflb" (replica + eager FRC),
     "lflb" (replica kept in sync, no FRC: the victim's forward is recomputed
@@ -104,8 +111,15 @@ def stage_plan(s, P, M, rc):
     EFEB placement (this build's reading): BRC_BWD(k) (with its RECV_GRAD
     from s+2) right before node s's own RECV_GRAD(k); on the last node (the
     replica of stage 0 needs stage 1's gradient, which comes last) all of
-    them after its own backwards."""
+    them after its own backwards.
+    d, D: pipeline d of D data-parallel pipelines (node ids d*P + s, peers in
+    the same pipeline); with D > 1 the step's gradient sum of the stage is
+    all-reduced over the pipelines (AR_SEND to each other pipeline, AR_RECV
+    from each, AR_SUM) before the replica sync and the update."""
     mode = rc_mode(rc)
+    if D > 1 and mode == "efeb":
+        raise PlanError("EFEB with D > 1 is not built (the replica's BRC gradient "
+                        "would need its own all-reduce)")
     rc, frc = mode != "none", mode in ("eflb", "efeb")
     efeb = mode == "efeb"
     r = (s + 1) % P
@@ -152,6 +166,12 @@ def stage_plan(s, P, M, rc):
         bwd(i)
     for i in range(M - W, M):
         bwd(i)
+    base = d * P
+    if D > 1:
+        others = [e * P + s - base for e in range(D) if e != d]   # local offsets
+        I.extend(Instr(AR_SEND, None, o, s) for o in others)
+        I.extend(Instr(AR_RECV, None, o, s) for o in others)
+        I.append(Instr(AR_SUM, None, None, s))
     if efeb:
         if s == P - 1:
             for k in range(M):
@@ -165,11 +185,13 @@ def stage_plan(s, P, M, rc):
         I.append(Instr(APPLY, None, None, (s + 1) % P))
     else:
         I.append(Instr(APPLY, None, None, s))
+    if base:   # peers are node ids: pipeline d's nodes are d*P + s
+        I = [i._replace(peer=i.peer + base) if i.peer is not None else i for i in I]
     return I
 
 
-def normal_plans(P, M, rc):
-    return {s: stage_plan(s, P, M, rc) for s in range(P)}
+def normal_plans(P, M, rc, D=1):
+    return {d * P + s: stage_plan(s, P, M, rc, d, D) for d in range(D) for s in range(P)}
 
 
 def gpipe_plan(s, P, M):
@@ -210,7 +232,7 @@ def inputs_of(ins, P):
         return [("act", X + 1, k)]
     if ins.kind in (SEND_GRAD, RESEND_GRAD, SEND_DGRAD):
         return [("dact", X, k)]
-    if ins.kind in (REPLICA_SEND, APPLY):
+    if ins.kind in (REPLICA_SEND, APPLY, AR_SEND, RESEND_AR, AR_SUM):
         return [("gradsum", X)]
     return []
 
@@ -246,6 +268,8 @@ def message_of(ins):
         return ("grad", ins.mb, ins.stage + 1)
     if ins.kind in (REPLICA_SEND, REPLICA_RECV):
         return ("gradsum", None, ins.stage)
+    if ins.kind in (AR_SEND, AR_RECV, RESEND_AR):
+        return ("ar", None, ins.stage)
     if ins.kind == SEND_DGRAD:
         return ("dgrad", ins.mb, ins.stage)
     if ins.kind == RECV_DGRAD:
@@ -366,8 +390,13 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     used for the following iterations ("all instructions of the victim node
     must be executed by its shadow node").
 
+    Node ids are d*P + s for pipeline d (D >= 1): the shadow and successor
+    are the victim's neighbours in its own pipeline; instructions name the
+    pipeline-local stage sv = v % P.
+
     Returns (new_plans, info). Raises Fatal if unrecoverable."""
-    u, w = (v - 1) % P, (v + 1) % P
+    base, sv = v - v % P, v % P
+    u, w = base + (sv - 1) % P, base + (sv + 1) % P
     pv = plans[v]
     executed_v = pv[:pcs[v]]
     commit = any(i.kind == REPLICA_SEND for i in executed_v)
@@ -384,7 +413,8 @@ def recovery_plans(plans, P, M, v, pcs, channels):
 
     # messages from v that a survivor has not consumed yet (delivered, in FIFO)
     pending_from_v = {n: {kind: [m for m, _ in channels.get((v, n, kind), [])]
-                          for kind in ("act", "grad", "gradsum", "dgrad")} for n in plans if n != v}
+                          for kind in ("act", "grad", "gradsum", "dgrad", "ar")}
+                      for n in plans if n != v}
 
     def delivered_filter(n, seq, local_peer_to):
         """Walk n's remaining RECVs from v in order against the delivered FIFO:
@@ -409,24 +439,24 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     # ---- A: the shadow's remaining instructions
     A = []
     for ins in plans[u][pcs[u]:]:
-        if ins.kind == FRC_FWD and ins.stage == v:
+        if ins.kind == FRC_FWD and ins.stage == sv:
             continue                                  # becomes v's FWD (in B)
         if ins.kind in SENDS and ins.peer == v:
             continue                                  # victim<->shadow (rule 2)
-        if ins.kind == APPLY and ins.stage == v and not commit and not efeb:
+        if ins.kind == APPLY and ins.stage == sv and not commit and not efeb:
             continue                                  # v's update runs from B
         A.append(ins)
     A = delivered_filter(u, A, lambda ins: None)
 
     # ---- B: the victim's whole-step instructions, rewritten for the shadow
     B = []
-    frc_done = {i.mb for i in executed(u) if i.kind == FRC_FWD and i.stage == v}
+    frc_done = {i.mb for i in executed(u) if i.kind == FRC_FWD and i.stage == sv}
     if not commit:
         for idx, ins in enumerate(pv):
             kd = ins.kind
             if kd in (LOAD_INPUTS, FRC_FWD, REPLICA_SEND, REPLICA_RECV):
                 continue
-            if kd == APPLY and (ins.stage != v or efeb):
+            if kd == APPLY and (ins.stage != sv or efeb):
                 continue
             if efeb and kd in (BWD, BRC_BWD, RECV_GRAD, RECV_DGRAD):
                 continue                              # the shadow's BRC_BWD does it
@@ -447,6 +477,17 @@ def recovery_plans(plans, P, M, v, pcs, channels):
         if efeb and n != u:
             seq = [i for i in seq if not (i.kind in SENDS and i.peer == v)]
             seq = delivered_filter(n, seq, lambda ins: u)
+        elif n != w and n != u:
+            # another pipeline's node of the victim's stage (D > 1): its
+            # all-reduce traffic with v goes to the shadow, which replays v's
+            # whole all-reduce; a contribution already sent to v went down
+            # with it and is sent again (RESEND_AR, first: the gradient sum
+            # it reads is complete and AR_SUM never overwrites it)
+            # (not after v's commit point: v's all-reduce was complete)
+            resend = [] if commit else [Instr(RESEND_AR, None, u, i.stage) for i in executed(n)
+                                        if i.kind == AR_SEND and i.peer == v]
+            seq = [i._replace(peer=u) if i.kind in SENDS and i.peer == v else i for i in seq]
+            seq = resend + delivered_filter(n, seq, lambda ins: u)
         elif n == w:
             resend = []
             if not commit and w != u:
@@ -469,7 +510,7 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     info = {"victim": v, "shadow": u, "successor": w, "commit": commit,
             "frc_done": sorted(frc_done),
             "brc_mb": sorted(i.mb for i in (A if efeb else B)
-                             if i.kind in (BWD, BRC_BWD) and i.stage == v),
+                             if i.kind in (BWD, BRC_BWD) and i.stage == sv),
             "resend": [i.mb for i in new.get(w, []) if i.kind == RESEND_GRAD]}
     return new, info
 
@@ -489,12 +530,12 @@ def recoverable(P, host, replica_on, dead, v):
     P:464 "consecutive nodes"), and v's stage has a replica on a live node
     (its predecessor). Non-adjacent preemptions after a failover are two
     independent recoveries."""
-    if v in dead or not (0 <= v < P):
+    if v in dead or v not in host:
         return False
-    if [X for X in range(P) if host[X] == v] != [v]:
+    if [X for X in host if host[X] == v] != [v]:
         return False
     r = replica_on[v]
-    return r is not None and r not in dead and r == (v - 1) % P
+    return r is not None and r not in dead and r == v - v % P + (v % P - 1) % P
 
 
 def cut(plans, v, pi):
@@ -521,19 +562,21 @@ def _f(x):
 
 def dump(P, M, rc, ranges, plans, host=None, replica_on=None, device=None, mode="normal",
          victim=None):
-    """host[X] = node running stage X; replica_on[X] = node holding X's replica."""
+    """host[X] = node running (global) stage X; replica_on[X] = node holding
+    X's replica. With D > 1 pipelines the global stage of pipeline d's stage
+    s is d*P + s (pass host / replica_on / device for all of them)."""
     host = host or {s: s for s in range(P)}
     if replica_on is None:
-        replica_on = {s: ((s - 1) % P if rc else None) for s in range(P)}
-    device = device or {n: 0 for n in range(P)}
+        replica_on = {X: ((X - X % P + (X % P - 1) % P) if rc else None) for X in host}
+    device = device or {n: 0 for n in host}
     hdr = f"# bamboo-plan v1 P={P} M={M} rc={rc_mode(rc)} mode={mode}"
     if mode != "normal":
         vs = list(victim) if isinstance(victim, (list, tuple)) else [victim]
         hdr += (f" victim={','.join(map(str, vs))}"
-                f" shadow={','.join(str((x - 1) % P) for x in vs)}")
+                f" shadow={','.join(str(x - x % P + (x % P - 1) % P) for x in vs)}")
     lines = [hdr]
-    for X in range(P):
-        a, b = ranges[X]
+    for X in sorted(host):
+        a, b = ranges[X % P]
         lines.append(f"# stage {X} node {host[X]} device {device[host[X]]} units {a}..{b} "
                      f"replica_on {_f(replica_on[X])}")
     for n in sorted(plans):
@@ -546,19 +589,25 @@ def lose_node(P, host, replica_on, v):
     """(host, replica_on) after node v died and its stage moved to the shadow
     v-1 (Q21): v's stage runs on the shadow without a replica (the replica was
     promoted), and every stage whose replica lived on v is unprotected."""
-    u = (v - 1) % P
+    u = v - v % P + (v % P - 1) % P
     host, replica_on = dict(host), dict(replica_on)
     host[v] = u
-    for X in range(P):
+    for X in replica_on:
         if replica_on[X] == v:
             replica_on[X] = None
     replica_on[v] = None
     return host, replica_on
 
 
-def failover_topology(P, v):
+def normal_topology(P, D=1):
+    """(host, replica_on) keyed by global stage d*P + s (= its node)."""
+    n = P * D
+    return ({g: g for g in range(n)}, {g: g - g % P + (g % P - 1) % P for g in range(n)})
+
+
+def failover_topology(P, v, D=1):
     """(host, replica_on) after stage v moved to its shadow (Q21)."""
-    return lose_node(P, {s: s for s in range(P)}, {s: (s - 1) % P for s in range(P)}, v)
+    return lose_node(P, *normal_topology(P, D), v)
 
 
 # ----------------------------------------------------------------------------
@@ -615,9 +664,9 @@ def dump_lines(plans):
     return "".join(line + "\n" for line in out)
 
 
-def recovery_dump(P, M, v, pi, rc=True):
+def recovery_dump(P, M, v, pi, rc=True, D=1):
     """Cut + continuation text of an injection at (v, pi) (DESIGN.md format)."""
-    plans = normal_plans(P, M, rc)
+    plans = normal_plans(P, M, rc, D)
     pcs, ch = cut(plans, v, pi)
     new, info = recovery_plans(plans, P, M, v, pcs, ch)
     hdr = (f"# bamboo-recovery v1 P={P} M={M} victim={v} shadow={info['shadow']} "
