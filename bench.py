@@ -24,6 +24,7 @@ recovery matrix (victims 0, 1, P/2, P-1 x first FWD / mid BWD), the GEMM
 roofline fraction and the oracle's CPU baseline.
 """
 import argparse
+import dataclasses
 import json
 import os
 
@@ -301,17 +302,19 @@ def run_ours(args, rank, ws, local):
 
     cfg = get_config(args.config)
     m = cfg.model
-    P = max(cfg.stages, ws, args.stages)
+    D = max(1, args.pipelines)   # data-parallel pipelines
+    P = max(cfg.stages, -(-ws // D), args.stages)
     M, mb = cfg.microbatches, cfg.micro_batch
-    samples = M * mb
+    samples = D * M * mb
     def fresh_id():   # every context needs its own rendezvous
         return bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None
     flat = make_params(m)
-    tok, tgt = make_tokens(cfg, 0)
-    host_batches = [make_tokens(cfg, s) for s in range(1, 3)]
+    bcfg = dataclasses.replace(cfg, microbatches=D * M)   # all D pipelines' micro-batches
+    tok, tgt = make_tokens(bcfg, 0)
+    host_batches = [make_tokens(bcfg, s) for s in range(1, 3)]
     lps = balanced_partition(m, P) if args.partition == "balanced" else None
     common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
-                  layers_per_stage=lps)
+                  layers_per_stage=lps, pipelines=D)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
 
     results = {}
@@ -344,7 +347,7 @@ def run_ours(args, rank, ws, local):
         pipe.stage_inputs(tok, tgt)
         res.update(e2e_ms=ms_e2e / e2e_steps, h2d=h2d / e2e_steps, d2h=d2h / e2e_steps)
         results[rc] = res
-        if rc and args.recovery:
+        if rc and args.recovery and D == 1:
             results["recovery"] = recovery_matrix(pipe, P, M, ws, res["ms"], rank)
         pipe.close()
         del pipe
@@ -416,9 +419,12 @@ def run_ours(args, rank, ws, local):
         "data": "synthetic (seeded tokens, random-init weights)",
         "config": {"workload": f"{cfg.name}: {MODEL_NAMES.get(cfg.name, cfg.name)} {m.n_layer}L "
                                f"H{m.d_model} S{m.seq_len} {'causal' if m.causal else 'bidirectional'}, "
-                               f"{P} stages, M={M}, mb={mb}, EFLB (eager FRC, lazy BRC)",
+                               f"{P} stages, M={M}, mb={mb}, EFLB (eager FRC, lazy BRC)"
+                               + (f", {D} data-parallel pipelines" if D > 1 else ""),
                    "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
-                   "seq_len": m.seq_len, "parallelism": f"pp{P} on {ws} GPU(s)",
+                   "seq_len": m.seq_len,
+                   "parallelism": (f"dp{D} x " if D > 1 else "") + f"pp{P} on {ws} GPU(s)",
+                   "pipelines": D,
                    "layers_per_stage": lps or "even",
                    "frc_retained_per_step": on["retained"], "saved_set_mb": on["slot_mb"],
                    "l2": "working set (weights, stash, FRC retention) >> 126 MB L2"},
@@ -545,6 +551,9 @@ def main():
     ap.add_argument("--retain", default="auto",
                     help="frc_retain_bytes per node: auto (free HBM) or bytes (0 = all M)")
     ap.add_argument("--no-recovery", dest="recovery", action="store_false")
+    ap.add_argument("--pipelines", type=int, default=1,
+                    help="D data-parallel pipelines (bb_opts.pipelines; the recovery matrix "
+                         "runs only at D=1)")
     args = ap.parse_args()
     if args.impl == "reference":
         # the oracle arm needs no GPU and no process group: rank 0 runs it,

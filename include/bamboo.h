@@ -119,10 +119,30 @@ typedef struct {
                                    detect_ms (P:417-420 timeouts), run to quiescence,
                                    agree on the cut from the victim's delivered messages
                                    and return BB_E_PREEMPTED from their own bb_step     */
+  int pipelines;                /* D data-parallel pipelines, default 1. Node
+                                   d*stages + s runs stage s of pipeline d on micro-batches
+                                   d*M .. d*M+M-1 of the step's D*M*micro_batch sequences;
+                                   its shadow / successor are its ring neighbours inside
+                                   pipeline d. After its last backward every stage's fp32
+                                   gradient sum is all-reduced with the same stage of the
+                                   other pipelines (sum in ascending pipeline order, so
+                                   every pipeline applies the same bits) before the replica
+                                   sync and Adam; a preempted pipeline's all-reduce is run
+                                   by its shadow after the recovery and the others wait for
+                                   it. node_rank then has D*stages entries. Not
+                                   with EFEB or detect_ms > 0                             */
+  size_t frc_swap_bytes;        /* per replica: pinned host memory for the FRC saved sets
+                                   beyond frc_retain_bytes ("swap out these data"):
+                                   each is copied to the host on its own stream after the
+                                   FRC and copied back by a lazy BRC instead of being
+                                   recomputed. 0 (default) = recompute. Costs PCIe time
+                                   per step                                 */
 } bb_opts;
 
 typedef struct {
-  float loss;            /* mean token cross-entropy of the step (NaN on ranks without stage P-1) */
+  float loss;            /* mean token cross-entropy of the step (NaN on ranks without stage P-1;
+                            D > 1: the sum over this rank's pipelines of their share, each
+                            share = its tokens' CE summed / all D*M*mb*S tokens)           */
   float step_ms;         /* host wall time of the call                                    */
   float device_ms;       /* max over local nodes of main-stream time of the step          */
   int gpu_launches;      /* kernels this process launched during the call                 */
@@ -141,6 +161,7 @@ typedef struct {
   int frc_recomputed_mb; /* forwards of the victim's stage recomputed during recovery: FRC
                             catch-up, beyond-budget BRC re-forwards, LFLB lazy FRC        */
   uint64_t bytes_resent; /* bytes re-sent (RESEND_GRAD) or rerouted during the recovery  */
+  int frc_swapped_mb;    /* FRC saved sets the lazy BRC copied back from host memory      */
 } bb_recovery_stats;
 
 /* Per-node accounting of the last step (opts.timing = 1), from CUDA events
@@ -182,8 +203,9 @@ bb_status bb_init(const bb_model *m, int stages, int microbatches, const bb_opts
  * it keeps. Resets Adam state and step count. */
 bb_status bb_load_params(void *ctx, const float *host, size_t n);
 
-/* One training step over M*mb sequences: tokens, targets = host int32 arrays
- * [M*mb, seq_len] row-major (micro-batch k = rows k*mb..k*mb+mb-1). Every rank
+/* One training step over D*M*mb sequences (D = opts.pipelines): tokens,
+ * targets = host int32 arrays [D*M*mb, seq_len] row-major (micro-batch j =
+ * rows j*mb..j*mb+mb-1; pipeline d takes j = d*M .. d*M+M-1). Every rank
  * passes the full arrays and uploads what its nodes need (the last node
  * fetches inputs for its FRC). Token and target ids must lie in [0, vocab):
  * BB_E_INVAL otherwise (checked before any device work). Returns BB_E_PREEMPTED if an armed injection
@@ -226,7 +248,10 @@ enum { BB_STATE_PARAMS = 0, BB_STATE_GRADS = 1, BB_STATE_ADAM_M = 2, BB_STATE_AD
 /* Copy stage `stage`'s fp32 state (what = BB_STATE_*) into host[n], n = the
  * stage's parameter count. replica = 0 reads the copy the stage runs on
  * (primary; the promoted replica after a failover), 1 reads the replica kept
- * by its predecessor. BB_E_INVAL if that copy is not hosted by this process. */
+ * by its predecessor. BB_E_INVAL if that copy is not hosted by this process.
+ * With D > 1 pipelines, stage < stages reads the lowest local pipeline's copy
+ * and stage = d*stages + s reads pipeline d's copy of stage s; GRADS is the
+ * pipeline's local gradient sum (before the all-reduce). */
 bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host, size_t n);
 
 /* Overwrite stage `stage`'s fp32 state (what = BB_STATE_PARAMS, _ADAM_M or

@@ -51,7 +51,8 @@ class BBOpts(ctypes.Structure):
                 ("node_rank", ctypes.POINTER(ctypes.c_int)), ("session_id", ctypes.c_void_p),
                 ("profile", ctypes.c_int), ("frc_retain_bytes", ctypes.c_size_t),
                 ("frc_persistent", ctypes.c_int), ("timing", ctypes.c_int),
-                ("detect_ms", ctypes.c_int)]
+                ("detect_ms", ctypes.c_int), ("pipelines", ctypes.c_int),
+                ("frc_swap_bytes", ctypes.c_size_t)]
 
 
 class BBStepStats(ctypes.Structure):
@@ -65,7 +66,8 @@ class BBRecoveryStats(ctypes.Structure):
                 ("commit", ctypes.c_int), ("brc_mb", ctypes.c_int), ("frc_done_mb", ctypes.c_int),
                 ("resent_mb", ctypes.c_int), ("recover_ms", ctypes.c_float),
                 ("loss", ctypes.c_float), ("interrupted_step_ms", ctypes.c_float),
-                ("frc_recomputed_mb", ctypes.c_int), ("bytes_resent", ctypes.c_uint64)]
+                ("frc_recomputed_mb", ctypes.c_int), ("bytes_resent", ctypes.c_uint64),
+                ("frc_swapped_mb", ctypes.c_int)]
 
 
 class BBNodeStat(ctypes.Structure):
@@ -161,7 +163,7 @@ def _ints(xs):
 def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-4, beta1=0.9,
               beta2=0.999, eps=1e-8, world_rank=0, world_size=1, device=0, node_rank=None,
               session_id=None, profile=False, frc_retain_bytes=0, frc_persistent=False,
-              timing=False, detect_ms=0):
+              timing=False, detect_ms=0, pipelines=1, frc_swap_bytes=0):
     """rc: True (= "eflb"), False (= "none") or a mode name in RC."""
     o = BBOpts()
     lib().bb_default_opts(ctypes.byref(o))
@@ -186,6 +188,8 @@ def make_opts(micro_batch=1, rc=True, prec="bf16", layers_per_stage=None, lr=1e-
     o.frc_persistent = int(bool(frc_persistent))
     o.timing = int(bool(timing))
     o.detect_ms = int(detect_ms)
+    o.pipelines = int(pipelines)
+    o.frc_swap_bytes = int(frc_swap_bytes)
     return o, keep
 
 
@@ -232,6 +236,9 @@ class Pipeline:
         self._o, self._keep = make_opts(**opts)
         self._m = _model(model)
         self.stages, self.microbatches = stages, microbatches
+        # int32 elements per tokens / targets array: D*M*mb sequences
+        self._n_in = (max(1, self._o.pipelines) * microbatches * self._o.micro_batch *
+                      self._m.seq_len)
         h = ctypes.c_void_p()
         st = lib().bb_init(ctypes.byref(self._m), stages, microbatches, ctypes.byref(self._o),
                            ctypes.byref(h))
@@ -256,9 +263,16 @@ class Pipeline:
         flat = np.ascontiguousarray(flat, dtype=np.float32)
         self._check(lib().bb_load_params(self._h, flat.ctypes.data, flat.size), "bb_load_params")
 
-    def stage_inputs(self, tokens, targets):
+    def _inputs(self, tokens, targets):
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         g = np.ascontiguousarray(targets, dtype=np.int32)
+        if t.size != self._n_in or g.size != self._n_in:
+            raise ValueError(f"tokens / targets: need {self._n_in} ids "
+                             "(pipelines * microbatches * micro_batch * seq_len)")
+        return t, g
+
+    def stage_inputs(self, tokens, targets):
+        t, g = self._inputs(tokens, targets)
         self._check(lib().bb_stage_inputs(self._h, t.ctypes.data, g.ctypes.data),
                     "bb_stage_inputs")
 
@@ -269,8 +283,7 @@ class Pipeline:
         if tokens is None:
             s = lib().bb_step(self._h, None, None, ctypes.byref(st))
         else:
-            t = np.ascontiguousarray(tokens, dtype=np.int32)
-            g = np.ascontiguousarray(targets, dtype=np.int32)
+            t, g = self._inputs(tokens, targets)
             s = lib().bb_step(self._h, t.ctypes.data, g.ctypes.data, ctypes.byref(st))
         if s == BB_E_PREEMPTED:
             return "preempted", st
@@ -302,7 +315,8 @@ class Pipeline:
         return b.value, r.value
 
     def read_state(self, stage, what="params", replica=False):
-        _, n = self.stage_params(stage)
+        """stage < stages, or d*stages + s for pipeline d's copy (D > 1)."""
+        _, n = self.stage_params(stage % self.stages)
         out = np.empty(n, np.float32)
         self._check(lib().bb_read_state(self._h, stage, int(replica), STATE[what],
                                         out.ctypes.data, n), "bb_read_state")

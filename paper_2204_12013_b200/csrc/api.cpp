@@ -198,21 +198,22 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
   const bb_opts &op = o ? *o : def;
   const bool rc = op.rc != BB_RC_NONE;
   try {
-    const int P = stages, M = microbatches;
+    const int P = stages, M = microbatches, D = op.pipelines < 1 ? 1 : op.pipelines;
     auto ranges = bb::partition(m->n_layer, P, op.layers_per_stage);
-    std::vector<int> dev(P, 0);
+    const int N = D * P;   // nodes
+    std::vector<int> dev(N, 0);
     const int ws = op.world_size < 1 ? 1 : op.world_size;
-    const int per = (P + ws - 1) / ws;
-    for (int n = 0; n < P; ++n) dev[n] = op.node_rank ? op.node_rank[n] : std::min(n / per, ws - 1);
-    bb::Plans plans = bb::normal_plans(P, M, (int)op.rc);
+    const int per = (N + ws - 1) / ws;
+    for (int n = 0; n < N; ++n) dev[n] = op.node_rank ? op.node_rank[n] : std::min(n / per, ws - 1);
+    bb::Plans plans = bb::normal_plans(P, M, (int)op.rc, D);
     std::string s;
     if (victim < 0) {
-      s = bb::dump(P, M, (int)op.rc, ranges, plans, bb::normal_topology(P, rc), dev, false, {});
+      s = bb::dump(P, M, (int)op.rc, ranges, plans, bb::normal_topology(P, rc, D), dev, false, {});
     } else {
-      if (!rc || victim >= P) return BB_E_INVAL;
+      if (!rc || victim >= N) return BB_E_INVAL;
       if (at_instr < 0) {
         s = bb::dump(P, M, (int)op.rc, ranges, bb::failover_plans(P, M, victim, &plans),
-                     bb::failover_topology(P, victim), dev, true, {victim});
+                     bb::failover_topology(P, victim, D), dev, true, {victim});
       } else {
         bb::Cut cut = bb::cut(plans, victim, at_instr);
         bb::RecoveryInfo info;

@@ -780,6 +780,29 @@ __global__ void sum_fixed_kernel(int n, const float *__restrict__ x, float *__re
   if (threadIdx.x == 0) out[0] = sh[0];
 }
 
+// ------------------------------------------------- all-reduce sum (D > 1)
+struct PipeSrc {
+  const float *p[kMaxPipelines];
+};
+// HBM-bound: D loads and one store per element, float4 when everything is
+// 16-byte aligned; grid-stride over a grid sized for the SM count
+template <typename T>
+__global__ void sum_pipelines_kernel(size_t n, PipeSrc src, int D, T *__restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    T a = reinterpret_cast<const T *>(src.p[0])[i];
+    for (int e = 1; e < D; ++e) {
+      const T b = reinterpret_cast<const T *>(src.p[e])[i];
+      if constexpr (sizeof(T) == 16) {
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      } else {
+        a += b;
+      }
+    }
+    dst[i] = a;
+  }
+}
+
 // ---------------------------------------------------------------- Adam
 __global__ void adam_kernel(size_t n, float *__restrict__ p, const float *__restrict__ g,
                             float *__restrict__ m, float *__restrict__ v,
@@ -1100,6 +1123,32 @@ cudaError_t gpu_sleep(unsigned long long ns, cudaStream_t s) {
 cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s) {
   sum_fixed_kernel<<<1, 1024, 0, s>>>(n, x, out);
   ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t sum_pipelines(size_t n, const float *const *src, int D, float *dst, cudaStream_t s) {
+  if (D < 1 || D > kMaxPipelines) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  PipeSrc ps{};
+  uintptr_t al = reinterpret_cast<uintptr_t>(dst);
+  for (int e = 0; e < D; ++e) {
+    ps.p[e] = src[e];
+    al |= reinterpret_cast<uintptr_t>(src[e]);
+  }
+  const size_t n4 = (al & 15) == 0 ? n / 4 : 0;
+  if (n4) {
+    sum_pipelines_kernel<float4><<<grid_for(n4, 256), 256, 0, s>>>(n4, ps, D,
+                                                                   reinterpret_cast<float4 *>(dst));
+    ++g_launches;
+  }
+  const size_t done = 4 * n4;
+  if (done < n) {
+    PipeSrc tail{};
+    for (int e = 0; e < D; ++e) tail.p[e] = src[e] + done;
+    sum_pipelines_kernel<float><<<grid_for(n - done, 256), 256, 0, s>>>(n - done, tail, D,
+                                                                        dst + done);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 

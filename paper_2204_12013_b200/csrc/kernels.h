@@ -92,6 +92,12 @@ cudaError_t cross_entropy(bool bf16, int R, int V, void *logits, const int32_t *
 // out[0] = sum of x[0..n) in a fixed order (single block).
 cudaError_t sum_fixed(int n, const float *x, float *out, cudaStream_t s);
 
+// D > 1 pipelines: dst = ((src[0] + src[1]) + src[2]) + ... over the
+// D contributions in ascending pipeline order, fp32 (every pipeline computes
+// the same bits). D <= kMaxPipelines; dst may alias none of the sources.
+constexpr int kMaxPipelines = 8;
+cudaError_t sum_pipelines(size_t n, const float *const *src, int D, float *dst, cudaStream_t s);
+
 cudaError_t adam(size_t n, float *p, const float *g, float *m, float *v, void *w16, float lr,
                  float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s);
 cudaError_t cast_f32_to_bf16(size_t n, const float *src, void *dst, cudaStream_t s);

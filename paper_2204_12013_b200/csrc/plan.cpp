@@ -11,15 +11,17 @@ const char *kind_name(Kind k) {
   static const char *n[] = {"LOAD_INPUTS", "FWD",          "FRC_FWD",      "BWD",
                             "SEND_ACT",    "RECV_ACT",     "SEND_GRAD",    "RECV_GRAD",
                             "RESEND_GRAD", "REPLICA_SEND", "REPLICA_RECV", "APPLY",
-                            "BRC_BWD",     "SEND_DGRAD",   "RECV_DGRAD"};
+                            "BRC_BWD",     "SEND_DGRAD",   "RECV_DGRAD",   "AR_SEND",
+                            "AR_RECV",     "AR_SUM",       "RESEND_AR"};
   return n[k];
 }
 bool is_send(Kind k) {
   return k == SEND_ACT || k == SEND_GRAD || k == RESEND_GRAD || k == REPLICA_SEND ||
-         k == SEND_DGRAD;
+         k == SEND_DGRAD || k == AR_SEND || k == RESEND_AR;
 }
 bool is_recv(Kind k) {
-  return k == RECV_ACT || k == RECV_GRAD || k == REPLICA_RECV || k == RECV_DGRAD;
+  return k == RECV_ACT || k == RECV_GRAD || k == REPLICA_RECV || k == RECV_DGRAD ||
+         k == AR_RECV;
 }
 
 Msg message_of(const Instr &i) {
@@ -33,6 +35,9 @@ Msg message_of(const Instr &i) {
     case REPLICA_RECV: return {MSG_GRADSUM, -1, i.stage};
     case SEND_DGRAD: return {MSG_DGRAD, i.mb, i.stage};
     case RECV_DGRAD: return {MSG_DGRAD, i.mb, i.stage + 1};
+    case AR_SEND:
+    case AR_RECV:
+    case RESEND_AR: return {MSG_AR, -1, i.stage};
     default: throw PlanError("message_of on a compute instruction");
   }
 }
@@ -57,6 +62,9 @@ std::vector<Key> inputs_of(const Instr &i, int P) {
     case SEND_DGRAD:
     case RESEND_GRAD: return {{K_DACT, X, k}};
     case REPLICA_SEND:
+    case AR_SEND:
+    case RESEND_AR:
+    case AR_SUM:
     case APPLY: return {{K_GRADSUM, X, 0}};
     default: return {};
   }
@@ -119,13 +127,15 @@ std::vector<std::pair<int, int>> partition(int L, int P, const int *lps) {
 }
 
 // -------------------------------------------------------------- normal plan
-std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
+std::vector<Instr> stage_plan(int s, int P, int M, int mode, int d, int D) {
   // mode = bb_rc_mode: NONE 0, EFLB 1 (replicas + eager FRC), LFLB 2
   // (replicas, no FRC: the forward is recomputed lazily on failure), EFEB 3
   // (eager FRC and eager BRC of the replica stage r = s+1 from the duplicate
   // gradient node s+2 sends, no replica sync)
   const bool rc = mode != 0, frc = mode == 1 || mode == 3, efeb = mode == 3;
   if (rc && P < 2) throw PlanError("RC needs stages >= 2");
+  if (D < 1 || d < 0 || d >= D) throw PlanError("bad pipeline index");
+  if (efeb && D > 1) throw PlanError("EFEB with more than one pipeline is not built");
   const int r = (s + 1) % P;
   std::vector<Instr> I;
   const bool need_tok = s == 0 || (rc && s == P - 1);
@@ -160,6 +170,17 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
     bwd(i);
   }
   for (int i = M - W; i < M; ++i) bwd(i);
+  // D > 1: the stage's gradient sum meets the same stage of the other
+  // pipelines before anything reads it (replica sync, update); peers are
+  // global node ids, marked here by an offset past the pipeline-local ids
+  std::vector<int> partners;
+  for (int e = 0; e < D; ++e)
+    if (e != d) partners.push_back(e * P + s);
+  const size_t ar_at = I.size();
+  for (int o : partners) I.push_back({AR_SEND, -1, o, s});
+  for (int o : partners) I.push_back({AR_RECV, -1, o, s});
+  if (D > 1) I.push_back({AR_SUM, -1, -1, s});
+  const size_t ar_end = I.size();
   if (efeb) {
     if (s == P - 1)   // stage 1's gradients come last: after the own backwards
       for (int k = 0; k < M; ++k) brc(k);
@@ -173,12 +194,17 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode) {
   } else {
     I.push_back({APPLY, -1, -1, s});
   }
+  // pipeline-local peers become global node ids (the all-reduce partners
+  // already are)
+  for (size_t i = 0; i < I.size(); ++i)
+    if (I[i].peer >= 0 && (i < ar_at || i >= ar_end)) I[i].peer += d * P;
   return I;
 }
 
-Plans normal_plans(int P, int M, int mode) {
+Plans normal_plans(int P, int M, int mode, int D) {
   Plans p;
-  for (int s = 0; s < P; ++s) p[s] = stage_plan(s, P, M, mode);
+  for (int d = 0; d < D; ++d)
+    for (int s = 0; s < P; ++s) p[d * P + s] = stage_plan(s, P, M, mode, d, D);
   return p;
 }
 
@@ -268,6 +294,7 @@ enum Fate { KEEP, DROP, TO_SHADOW };
 
 struct Loss {
   int P, M, v, u, w;
+  int sv;   // the victim's stage in its pipeline (instructions name stages)
   bool efeb = false, commit = false;
   std::set<int> frc_done;
   const std::map<int, int> *pcs = nullptr;
@@ -290,16 +317,17 @@ std::map<int, std::deque<Msg>> undelivered_queue(const Loss &x, int n) {
 }
 
 Fate shadow_fate(const Loss &x, const Instr &i) {
-  if (i.kind == FRC_FWD && i.stage == x.v) return DROP;
+  if (i.kind == FRC_FWD && i.stage == x.sv) return DROP;
   if (is_send(i.kind) && i.peer == x.v) return DROP;
-  if (i.kind == APPLY && i.stage == x.v && !x.commit && !x.efeb) return DROP;
+  if (i.kind == APPLY && i.stage == x.sv && !x.commit && !x.efeb) return DROP;
   return KEEP;
 }
 
-Fate survivor_fate(const Loss &x, int n, const Instr &i) {
+Fate survivor_fate(const Loss &x, int /*n*/, const Instr &i) {
   if (!is_send(i.kind) || i.peer != x.v) return KEEP;
   if (x.efeb) return DROP;
-  if (n != x.w || i.kind == REPLICA_SEND) return DROP;
+  if (i.kind == AR_SEND) return TO_SHADOW;   // the shadow replays v's all-reduce
+  if (i.kind == REPLICA_SEND) return DROP;   // w's replica on v is gone (Q21)
   return TO_SHADOW;
 }
 
@@ -313,7 +341,7 @@ bool victim_work(const Loss &x, const Instr &i, int idx) {
     case REPLICA_RECV:
       return false;
     case APPLY:
-      return i.stage == x.v && !x.efeb;
+      return i.stage == x.sv && !x.efeb;
     case BWD:
       return !x.efeb;
     case RECV_GRAD:
@@ -476,8 +504,9 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
   x.P = P;
   x.M = M;
   x.v = v;
-  x.u = (v - 1 + P) % P;
-  x.w = (v + 1) % P;
+  x.sv = v % P;
+  x.u = ring_prev(P, v);
+  x.w = ring_next(P, v);
   x.pcs = &pcs;
   x.ch = &ch;
   const std::vector<Instr> &pv = plans.at(v), &pu = plans.at(x.u);
@@ -485,7 +514,7 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
   for (auto &kv : plans)
     for (const Instr &i : kv.second) x.efeb = x.efeb || i.kind == BRC_BWD;
   for (int i = 0; i < pcs.at(x.u); ++i)
-    if (pu[i].kind == FRC_FWD && pu[i].stage == v) x.frc_done.insert(pu[i].mb);
+    if (pu[i].kind == FRC_FWD && pu[i].stage == x.sv) x.frc_done.insert(pu[i].mb);
 
   Plans out;
   for (auto &kv : plans) {
@@ -499,6 +528,17 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
       for (int i = 0; i < pcs.at(n); ++i) {
         const Instr &e = kv.second[i];
         if (e.kind == SEND_GRAD && e.peer == v) again.push_back({RESEND_GRAD, e.mb, x.u, e.stage});
+      }
+      seq.insert(seq.begin(), again.begin(), again.end());
+    }
+    if (n / P != v / P && !x.commit) {
+      // another pipeline: a contribution v received went down with it; the
+      // shadow receives it again when it replays v's all-reduce (nothing to
+      // redo after v's commit point, its all-reduce was complete)
+      std::vector<Instr> again;
+      for (int i = 0; i < pcs.at(n); ++i) {
+        const Instr &e = kv.second[i];
+        if (e.kind == AR_SEND && e.peer == v) again.push_back({RESEND_AR, -1, x.u, e.stage});
       }
       seq.insert(seq.begin(), again.begin(), again.end());
     }
@@ -525,7 +565,7 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
     // the victim-stage backwards still to run: B's (EFLB / LFLB) or the
     // shadow's pending eager BRCs (EFEB)
     for (const Instr &i : x.efeb ? out[x.u] : B)
-      if ((i.kind == BWD || i.kind == BRC_BWD) && i.stage == v) info->brc_mb.push_back(i.mb);
+      if ((i.kind == BWD || i.kind == BRC_BWD) && i.stage == x.sv) info->brc_mb.push_back(i.mb);
     info->resend.clear();
     if (out.count(x.w))
       for (const Instr &i : out[x.w])
@@ -541,33 +581,36 @@ Plans failover_plans(int P, int M, int v, const Plans *base) {
   return recovery_plans(plans, P, M, v, pcs, Channels{}, nullptr);
 }
 
-Topology normal_topology(int P, bool rc) {
+Topology normal_topology(int P, bool rc, int D) {
   Topology t;
-  for (int s = 0; s < P; ++s) {
-    t.host.push_back(s);
-    t.replica_on.push_back(rc ? (s - 1 + P) % P : -1);
+  for (int g = 0; g < D * P; ++g) {
+    t.host.push_back(g);
+    t.replica_on.push_back(rc ? ring_prev(P, g) : -1);
   }
   return t;
 }
 
 Topology lose_node(int P, const Topology &t0, int v) {
   Topology t = t0;
-  t.host[v] = (v - 1 + P) % P;
-  for (int X = 0; X < P; ++X)
-    if (t.replica_on[X] == v) t.replica_on[X] = -1;
+  t.host[v] = ring_prev(P, v);
+  for (int &r : t.replica_on)
+    if (r == v) r = -1;
   t.replica_on[v] = -1;
   return t;
 }
 
-Topology failover_topology(int P, int v) { return lose_node(P, normal_topology(P, true), v); }
+Topology failover_topology(int P, int v, int D) {
+  return lose_node(P, normal_topology(P, true, D), v);
+}
 
 bool recoverable(int P, const Topology &t, const std::vector<int> &dead, int v) {
   auto is_dead = [&](int n) { return std::find(dead.begin(), dead.end(), n) != dead.end(); };
-  if (v < 0 || v >= P || is_dead(v)) return false;
-  for (int X = 0; X < P; ++X)
-    if ((t.host[X] == v) != (X == v)) return false;   // v runs exactly its own stage
+  const int G = (int)t.host.size();
+  if (v < 0 || v >= G || is_dead(v)) return false;
+  for (int g = 0; g < G; ++g)
+    if ((t.host[g] == v) != (g == v)) return false;   // v runs exactly its own stage
   const int r = t.replica_on[v];
-  return r >= 0 && !is_dead(r) && r == (v - 1 + P) % P;
+  return r >= 0 && !is_dead(r) && r == ring_prev(P, v);
 }
 
 // --------------------------------------------------------------------- dump
@@ -596,14 +639,14 @@ std::string dump(int P, int M, int rc, const std::vector<std::pair<int, int>> &r
     o << " victim=";
     for (size_t i = 0; i < victims.size(); ++i) o << (i ? "," : "") << victims[i];
     o << " shadow=";
-    for (size_t i = 0; i < victims.size(); ++i) o << (i ? "," : "") << (victims[i] - 1 + P) % P;
+    for (size_t i = 0; i < victims.size(); ++i) o << (i ? "," : "") << ring_prev(P, victims[i]);
   }
   o << '\n';
-  for (int X = 0; X < P; ++X) {
-    const int n = topo.host[X];
-    o << "# stage " << X << " node " << n << " device " << node_device[n] << " units "
-      << ranges[X].first << ".." << ranges[X].second << " replica_on " << fld(topo.replica_on[X])
-      << '\n';
+  for (int g = 0; g < (int)topo.host.size(); ++g) {
+    const int n = topo.host[g];
+    o << "# stage " << g << " node " << n << " device " << node_device[n] << " units "
+      << ranges[g % P].first << ".." << ranges[g % P].second << " replica_on "
+      << fld(topo.replica_on[g]) << '\n';
   }
   o << dump_lines(plans);
   return o.str();

@@ -25,7 +25,11 @@ enum Kind : int8_t {
   LOAD_INPUTS, FWD, FRC_FWD, BWD, SEND_ACT, RECV_ACT, SEND_GRAD, RECV_GRAD, RESEND_GRAD,
   REPLICA_SEND, REPLICA_RECV, APPLY,
   BRC_BWD,                 // EFEB: eager redundant backward of the replica stage
-  SEND_DGRAD, RECV_DGRAD   // EFEB: a stage's input-gradient duplicated to the node two back
+  SEND_DGRAD, RECV_DGRAD,  // EFEB: a stage's input-gradient duplicated to the node two back
+  // D > 1 pipelines: the stage's gradient sum to / from the
+  // same stage of every other pipeline, then the sum of all D in ascending
+  // pipeline order; RESEND_AR gives a lost victim's shadow a contribution again
+  AR_SEND, AR_RECV, AR_SUM, RESEND_AR
 };
 const char *kind_name(Kind k);
 bool is_send(Kind k);
@@ -40,7 +44,8 @@ struct Instr {
 };
 
 enum MsgKind : int8_t { MSG_ACT = 0, MSG_GRAD = 1, MSG_GRADSUM = 2, MSG_STATE = 3 /* rejoin only */,
-                        MSG_DGRAD = 4 /* EFEB duplicate gradients */ };
+                        MSG_DGRAD = 4 /* EFEB duplicate gradients */,
+                        MSG_AR = 5 /* D > 1 all-reduce contributions */ };
 struct Msg {
   MsgKind kind;
   int mb;
@@ -50,7 +55,8 @@ struct Msg {
 Msg message_of(const Instr &i);
 
 // Data keys of the symbolic store (mirrors of the runtime buffers).
-enum KeyType : int8_t { K_TOK, K_TGT, K_ACT, K_DACT, K_SAVED, K_LOSS, K_GRADSUM };
+enum KeyType : int8_t { K_TOK, K_TGT, K_ACT, K_DACT, K_SAVED, K_LOSS, K_GRADSUM,
+                        K_AR /* (stage, pipeline): a received all-reduce contribution */ };
 struct Key {
   KeyType t;
   int a, b;
@@ -74,8 +80,10 @@ struct PlanError : std::exception {
 std::vector<std::pair<int, int>> partition(int n_layer, int P, const int *layers_per_stage);
 
 // mode = bb_rc_mode (0 none, 1 EFLB, 2 LFLB, 3 EFEB); a bool converts to none / EFLB.
-std::vector<Instr> stage_plan(int s, int P, int M, int mode);
-Plans normal_plans(int P, int M, int mode);
+// Pipeline d of D: node ids d*P + s (peers inside the pipeline, plus the
+// all-reduce partners e*P + s of the other pipelines when D > 1).
+std::vector<Instr> stage_plan(int s, int P, int M, int mode, int d = 0, int D = 1);
+Plans normal_plans(int P, int M, int mode, int D = 1);
 
 // Round-robin lockstep (one instruction per node per round, ascending node
 // id); RECVs wait for their message, SENDs are buffered per (src,dst,kind).
@@ -102,12 +110,17 @@ Plans recovery_plans(const Plans &plans, int P, int M, int victim, const std::ma
 // at an empty cut.
 Plans failover_plans(int P, int M, int victim, const Plans *base = nullptr);
 
+// Indexed by global stage g = d*P + s (pipeline d's stage s; its node in the
+// normal plans). A node's shadow / successor are its neighbours in its own
+// pipeline's ring.
 struct Topology {
-  std::vector<int> host;        // stage -> node
-  std::vector<int> replica_on;  // stage -> node holding its replica, -1 none
+  std::vector<int> host;        // global stage -> node
+  std::vector<int> replica_on;  // global stage -> node holding its replica, -1 none
 };
-Topology normal_topology(int P, bool rc);
-Topology failover_topology(int P, int victim);
+inline int ring_prev(int P, int n) { return n - n % P + (n % P + P - 1) % P; }
+inline int ring_next(int P, int n) { return n - n % P + (n % P + 1) % P; }
+Topology normal_topology(int P, bool rc, int D = 1);
+Topology failover_topology(int P, int victim, int D = 1);
 // Topology after node v died and its stage moved to the shadow v-1 (Q21):
 // v's stage runs unprotected on the shadow; every stage whose replica lived
 // on v loses its protection.

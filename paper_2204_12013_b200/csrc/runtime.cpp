@@ -164,6 +164,9 @@ static void layout_slots(const Dims &d, size_t tsz, StageInfo &si) {
 namespace {
 double watch_s();
 constexpr int kScratchSlot = -2;   // FRC beyond the retention budget
+// Entry::slot of a saved set: >= 0 a device slot, -1 gone (a BRC recomputes
+// it), <= kHostSlot0 swapped to host slot kHostSlot0 - slot
+constexpr int kHostSlot0 = -3;
 char *slot_base(const Copy &cp, int slot) {
   return slot == kScratchSlot ? cp.scratch : cp.sp.at(slot);
 }
@@ -381,7 +384,7 @@ void stage_forward(Ctx &c, Node &nd, Copy &cp, int X, int k, int slot, cudaStrea
             sl + u.dlog, d.V, nullptr, nullptr, nullptr}, tg);
       {
         Prof pf(c, nd, s, PC_CE, 0);
-        const float inv = 1.0f / (float)((double)d.M * d.mb * d.S);
+        const float inv = 1.0f / (float)((double)d.D * d.M * d.mb * d.S);   // whole-batch mean
         CK(k::cross_entropy(b16, R, d.V, sl + u.dlog, nd.d_tgt + (size_t)k * R, inv, loss_rows,
                             s));
         CK(k::sum_fixed(R, loss_rows, cp.loss + k, s));
@@ -521,11 +524,12 @@ XEdge &xedge(Ctx &c, int src, int dst, int kind) {
 }
 
 size_t msg_count(const Ctx &c, MsgKind kind, int stage) {
-  if (kind == MSG_GRADSUM) return c.stages[stage].pcount;
+  if (kind == MSG_GRADSUM || kind == MSG_AR) return c.stages[stage].pcount;
   return (size_t)c.d.R() * c.d.H;
 }
 size_t msg_bytes(const Ctx &c, MsgKind kind, int stage) {
-  return msg_count(c, kind, stage) * (kind == MSG_GRADSUM ? sizeof(float) : c.act_bytes);
+  const bool f32 = kind == MSG_GRADSUM || kind == MSG_AR;
+  return msg_count(c, kind, stage) * (f32 ? sizeof(float) : c.act_bytes);
 }
 
 Key payload_key(const Instr &ins) {
@@ -587,9 +591,10 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
   switch (ins.kind) {
     case LOAD_INPUTS: {
       const size_t n = (size_t)M * d.R();
+      const size_t off = (size_t)(nd.n / P) * n;   // pipeline d's micro-batches d*M ..
       if (!c.resident_step) {   // the last node fetches its inputs itself
-        CK(cudaMemcpyAsync(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice, nd.main));
-        CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice, nd.main));
+        CK(cudaMemcpyAsync(nd.d_tok, c.h_tok + off, n * 4, cudaMemcpyHostToDevice, nd.main));
+        CK(cudaMemcpyAsync(nd.d_tgt, c.h_tgt + off, n * 4, cudaMemcpyHostToDevice, nd.main));
         if (nd.needs_csr) CK(k::embed_csr(M, d.R(), nd.d_tok, nd.d_csr, nd.main));
         c.h2d += 2 * n * 4;
       }
@@ -610,11 +615,14 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       // lazy BRC while the replica's pool (cp.retain slots) has a free slot;
       // beyond that it runs in the scratch slot and keeps only its input and
       // output (the BRC recomputes the forward).
-      bool keep = true;
+      bool keep = true, swap = false;
       int slot;
       if (frc && cp.free_slots.empty() && cp.scratch) {
         keep = false;
         slot = kScratchSlot;
+        // host-swap tier: the saved set goes to pinned host memory instead
+        swap = cp.hnext < (int)cp.hslots.size();
+        if (cp.scratch_ev) wait_ev(s, cp.scratch_ev);   // the last swap-out read it
       } else {
         if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
         slot = cp.free_slots.back();
@@ -630,6 +638,14 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       if (c.recovering && !frc && X == c.rec_stage) ++c.frc_recomputed;
       cudaEvent_t e = record(nd, s);
       nd.store[{K_SAVED, X, k}] = {nullptr, e, keep ? slot : -1};
+      if (swap) {
+        const int h = cp.hnext++;
+        wait_ev(nd.swap, e);
+        CK(cudaMemcpyAsync(cp.hslots[h], cp.scratch, c.stages[X].slot_bytes,
+                           cudaMemcpyDeviceToHost, nd.swap));
+        cp.scratch_ev = record(nd, nd.swap);
+        nd.store[{K_SAVED, X, k}] = {cp.hslots[h], cp.scratch_ev, kHostSlot0 - h};
+      }
       if (X < P - 1)
         nd.store[{K_ACT, X + 1, k}] = {out, e};
       else
@@ -656,7 +672,15 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       void *dx = X > 0 ? arena_alloc(nd, msg_bytes(c, MSG_GRAD, X)) : nullptr;
       TMark tm(c, nd, s, brc ? 1 : 2);
       int slot = sv.slot;
-      if (slot < 0) {
+      if (slot <= kHostSlot0) {
+        // swapped to the host: copy it back into a device slot
+        if (cp.free_slots.empty()) throw RtError{BB_E_STATE, "saved-set pool exhausted"};
+        slot = cp.free_slots.back();
+        cp.free_slots.pop_back();
+        CK(cudaMemcpyAsync(slot_base(cp, slot), sv.p, c.stages[X].slot_bytes,
+                           cudaMemcpyHostToDevice, s));
+        if (c.recovering) ++c.frc_swapped;
+      } else if (slot < 0) {
         // an FRC saved set beyond the retention budget: recompute the forward
         // from the retained stage input (same kernels, same order: the saved
         // set is bit-identical to the one FNC / FRC produced)
@@ -679,7 +703,9 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
     case SEND_GRAD:
     case SEND_DGRAD:
     case RESEND_GRAD:
-    case REPLICA_SEND: {
+    case REPLICA_SEND:
+    case AR_SEND:
+    case RESEND_AR: {
       const Msg m = message_of(ins);
       const ChanKey ck{nd.n, ins.peer, (int)m.kind};
       if (ph.drop_to_victim && ins.peer == ph.victim) {
@@ -688,13 +714,18 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         auto it = c.victim_consumed.find(ck);
         if (it == c.victim_consumed.end() || sent > it->second) return true;
       }
-      const Entry &pl = need(nd, payload_key(ins));
+      Entry pl = need(nd, payload_key(ins));
+      // an all-reduce contribution is the local sum, never the total
+      if (m.kind == MSG_AR) pl.p = nd.copies.at(X).grad;
       const size_t bytes = msg_bytes(c, m.kind, m.stage);
-      if (c.recovering && (ins.kind == RESEND_GRAD || (ins.kind == SEND_ACT && X == c.rec_stage)))
+      if (c.recovering && (ins.kind == RESEND_GRAD || ins.kind == RESEND_AR ||
+                           (ins.kind == SEND_ACT && X == c.rec_stage)))
         c.bytes_rerouted += bytes;
       if (is_local(c, ins.peer)) {
         Node &dst = c.nodes.at(ins.peer);
-        void *dp = m.kind == MSG_GRADSUM ? (void *)dst.copies.at(X).grad : arena_alloc(dst, bytes);
+        void *dp = m.kind == MSG_GRADSUM ? (void *)dst.copies.at(X).grad
+                   : m.kind == MSG_AR    ? (void *)dst.copies.at(X).ar_in.at(nd.n / P)
+                                         : arena_alloc(dst, bytes);
         wait_ev(nd.main, pl.ev);
         // the receiver's step-start memset of that buffer ran on ITS stream:
         // order this cross-node write after it explicitly
@@ -715,7 +746,8 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
     case RECV_ACT:
     case RECV_GRAD:
     case RECV_DGRAD:
-    case REPLICA_RECV: {
+    case REPLICA_RECV:
+    case AR_RECV: {
       const Msg m = message_of(ins);
       const ChanKey ck{ins.peer, nd.n, (int)m.kind};
       Entry got;
@@ -744,21 +776,40 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       }
       if (ins.kind == RECV_ACT)
         nd.store[{K_ACT, X, k}] = got;
+      else if (ins.kind == AR_RECV)
+        nd.store[{K_AR, X, ins.peer / P}] = got;   // a shadow's stays its pipeline's
       else if (ins.kind == RECV_GRAD || ins.kind == RECV_DGRAD)
         nd.store[{K_DACT, X + 1, k}] = got;
       else
         nd.store[{K_GRADSUM, X, 0}] = {nd.copies.at(X).grad, got.ev};
       return true;
     }
+    case AR_SUM: {
+      // the D contributions in ascending pipeline order: every
+      // pipeline adds the same operands in the same order, same bits
+      Copy &cp = nd.copies.at(X);
+      std::vector<const float *> src(d.D);
+      const int own = nd.n / P;
+      for (int e = 0; e < d.D; ++e) {
+        const Entry &en = need(nd, e == own ? Key{K_GRADSUM, X, 0} : Key{K_AR, X, e});
+        wait_ev(nd.main, en.ev);
+        src[e] = e == own ? cp.grad : (const float *)en.p;
+      }
+      CK(k::sum_pipelines(c.stages[X].pcount, src.data(), d.D, cp.arsum, nd.main));
+      nd.store[{K_GRADSUM, X, 0}] = {cp.arsum, record(nd, nd.main)};
+      return true;
+    }
     case APPLY: {
       Copy &cp = nd.copies.at(X);
-      wait_ev(nd.main, need(nd, {K_GRADSUM, X, 0}).ev);
+      const Entry gs = need(nd, {K_GRADSUM, X, 0});   // the local sum, or the total (D > 1)
+      wait_ev(nd.main, gs.ev);
       wait_ev(nd.main, record(nd, nd.frc));   // the FRC stream read these parameters
       cp.t += 1;
       const double b1 = c.o.beta1, b2 = c.o.beta2;
       const float bc1 = (float)(1.0 - std::pow(b1, cp.t)), bc2 = (float)(1.0 - std::pow(b2, cp.t));
       Prof pf(c, nd, nd.main, PC_ADAM, 16.0 * c.stages[X].pcount);
-      CK(k::adam(c.stages[X].pcount, cp.master, cp.grad, cp.m, cp.v, c.bf16 ? cp.work : nullptr,
+      CK(k::adam(c.stages[X].pcount, cp.master, (const float *)gs.p, cp.m, cp.v,
+                 c.bf16 ? cp.work : nullptr,
                  c.o.lr, c.o.beta1, c.o.beta2, c.o.eps, bc1, bc2, nd.main));
       return true;
     }
@@ -935,6 +986,7 @@ void sync_all(Ctx &c, bool comm_too) {
   for (auto &kv : c.nodes) {
     CK(cudaStreamSynchronize(kv.second.main));
     CK(cudaStreamSynchronize(kv.second.frc));
+    if (kv.second.swap) CK(cudaStreamSynchronize(kv.second.swap));
   }
   if (comm_too)
     for (auto &kv : c.x.edges)
@@ -959,6 +1011,10 @@ void begin_step(Ctx &c) {
   for (auto &kv : c.nodes) {
     Node &nd = kv.second;
     if (!nd.alive) continue;
+    for (auto &cc : nd.copies) {   // host-swap slots are free again (sync_all at step end)
+      cc.second.hnext = 0;
+      cc.second.scratch_ev = nullptr;
+    }
     nd.evnext = 0;
     nd.store.clear();
     nd.arena_used = 0;
@@ -994,16 +1050,34 @@ void stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
   const size_t R = d.R();
   // ids index the embedding / head rows on the device: reject out-of-range
   // ids here rather than read or write outside the tensors
-  for (size_t i = 0; i < (size_t)d.M * R; ++i)
+  const size_t n = (size_t)d.D * d.M * R;   // every pipeline's micro-batches
+  for (size_t i = 0; i < n; ++i)
     if (tok[i] < 0 || tok[i] >= d.V || tgt[i] < 0 || tgt[i] >= d.V)
       throw RtError{BB_E_INVAL, "token or target id outside [0, vocab)"};
-  std::memcpy(c.h_tok, tok, (size_t)d.M * R * 4);
-  std::memcpy(c.h_tgt, tgt, (size_t)d.M * R * 4);
+  std::memcpy(c.h_tok, tok, n * 4);
+  std::memcpy(c.h_tgt, tgt, n * 4);
 }
 
+float read_loss_of(Ctx &c, int pipe);
+
+// The step's loss: the sum of the local pipelines' shares (each is its
+// micro-batches' token CE over the whole batch's token count); NaN without a
+// local last stage.
 float read_loss(Ctx &c) {
+  float sum = 0.f;
+  bool any = false;
+  for (int p = 0; p < c.d.D; ++p) {
+    const float l = read_loss_of(c, p);
+    if (std::isnan(l) && !c.nodes.count(c.topo.host[p * c.d.P + c.d.P - 1])) continue;
+    sum += l;
+    any = true;
+  }
+  return any ? sum : NAN;
+}
+
+float read_loss_of(Ctx &c, int pipe) {
   const int X = c.d.P - 1;
-  const int n = c.topo.host[X];
+  const int n = c.topo.host[pipe * c.d.P + X];
   if (!c.nodes.count(n) || !c.nodes.at(n).alive) return NAN;
   Node &nd = c.nodes.at(n);
   Copy &cp = nd.copies.at(X);
@@ -1258,6 +1332,12 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     if (m->d_model / m->n_head != 64 && m->d_model / m->n_head != 32)
       throw RtError{BB_E_UNSUPPORTED, "attention kernels take head dim 64 (or 32)"};
     if (c.o.micro_batch < 1) throw RtError{BB_E_INVAL, "micro_batch < 1"};
+    const int D = c.o.pipelines < 1 ? 1 : c.o.pipelines, N = D * P;   // pipelines, nodes
+    if (D > k::kMaxPipelines) throw RtError{BB_E_UNSUPPORTED, "at most 8 pipelines"};
+    if (D > 1 && c.o.rc == BB_RC_EFEB)
+      throw RtError{BB_E_UNSUPPORTED, "EFEB with more than one pipeline is not built"};
+    if (D > 1 && c.o.detect_ms > 0)
+      throw RtError{BB_E_UNSUPPORTED, "fail-stop detection with more than one pipeline"};
     if (c.o.detect_ms > 0 && (c.o.world_size != P || c.o.node_rank))
       // a process death takes all its nodes: only one node per rank is recoverable
       throw RtError{BB_E_INVAL, "fail-stop mode needs one node per rank (world_size == stages)"};
@@ -1265,17 +1345,17 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       // the transposed (MN-major) operands of dX / dW need >= 64 rows
       throw RtError{BB_E_UNSUPPORTED, "bf16 path needs d_model >= 64"};
     c.d = {m->n_layer, m->d_model, m->n_head, m->d_ff, m->vocab, m->seq_len, m->causal ? 1 : 0,
-           P, M, c.o.micro_batch};
+           P, M, c.o.micro_batch, D};
     c.bf16 = c.o.prec == BB_PREC_BF16;
     c.act_bytes = c.bf16 ? 2 : 4;
     const bool rc = c.o.rc != BB_RC_NONE;
     try {
       c.ranges = partition(m->n_layer, P, c.o.layers_per_stage);
-      c.plans = normal_plans(P, M, (int)c.o.rc);
+      c.plans = normal_plans(P, M, (int)c.o.rc, D);
     } catch (const PlanError &e) {
       throw RtError{BB_E_INVAL, e.msg};
     }
-    c.topo = normal_topology(P, rc);
+    c.topo = normal_topology(P, rc, D);
     for (int X = 0; X < P; ++X) {
       c.stages.push_back(make_stage(c.d, X, c.ranges[X].first, c.ranges[X].second));
       layout_slots(c.d, c.act_bytes, c.stages.back());
@@ -1283,26 +1363,27 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     auto ur = unit_param_ranges(c.d);
     c.total_params = ur.back().first + ur.back().second;
     // node -> rank
-    c.node_rank.resize(P);
-    const int per = (P + c.o.world_size - 1) / c.o.world_size;
-    for (int n = 0; n < P; ++n) {
+    c.node_rank.resize(N);
+    const int per = (N + c.o.world_size - 1) / c.o.world_size;
+    for (int n = 0; n < N; ++n) {
       c.node_rank[n] = c.o.node_rank ? c.o.node_rank[n] : std::min(n / per, c.o.world_size - 1);
       if (c.node_rank[n] < 0 || c.node_rank[n] >= c.o.world_size)
         throw RtError{BB_E_INVAL, "bad node_rank"};
     }
-    c.node_device.assign(P, 0);
-    for (int n = 0; n < P; ++n) c.node_device[n] = c.node_rank[n];
+    c.node_device.assign(N, 0);
+    for (int n = 0; n < N; ++n) c.node_device[n] = c.node_rank[n];
     CK(cudaSetDevice(c.o.device));
     const size_t R = c.d.R();
     c.csr_stride = k::embed_csr_ints((int)R);
-    CK(cudaMallocHost(&c.h_tok, (size_t)M * R * 4));
-    CK(cudaMallocHost(&c.h_tgt, (size_t)M * R * 4));
+    CK(cudaMallocHost(&c.h_tok, (size_t)D * M * R * 4));
+    CK(cudaMallocHost(&c.h_tgt, (size_t)D * M * R * 4));
     int lo_prio = 0, hi_prio = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     const size_t act = R * c.d.H * c.act_bytes;
-    for (int n = 0; n < P; ++n) {
+    for (int n = 0; n < N; ++n) {
       if (c.node_rank[n] != c.o.world_rank) continue;
       Node &nd = c.nodes[n];
+      const int sn = n % P;   // the node's stage
       nd.n = n;
       if (c.o.profile) {
         // profiling: every local node issues into one serialised stream so
@@ -1316,8 +1397,8 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       CK(cudaEventCreate(&nd.t0));
       CK(cudaEventCreate(&nd.t1));
       CK(cudaEventCreateWithFlags(&nd.ev_begin, cudaEventDisableTiming));
-      std::vector<std::pair<int, bool>> hosted{{n, false}};
-      if (rc) hosted.push_back({(n + 1) % P, true});
+      std::vector<std::pair<int, bool>> hosted{{sn, false}};
+      if (rc) hosted.push_back({(sn + 1) % P, true});
       for (auto &h : hosted) {
         const int X = h.first;
         const StageInfo &si = c.stages[X];
@@ -1333,6 +1414,12 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           grow_slots(cp, std::min(M, P - X), si.slot_bytes);
         }
         if (X == P - 1) cp.loss = (float *)dmalloc(M * 4);
+        if (D > 1) {   // a replica may be promoted: its node then runs the all-reduce
+          cp.arsum = (float *)dmalloc(si.pcount * 4);
+          cp.ar_in.assign(D, nullptr);
+          for (int e = 0; e < D; ++e)
+            if (e != n / P) cp.ar_in[e] = (float *)dmalloc(si.pcount * 4);
+        }
       }
       // normal 1F1B step: FWD / FRC outputs, BWD input-gradients, local receives
       nd.arena_bytes = (size_t)(6 * M + 8) * al(act);
@@ -1357,7 +1444,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
       nd.d_csr = (int32_t *)dmalloc((size_t)M * c.csr_stride * 4);
       // the embedding backward runs where a copy of stage 0 lives (its own
       // node, the replica holder for a lazy BRC)
-      nd.needs_csr = n == 0 || (rc && n == P - 1);
+      nd.needs_csr = sn == 0 || (rc && sn == P - 1);
     }
     // Cross-rank edges, set up before the retention pools so an automatic
     // FRC budget sees the receive arenas: one per (src node, dst node, kind) whose endpoints
@@ -1366,33 +1453,44 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     if (c.o.world_size > 1) {
       if (!c.o.session_id) throw RtError{BB_E_INVAL, "session_id required for world_size > 1"};
       std::set<std::tuple<int, int, int>> want;
+      // node of pipeline p's stage s (ring inside the pipeline)
+      auto node = [&](int p, int s) { return p * P + ((s % P) + P) % P; };
       auto add = [&](int a, int b, int kind) {
-        a = (a % P + P) % P;
-        b = (b % P + P) % P;
         if (a != b && c.node_rank[a] != c.node_rank[b]) want.insert({a, b, kind});
       };
-      for (int a = 0; a < P; ++a) {
-        if (a < P - 1) add(a, a + 1, MSG_ACT);
-        add(a, a + 2, MSG_ACT);
-        if (a > 0) add(a, a - 1, MSG_GRAD);
-        add(a, a - 2, MSG_GRAD);
-        add(a, a - 1, MSG_GRADSUM);
-        add(a, a + 1, MSG_STATE);   // rejoin: shadow -> returning node
-        add(a, a - 1, MSG_STATE);   // rejoin: successor -> returning node
-        if (c.o.rc == BB_RC_EFEB) {   // eager-BRC gradients; after a loss the shadow
-          add(a, a - 2, MSG_DGRAD);    // takes over the victim's (one hop back)
-          add(a, a - 1, MSG_DGRAD);
+      for (int p = 0; p < D; ++p)
+        for (int s = 0; s < P; ++s) {
+          const int a = node(p, s);
+          if (s < P - 1) add(a, node(p, s + 1), MSG_ACT);
+          add(a, node(p, s + 2), MSG_ACT);
+          if (s > 0) add(a, node(p, s - 1), MSG_GRAD);
+          add(a, node(p, s - 2), MSG_GRAD);
+          add(a, node(p, s - 1), MSG_GRADSUM);
+          add(node(p, s - 1), a, MSG_STATE);   // rejoin: shadow -> returning node
+          add(node(p, s + 1), a, MSG_STATE);   // rejoin: successor -> returning node
+          if (c.o.rc == BB_RC_EFEB) {   // eager-BRC gradients; after a loss the shadow
+            add(a, node(p, s - 2), MSG_DGRAD);    // takes over the victim's (one hop back)
+            add(a, node(p, s - 1), MSG_DGRAD);
+          }
+          // all-reduce partners, and the shadow that stands in for a lost one
+          for (int q = 0; q < D; ++q) {
+            if (q == p) continue;
+            add(a, node(q, s), MSG_AR);
+            add(a, node(q, s - 1), MSG_AR);
+            add(node(q, s - 1), a, MSG_AR);
+          }
         }
-      }
       size_t gmax = 0;
       for (auto &st : c.stages) gmax = std::max(gmax, st.pcount);
       const std::vector<size_t> slot_bytes{act, act, gmax * sizeof(float),
-                                           3 * gmax * sizeof(float), act};
+                                           3 * gmax * sizeof(float), act, gmax * sizeof(float)};
       // rejoin sends one state message per edge, two when P == 2 (the shadow
       // and the successor are the same node)
-      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, P == 2 ? 2 : 1, 2 * M + 4};
+      // (all-reduce: one contribution per stage and step; two when both ends
+      // are shadows of the same lost stage and also exchange their own)
+      const std::vector<int> caps{2 * M + 4, 2 * M + 4, 4, P == 2 ? 2 : 1, 2 * M + 4, 2};
       const std::vector<std::tuple<int, int, int>> wl(want.begin(), want.end());
-      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, P, wl, c.node_rank,
+      const std::string xe = xport_init(c.x, c.o.world_rank, c.o.world_size, N, wl, c.node_rank,
                                         slot_bytes, caps, c.o.session_id, hi_prio,
                                         /*callback_mode=*/c.o.detect_ms > 0);
       if (!xe.empty()) throw RtError{BB_E_CUDA, "transport init: " + xe};
@@ -1427,6 +1525,14 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           if (frc && full < M) {
             cp.scratch = (char *)dmalloc(si.slot_bytes);
             cp.chunks.push_back({cp.scratch, si.slot_bytes});
+            // host-swap tier for the rest
+            const size_t nh = std::min<size_t>(M - full, c.o.frc_swap_bytes / si.slot_bytes);
+            if (nh > 0) {
+              CK(cudaHostAlloc(&cp.hbase, nh * si.slot_bytes, cudaHostAllocDefault));
+              for (size_t i = 0; i < nh; ++i) cp.hslots.push_back(cp.hbase + i * si.slot_bytes);
+              Node &hn = c.nodes.at(kv.first);
+              if (!hn.swap) CK(cudaStreamCreateWithFlags(&hn.swap, cudaStreamNonBlocking));
+            }
           }
         }
     }
@@ -1616,8 +1722,9 @@ bb_status rt_stage_inputs(Ctx &c, const int32_t *tok, const int32_t *tgt) {
     const size_t n = (size_t)c.d.M * c.d.R();
     for (auto &kv : c.nodes) {
       Node &nd = kv.second;
-      CK(cudaMemcpy(nd.d_tok, c.h_tok, n * 4, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(nd.d_tgt, c.h_tgt, n * 4, cudaMemcpyHostToDevice));
+      const size_t off = (size_t)(nd.n / c.d.P) * n;   // the node's pipeline's share
+      CK(cudaMemcpy(nd.d_tok, c.h_tok + off, n * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(nd.d_tgt, c.h_tgt + off, n * 4, cudaMemcpyHostToDevice));
       if (nd.needs_csr) CK(k::embed_csr(c.d.M, c.d.R(), nd.d_tok, nd.d_csr, nd.main));
       CK(cudaStreamSynchronize(nd.main));
     }
@@ -1635,8 +1742,8 @@ bb_status rt_preempt(Ctx &c, int stage, int at_instr) {
     c.err = "recovery pending";
     return BB_E_STATE;
   }
-  if (stage < 0 || stage >= c.d.P) {
-    c.err = "unknown stage";
+  if (stage < 0 || stage >= c.d.D * c.d.P) {
+    c.err = "unknown node";
     return BB_E_INVAL;
   }
   if (c.o.rc == BB_RC_NONE || !recoverable(c.d.P, c.topo, c.victims, stage)) {
@@ -1663,7 +1770,7 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
   const double t0 = now_ms();
   try {
     if (!c.interrupted) throw RtError{BB_E_STATE, "no interrupted step"};
-    const int P = c.d.P, M = c.d.M, v = c.inj_v, u = (v - 1 + P) % P;
+    const int P = c.d.P, M = c.d.M, v = c.inj_v, u = ring_prev(P, v), sv = v % P;
     try {
       c.continuation = recovery_plans(c.plans, P, M, v, c.cut.pcs, c.cut.ch, &c.rinfo);
     } catch (const PlanError &e) {
@@ -1682,10 +1789,10 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
     // promoted pool must also hold the victim stage's 1F1B stash (min(M, P-v)
     // in flight) and one BRC re-forward next to the retained FRC saved sets.
     if (c.nodes.count(u)) {
-      Copy &cp = c.nodes.at(u).copies.at(v);
+      Copy &cp = c.nodes.at(u).copies.at(sv);
       cp.replica = false;
-      const int need = std::min(M, cp.retain + std::min(M, P - v) + 1);
-      const size_t sb = c.stages[v].slot_bytes;
+      const int need = std::min(M, cp.retain + std::min(M, P - sv) + 1);
+      const size_t sb = c.stages[sv].slot_bytes;
       try {
         grow_slots(cp, need - cp.nslots(), sb);
       } catch (const RtError &e) {
@@ -1698,8 +1805,9 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
     }
     Phase ph;
     c.recovering = true;
-    c.rec_stage = v;
+    c.rec_stage = sv;
     c.frc_recomputed = 0;
+    c.frc_swapped = 0;
     c.bytes_rerouted = 0;
     run(c, c.continuation, nullptr, ph);
     c.recovering = false;
@@ -1734,6 +1842,7 @@ bb_status rt_recover(Ctx &c, bb_recovery_stats *r) {
       r->interrupted_step_ms = c.last_step_ms;
       r->frc_recomputed_mb = c.frc_recomputed;
       r->bytes_resent = c.bytes_rerouted;
+      r->frc_swapped_mb = c.frc_swapped;
     }
     return BB_OK;
   } catch (const RtError &e) {
@@ -1757,12 +1866,13 @@ bb_status rt_rejoin(Ctx &c) {
     c.x.barrier();
     // the most recent victim returns first (LIFO): the plans and topology
     // go back to those in force before its preemption
-    const int P = c.d.P, v = c.victims.back(), u = (v - 1 + P) % P, w = (v + 1) % P;
+    const int P = c.d.P, v = c.victims.back(), u = ring_prev(P, v), w = ring_next(P, v);
+    const int sv = v % P, sw = w % P;   // stages of the returning node and its successor
     auto parts = [&](Copy &cp) {
       return std::vector<float *>{cp.master, cp.m, cp.v};
     };
     // senders
-    for (auto pr : std::vector<std::pair<int, int>>{{u, v}, {w, w}}) {
+    for (auto pr : std::vector<std::pair<int, int>>{{u, sv}, {w, sw}}) {
       const int from = pr.first, X = pr.second;
       if (!c.nodes.count(from)) continue;
       Node &src = c.nodes.at(from);
@@ -1788,7 +1898,7 @@ bb_status rt_rejoin(Ctx &c) {
     // the returning node
     if (c.nodes.count(v)) {
       Node &nd = c.nodes.at(v);
-      for (auto pr : std::vector<std::pair<int, int>>{{u, v}, {w, w}}) {
+      for (auto pr : std::vector<std::pair<int, int>>{{u, sv}, {w, sw}}) {
         const int from = pr.first, X = pr.second;
         Copy &dc = nd.copies.at(X);
         const size_t n = c.stages[X].pcount;
@@ -1810,13 +1920,13 @@ bb_status rt_rejoin(Ctx &c) {
         if (c.bf16) CK(k::cast_f32_to_bf16(n, dc.master, dc.work, nd.main));
         CK(cudaMemsetAsync(dc.grad, 0, n * 4, nd.main));
         dc.t = (int)c.adam_steps;   // every stage took one Adam step per step since load
-        dc.replica = X != v;
+        dc.replica = X != sv;
       }
       nd.alive = true;
     }
     if (c.nodes.count(u)) {
       // the shadow's copy is a replica again: back to its retention pool
-      Copy &cp = c.nodes.at(u).copies.at(v);
+      Copy &cp = c.nodes.at(u).copies.at(sv);
       cp.replica = true;
       const bool scr = cp.scratch != nullptr;
       free_slots_all(cp);
@@ -1840,10 +1950,19 @@ bb_status rt_rejoin(Ctx &c) {
 
 bb_status rt_read_state(Ctx &c, int X, int replica, int what, float *host, size_t n) {
   try {
-    if (X < 0 || X >= c.d.P) throw RtError{BB_E_INVAL, "bad stage"};
-    const int node = replica ? c.topo.replica_on[X] : c.topo.host[X];
-    if (node < 0 || !c.nodes.count(node) || !c.nodes.at(node).alive)
-      throw RtError{BB_E_INVAL, "copy not hosted by this process"};
+    if (X < 0 || X >= c.d.D * c.d.P) throw RtError{BB_E_INVAL, "bad stage"};
+    // X < P: the lowest pipeline whose copy this process hosts (D > 1: the
+    // copies of a stage are identical across pipelines, except grads = the
+    // local sums); X = d*P + s: pipeline d's copy of stage s
+    const int p0 = X < c.d.P ? 0 : X / c.d.P, p1 = X < c.d.P ? c.d.D : p0 + 1;
+    X %= c.d.P;
+    int node = -1;
+    for (int p = p0; p < p1 && node < 0; ++p) {
+      const int g = p * c.d.P + X;
+      const int nn = replica ? c.topo.replica_on[g] : c.topo.host[g];
+      if (nn >= 0 && c.nodes.count(nn) && c.nodes.at(nn).alive) node = nn;
+    }
+    if (node < 0) throw RtError{BB_E_INVAL, "copy not hosted by this process"};
     Copy &cp = c.nodes.at(node).copies.at(X);
     if (n != c.stages[X].pcount) throw RtError{BB_E_INVAL, "size mismatch"};
     const float *src = what == BB_STATE_PARAMS ? cp.master
@@ -2000,6 +2119,9 @@ void rt_destroy(Ctx &c) {
       if (c.bf16) cudaFree(cp.work);
       free_slots_all(cp);
       if (cp.loss) cudaFree(cp.loss);
+      cudaFree(cp.arsum);
+      for (auto p : cp.ar_in) cudaFree(p);
+      if (cp.hbase) cudaFreeHost(cp.hbase);
     }
     cudaFree(nd.arena);
     for (auto &sc : nd.sc) {
@@ -2024,6 +2146,7 @@ void rt_destroy(Ctx &c) {
       cudaStreamDestroy(nd.main);
       cudaStreamDestroy(nd.frc);
     }
+    if (nd.swap) cudaStreamDestroy(nd.swap);
   }
   for (auto e : c.prof_pool) cudaEventDestroy(e);
   if (c.serial) cudaStreamDestroy(c.serial);

@@ -28,6 +28,7 @@ namespace bb {
 struct Dims {
   int L, H, nh, F, V, S, causal;
   int P, M, mb;
+  int D = 1;   // data-parallel pipelines (node d*P + s)
   int R() const { return mb * S; }
   int d() const { return H / nh; }
 };
@@ -75,12 +76,24 @@ struct Copy {
   std::vector<int> free_slots;
   int retain = 0;              // FRC saved sets kept per step (replica; budget, Q10)
   float *loss = nullptr;  // [M] per-micro-batch losses (stage P-1 only)
+  // D > 1: the all-reduced total (AR_SUM writes it, the replica sync and
+  // Adam read it; grad keeps the local sum so it can be re-sent) and the
+  // receive buffers of the other pipelines' contributions from local nodes
+  float *arsum = nullptr;
+  std::vector<float *> ar_in;
+  // host-swap tier (opts.frc_swap_bytes): pinned host slots for the
+  // FRC saved sets beyond the HBM budget, handed out in order each step
+  char *hbase = nullptr;
+  std::vector<char *> hslots;
+  int hnext = 0;
+  cudaEvent_t scratch_ev = nullptr;   // the scratch slot's last swap-out (this step)
 };
 
 struct Node {
   int n = -1;
   bool alive = true;
   cudaStream_t main = nullptr, frc = nullptr;
+  cudaStream_t swap = nullptr;   // device -> host copies of swapped FRC saved sets
   std::map<int, Copy> copies;
   std::map<Key, Entry> store;
   char *arena = nullptr;
@@ -181,6 +194,7 @@ struct Ctx {
   bool recovering = false;      // inside bb_recover's continuation
   int rec_stage = -1;           // the victim's stage (recovery accounting)
   int frc_recomputed = 0;       // forwards recomputed by the current recovery
+  int frc_swapped = 0;          // saved sets the current recovery copied back from the host
   uint64_t bytes_rerouted = 0;  // bytes resent / rerouted by the current recovery
 };
 

@@ -7,6 +7,7 @@ preemption, and saves each rank's hosted stage states to <out>/rank<r>.npz.
 The harness process group is gloo (host-side id broadcast and barriers only;
 the library never uses it)."""
 import argparse
+import dataclasses
 import os
 
 # Every node has a main + FRC stream and every NCCL edge its own stream:
@@ -40,6 +41,7 @@ def main():
     ap.add_argument("--events", default="", help="t:v:pi or t:rejoin, comma separated")
     ap.add_argument("--failstop", default="", help="t:v:pi — fail-stop loss armed on v's rank only")
     ap.add_argument("--detect", type=int, default=0, help="bb_opts.detect_ms")
+    ap.add_argument("--pipelines", type=int, default=1, help="bb_opts.pipelines (D)")
     a = ap.parse_args()
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -52,7 +54,7 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     p = bb.Pipeline(cfg.model, P, cfg.microbatches, micro_batch=cfg.micro_batch, rc=a.rc,
                     prec=a.prec, lr=1e-4, world_rank=rank, world_size=ws, device=dev,
-                    session_id=obj[0], detect_ms=a.detect)
+                    session_id=obj[0], detect_ms=a.detect, pipelines=a.pipelines)
     p.load_params(make_params(cfg.model))
     losses, rec = [], None
     events = {}
@@ -62,8 +64,9 @@ def main():
     if a.victim >= 0:
         events[0] = (a.victim, a.pi)
     fs = tuple(int(x) for x in a.failstop.split(":")) if a.failstop else None
+    bcfg = dataclasses.replace(cfg, microbatches=a.pipelines * cfg.microbatches)
     for t in range(a.steps):
-        tok, tgt = make_tokens(cfg, t)
+        tok, tgt = make_tokens(bcfg, t)   # D*M micro-batches
         if fs is not None and fs[0] == t and fs[1] == rank:   # one node per rank
             p.preempt(fs[1], fs[2])
             status, st = p.step(tok, tgt)
@@ -89,7 +92,7 @@ def main():
         out["rec"] = np.array([rec.victim, rec.shadow, rec.commit, rec.brc_mb, rec.frc_done_mb,
                                rec.resent_mb, rec.frc_recomputed_mb], np.int64)
         out["rec_loss"] = np.float32(rec.loss)
-    for s in range(P):
+    for s in range(P * a.pipelines):   # d*P + s: pipeline d's copy
         for what in ("params", "grads", "adam_m", "adam_v"):
             try:
                 out[f"{what}_{s}"] = p.read_state(s, what)

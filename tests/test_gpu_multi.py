@@ -150,3 +150,49 @@ def test_multi_process_modes_bitwise(mode):
             assert got and all(g == float(losses[t]) for g in got), (mode, extra, t)
         for w in state:
             assert np.array_equal(merged(ranks, 3, w), state[w]), (mode, extra, w)
+
+
+def single_dp(cfg, D, steps):
+    """D pipelines in one process, failure-free: per-step losses and every
+    pipeline's copy of every stage (index d*P + s)."""
+    import dataclasses
+    import paper_2204_12013_b200 as bb
+    p = bb.Pipeline(cfg.model, cfg.stages, cfg.microbatches, micro_batch=cfg.micro_batch, rc=True,
+                    lr=1e-4, pipelines=D)
+    p.load_params(make_params(cfg.model))
+    bcfg = dataclasses.replace(cfg, microbatches=D * cfg.microbatches)
+    losses = []
+    for t in range(steps):
+        status, st = p.step(*make_tokens(bcfg, t))
+        losses.append(st.loss)
+    G = D * cfg.stages
+    state = {w: np.concatenate([p.read_state(g, w) for g in range(G)])
+             for w in ("params", "grads", "adam_m", "adam_v")}
+    p.close()
+    return losses, state
+
+
+@pytest.mark.parametrize("n,victim,pi", [(4, -1, 0), (2, -1, 0), (4, 3, 12), (4, 0, 30),
+                                         (2, 1, 25)])
+def test_multi_process_dp_bitwise(n, victim, pi):
+    """D=2 pipelines of P=2 (4 nodes) over n processes: n=4 puts every edge
+    (activations, gradients, replica sync, all-reduce) across processes;
+    n=2 gives each process one pipeline, so only the all-reduce crosses. The
+    per-rank loss shares add up to the single-process loss and every
+    pipeline's state equals the single-process D=2 run bit for bit, also
+    after a preemption (the other pipeline's all-reduce waits for the
+    victim's shadow, which replays it)."""
+    cfg = get_config("C0")
+    D, P = 2, cfg.stages
+    losses, state = single_dp(cfg, D, 2)
+    extra = {"victim": victim, "pi": pi} if victim >= 0 else {}
+    ranks = run_mp(n, config="C0", stages=P, steps=2, pipelines=D, **extra)
+    for t in range(2):
+        parts = [np.float32(r["losses"][t]) for r in ranks if not np.isnan(r["losses"][t])]
+        assert len(parts) == D, parts   # one share per pipeline, on its last stage's rank
+        tot = np.float32(0)
+        for x in parts:
+            tot = np.float32(tot + x)
+        assert tot == np.float32(losses[t]), (t, parts, losses[t])
+    for w in state:
+        assert np.array_equal(merged(ranks, D * P, w), state[w]), w

@@ -385,6 +385,35 @@ def test_frc_retention_budget_recovery_bitwise(budget):
             p.close()
 
 
+@pytest.mark.parametrize("host_sets", [2, 100])
+def test_frc_host_swap_recovery_bitwise(host_sets):
+    """Host-swap tier (frc_swap_bytes, "swap out these data"): with one
+    saved set in HBM, the next `host_sets` FRC saved sets go to pinned host
+    memory and a lazy BRC copies them back; the rest (if any) are recomputed.
+    Bit-identical to full retention for every victim; the recovery reports
+    the saved sets it brought back."""
+    cfg = dataclasses.replace(get_config("C0"), stages=3, microbatches=6)
+    flat = make_params(cfg.model)
+    _, ref, _ = _run(cfg, flat, "bf16", 2)
+    probe = _gpu(cfg, flat, "bf16")
+    slot = max(probe.stage_memory(s)[0] for s in range(cfg.stages))
+    probe.close()
+    plans = opl.normal_plans(cfg.stages, cfg.microbatches, True)
+    swapped = 0
+    for v in range(cfg.stages):
+        for pi in (3, len(plans[v]) // 2, len(plans[v]) - 6):
+            p, got, rec = _run(cfg, flat, "bf16", 2, inject=(0, v, pi), frc_retain_bytes=slot,
+                               frc_swap_bytes=host_sets * slot)
+            for (la, sa), (lb, sb) in zip(got, ref):
+                assert la == lb, (v, pi)
+                for w in sa:
+                    assert np.array_equal(sa[w], sb[w]), (v, pi, w)
+            swapped += rec.frc_swapped_mb
+            assert rec.frc_swapped_mb <= host_sets
+            p.close()
+    assert swapped > 0
+
+
 def test_frc_tile_grid_bitwise_and_node_stats():
     """FRC GEMMs on one-CTA-per-tile grids (default) vs persistent grids:
     identical results bit for bit; per-node accounting is consistent."""

@@ -127,3 +127,34 @@ def test_cpp_recovery_matches_oracle_every_point(mode):
                     assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc=mode,
                                          micro_batch=1) == \
                         pl.recovery_dump(P, M, v, pi, rc=mode), (P, M, v, pi)
+
+
+@pytest.mark.parametrize("mode", ["none", "eflb", "lflb"])
+def test_cpp_dp_plans_match_oracle_every_point(mode):
+    """D > 1 data-parallel pipelines: normal dumps (with the
+    default rank layout over 1, 2 and D*P processes), failover dumps of every
+    node and the cut + continuation of every injection point agree with the
+    oracle's, including the other pipelines' re-sent all-reduce
+    contributions."""
+    m = dict(n_layer=6, d_model=64, n_head=2, d_ff=256, vocab=128, seq_len=32, causal=1)
+    for P, M, D in ((2, 1, 2), (2, 2, 2), (3, 2, 2), (2, 3, 3), (4, 2, 2)):
+        plans = pl.normal_plans(P, M, mode, D)
+        host, rep = pl.normal_topology(P, D)
+        if mode == "none":
+            rep = {g: None for g in host}
+        for ws in (1, 2, D * P):
+            per = -(-(D * P) // ws)
+            dev = {n: min(n // per, ws - 1) for n in range(D * P)}
+            assert bbl.plan_dump(m, P, M, rc=mode, micro_batch=1, pipelines=D, world_size=ws) == \
+                pl.dump(P, M, mode, pl.partition(6, P), plans, host, rep, dev), (P, M, D, ws)
+        if mode == "none":
+            continue
+        for v in range(D * P):
+            fh, fr = pl.failover_topology(P, v, D)
+            assert bbl.plan_dump(m, P, M, victim=v, rc=mode, micro_batch=1, pipelines=D) == \
+                pl.dump(P, M, mode, pl.partition(6, P), pl.failover_plans(P, M, v, plans),
+                        fh, fr, mode="failover", victim=v), (P, M, D, v)
+            for pi in range(len(plans[v]) + 1):
+                assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc=mode, micro_batch=1,
+                                     pipelines=D) == \
+                    pl.recovery_dump(P, M, v, pi, rc=mode, D=D), (P, M, D, v, pi)
