@@ -1605,8 +1605,11 @@ bb_status step_failstop(Ctx &c, bb_step_stats *st, double t0) {
     add_edge_sends(c, c.plans, nullptr);
     ++c.steps_done;
     ++c.adam_steps;
-    finish_stats(c, st, t0);
-    if (st) st->loss = read_loss(c);
+    {
+      const float loss = read_loss(c);   // its 4-byte read counts in d2h_bytes
+      finish_stats(c, st, t0);
+      if (st) st->loss = loss;
+    }
     return BB_OK;
   }
   // a node died: agree on the cut. Publish how far our nodes got, meet the
@@ -1671,8 +1674,11 @@ bb_status rt_step(Ctx &c, const int32_t *tok, const int32_t *tgt, bb_step_stats 
       sync_all(c, true);
       ++c.steps_done;
       ++c.adam_steps;
-      finish_stats(c, st, t0);
-      if (st) st->loss = read_loss(c);
+      {
+        const float loss = read_loss(c);   // its 4-byte read counts in d2h_bytes
+        finish_stats(c, st, t0);
+        if (st) st->loss = loss;
+      }
       return BB_OK;
     }
     // injected preemption: every rank computes the same cut (Q12/Q14)

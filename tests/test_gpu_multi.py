@@ -172,7 +172,7 @@ def single_dp(cfg, D, steps):
     return losses, state
 
 
-@pytest.mark.parametrize("n,victim,pi", [(4, -1, 0), (2, -1, 0), (4, 3, 12), (4, 0, 30),
+@pytest.mark.parametrize("n,victim,pi", [(4, -1, 0), (2, -1, 0), (4, 3, 12), (4, 0, 22),
                                          (2, 1, 25)])
 def test_multi_process_dp_bitwise(n, victim, pi):
     """D=2 pipelines of P=2 (4 nodes) over n processes: n=4 puts every edge
