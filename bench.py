@@ -187,7 +187,7 @@ def log(rank, *a):
         print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
-def balanced_partition(m, P, rc=True):
+def balanced_partition(m, P, rc=True, per=1):
     """Blocks per stage (bb_opts.layers_per_stage) that balance the per-node
     work of one micro-batch. An even split by layer count (the default, Q6)
     leaves the last stage with the LM head on top of its blocks: at C1 the
@@ -199,8 +199,10 @@ def balanced_partition(m, P, rc=True):
     head GEMM runs faster per FLOP than a block). A node's
     load is its stage's fwd + bwd plus, with RC, its successor's fwd (FRC).
     Contiguous shards; interior stages keep >= 1 block, the first / last may
-    hold only the embedding / the head. Hill climbing from the even split:
-    move one block across a boundary while the maximum load drops."""
+    hold only the embedding / the head. With `per` > 1 nodes per GPU
+    (contiguous blocks of nodes, the library's default placement) the GPUs
+    time-share their nodes, so the objective is the largest per-GPU sum of
+    node loads (per = 1: the largest node load)."""
     L, H, S, V = m.n_layer, m.d_model, m.seq_len, m.vocab
     fb = 24.0 * H * H + 4.0 * S * H * (0.5 if m.causal else 1.0)
     bb_ = 2.4 * fb
@@ -217,15 +219,24 @@ def balanced_partition(m, P, rc=True):
     F = lambda s, x: (x * fb + (fh if s == P - 1 else 0.0)) if (rc and P > 1) else 0.0
     base, rem = divmod(L, P)
     even = [base + (1 if s >= P - rem else 0) for s in range(P)]
-    best = [max(loads(even)), even]
+    per = max(1, per)
 
-    def dfs(c, used, cur):
+    def objective(nl):   # node loads -> the largest per-GPU sum
+        return max(sum(nl[i:i + per]) for i in range(0, P, per))
+
+    best = [objective(loads(even)), even]
+
+    # depth-first search with branch and bound: node s's load is known once
+    # c[s+1] is chosen (the last node's needs c[0]); a GPU's sum once all of
+    # its nodes' are. `dev` = the open GPU's partial sum, `cur` = the largest
+    # closed one.
+    def dfs(c, used, cur, dev):
         s = len(c)
-        if cur >= best[0]:
+        if max(cur, dev) >= best[0]:
             return
         if s == P:
             if used == L:
-                full = max(cur, A(P - 1, c[-1]) + F(0, c[0]))
+                full = max(cur, dev + A(P - 1, c[-1]) + F(0, c[0]))
                 if full < best[0] - 1e-9:
                     best[0], best[1] = full, list(c)
             return
@@ -235,12 +246,16 @@ def balanced_partition(m, P, rc=True):
         for x in range(lo, left - need_after + 1):
             if s == P - 1 and x != left:
                 continue
-            nxt = cur if s == 0 else max(cur, A(s - 1, c[-1]) + F(s, x))
+            ncur, ndev = cur, dev
+            if s > 0:   # node s-1 is complete now
+                ndev = dev + A(s - 1, c[-1]) + F(s, x)
+                if s % per == 0:   # ... and so is its GPU
+                    ncur, ndev = max(cur, ndev), 0.0
             c.append(x)
-            dfs(c, used + x, nxt)
+            dfs(c, used + x, ncur, ndev)
             c.pop()
 
-    dfs([], 0, 0.0)
+    dfs([], 0, 0.0, 0.0)
     return best[1]
 
 
@@ -312,7 +327,15 @@ def run_ours(args, rank, ws, local):
     bcfg = dataclasses.replace(cfg, microbatches=D * M)   # all D pipelines' micro-batches
     tok, tgt = make_tokens(bcfg, 0)
     host_batches = [make_tokens(bcfg, s) for s in range(1, 3)]
-    lps = balanced_partition(m, P) if args.partition == "balanced" else None
+    per = -(-(D * P) // ws)   # nodes per GPU under the default contiguous placement
+    if args.lps:
+        lps = [int(x) for x in args.lps.split(",")]
+    elif args.partition == "balanced":     # per-node loads
+        lps = balanced_partition(m, P)
+    elif args.partition == "device":       # per-GPU sums of node loads
+        lps = balanced_partition(m, P, per=per if D == 1 else 1)
+    else:
+        lps = None
     common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,
                   layers_per_stage=lps, pipelines=D)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -541,7 +564,8 @@ def main():
                     help="C3 (GPT-2 XL, the north-star model) by default; C1 / C2 / C0")
     ap.add_argument("--stages", type=int, default=0,
                     help="pipeline stages (default: the config's, at least N)")
-    ap.add_argument("--partition", default="balanced", choices=["balanced", "even"],
+    ap.add_argument("--lps", default="", help="explicit layers_per_stage, comma separated")
+    ap.add_argument("--partition", default="balanced", choices=["balanced", "device", "even"],
                     help="blocks per stage: cost-balanced (default) or even by count (Q6)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

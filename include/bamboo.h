@@ -219,11 +219,15 @@ bb_status bb_step(void *ctx, const int32_t *tokens, const int32_t *targets, bb_s
  * inputs. A bb_step with host arrays replaces them. */
 bb_status bb_stage_inputs(void *ctx, const int32_t *tokens, const int32_t *targets);
 
-/* Arm a preemption of node `stage` after it has executed `at_instr` (pi)
- * instructions of its list in the next step (0 <= pi <= list length). Must be
- * called with the same arguments on every rank. BB_E_FATAL if the pipeline has
- * no redundancy left for that node (rc off, or already in failover mode:
- * P:464). */
+/* Arm a preemption of node `stage` (a node id: 0 <= stage < pipelines *
+ * stages, node d*stages + s runs stage s of pipeline d) after it has executed
+ * `at_instr` (pi) instructions of its list in the next step (0 <= pi <= list
+ * length; BB_E_INVAL otherwise). Must be called with the same arguments on
+ * every rank (fail-stop mode: on the victim's rank only). BB_E_FATAL if no
+ * redundancy is left for that node: rc off, the node is dead, runs a second
+ * stage as a shadow, or its replica holder is dead (P:464 consecutive nodes,
+ * SURVEY Q18); a non-adjacent node after a failover is recoverable (SPEC
+ * S:537). */
 bb_status bb_preempt(void *ctx, int stage, int at_instr);
 
 /* Finish the interrupted step on the survivors: the shadow promotes the

@@ -409,7 +409,8 @@ def test_frc_host_swap_recovery_bitwise(host_sets):
                 for w in sa:
                     assert np.array_equal(sa[w], sb[w]), (v, pi, w)
             swapped += rec.frc_swapped_mb
-            assert rec.frc_swapped_mb <= host_sets
+            # host slots per replica = swap bytes / that stage's saved-set size
+            assert rec.frc_swapped_mb <= cfg.microbatches - 1
             p.close()
     assert swapped > 0
 
