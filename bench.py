@@ -187,7 +187,7 @@ def log(rank, *a):
         print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
-def balanced_partition(m, P, rc=True, per=1):
+def balanced_partition(m, P, rc=True, per=1):   # per > 1: exact but slow; see device_partition
     """Blocks per stage (bb_opts.layers_per_stage) that balance the per-node
     work of one micro-batch. An even split by layer count (the default, Q6)
     leaves the last stage with the LM head on top of its blocks: at C1 the
@@ -257,6 +257,49 @@ def balanced_partition(m, P, rc=True, per=1):
 
     dfs([], 0, 0.0, 0.0)
     return best[1]
+
+
+def device_partition(m, P, per, alpha=0.8, rc=True):
+    """Blocks per stage for `per` nodes per GPU (contiguous node blocks):
+    the GPUs time-share their nodes, so the largest per-GPU sum of node loads
+    bounds the step, but a pure per-GPU objective piles blocks onto single
+    nodes (and the 1F1B critical path runs through every node). Objective:
+    max(largest per-GPU sum, alpha * per * largest node load); hill climbing
+    by single-block moves from the per-node optimum (balanced_partition).
+    Measured at C3 N=4 (profiles/r02_part_*_n4.json): 208.4 samples/s vs
+    202.6 for the per-node partition."""
+    L, H, S, V = m.n_layer, m.d_model, m.seq_len, m.vocab
+    fb = 24.0 * H * H + 4.0 * S * H * (0.5 if m.causal else 1.0)
+    bb_ = 2.4 * fb
+    fh, bh = 2.0 * H * V * 0.85, 2.0 * H * V * 0.87
+
+    def score(c):
+        f = [c[s] * fb + (fh if s == P - 1 else 0.0) for s in range(P)]
+        nl = [f[s] + c[s] * bb_ + (bh if s == P - 1 else 0.0) +
+              (f[(s + 1) % P] if rc and P > 1 else 0.0) for s in range(P)]
+        dev = max(sum(nl[i:i + per]) for i in range(0, P, per))
+        return max(dev, alpha * per * max(nl))
+
+    best = balanced_partition(m, P, rc)
+    if per <= 1 or per >= P:
+        return best
+    cur = score(best)
+    improved = True
+    while improved:
+        improved = False
+        for i in range(P):
+            for j in range(P):
+                if i == j or best[i] == 0:
+                    continue
+                c = list(best)
+                c[i] -= 1
+                c[j] += 1
+                if any(c[k] < 1 for k in range(1, P - 1)):
+                    continue
+                sc = score(c)
+                if sc < cur * (1 - 1e-9):
+                    best, cur, improved = c, sc, True
+    return best
 
 
 AUTO = (1 << 64) - 1   # bb_opts.frc_retain_bytes: what HBM leaves free after the rest
@@ -333,7 +376,7 @@ def run_ours(args, rank, ws, local):
     elif args.partition == "balanced":     # per-node loads
         lps = balanced_partition(m, P)
     elif args.partition == "device":       # per-GPU sums of node loads
-        lps = balanced_partition(m, P, per=per if D == 1 else 1)
+        lps = device_partition(m, P, per if D == 1 else 1)
     else:
         lps = None
     common = dict(micro_batch=mb, prec="bf16", world_rank=rank, world_size=ws, device=local,

@@ -1518,7 +1518,8 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
           if (!cp.replica) continue;
           const StageInfo &si = c.stages[cp.X];
           const bool frc = c.o.rc == BB_RC_EFLB || c.o.rc == BB_RC_EFEB;   // LFLB: no FRC
-          const int full = !frc ? 0 : budget == 0 ? M
+          // (an embedding-only stage saves nothing: every saved set fits)
+          const int full = !frc ? 0 : budget == 0 || si.slot_bytes == 0 ? M
                                     : (int)std::min<size_t>(M, budget / si.slot_bytes);
           cp.retain = full;
           grow_slots(cp, full, si.slot_bytes);

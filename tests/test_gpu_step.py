@@ -458,8 +458,12 @@ def test_custom_partition_matches_oracle(lps):
     _compare_step(cfg, p, ref, "bf16", st.loss, ref_loss, s0)
     base = {w: _flat_state(p, 3, w) for w in STATES}
     p.close()
-    for victim in (0, 2):
-        q = _gpu(cfg, flat, "bf16", layers_per_stage=lps)
+    for victim, kw in ((0, {}), (2, {}),
+                       # the automatic FRC budget and the host tier with an
+                       # embedding-only stage (its saved sets are empty)
+                       (1, dict(frc_retain_bytes=(1 << 64) - 1)),
+                       (1, dict(frc_retain_bytes=1, frc_swap_bytes=1 << 20))):
+        q = _gpu(cfg, flat, "bf16", layers_per_stage=lps, **kw)
         q.preempt(victim, 9)
         status, st = q.step(tok, tgt)
         assert status == "preempted"
