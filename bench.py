@@ -608,8 +608,9 @@ def main():
     ap.add_argument("--stages", type=int, default=0,
                     help="pipeline stages (default: the config's, at least N)")
     ap.add_argument("--lps", default="", help="explicit layers_per_stage, comma separated")
-    ap.add_argument("--partition", default="balanced", choices=["balanced", "device", "even"],
-                    help="blocks per stage: cost-balanced (default) or even by count (Q6)")
+    ap.add_argument("--partition", default="device", choices=["balanced", "device", "even"],
+                    help="blocks per stage: cost-balanced per GPU (default; = per node when "
+                         "each GPU has one node or all of them), per node, or even by count (Q6)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
