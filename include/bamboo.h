@@ -110,7 +110,8 @@ typedef struct {
                                    bb_node_stats (busy / bubble / FRC accounting)        */
   int detect_ms;                /* 0 (default): injected preemptions, bb_preempt called with
                                    the same arguments on every rank. > 0: fail-stop mode
-                                   (needs one node per rank): bb_preempt is called on the
+                                   (needs one node per rank, world_size = pipelines *
+                                   stages): bb_preempt is called on the
                                    victim's rank only; that rank stops at the injection
                                    point and goes silent (its bb_step returns
                                    BB_E_PREEMPTED; the caller then calls bb_destroy and
@@ -130,7 +131,7 @@ typedef struct {
                                    sync and Adam; a preempted pipeline's all-reduce is run
                                    by its shadow after the recovery and the others wait for
                                    it. node_rank then has D*stages entries. Not
-                                   with EFEB or detect_ms > 0                             */
+                                   with EFEB                                               */
   size_t frc_swap_bytes;        /* per replica: pinned host memory for the FRC saved sets
                                    beyond frc_retain_bytes ("swap out these data"):
                                    each is copied to the host on its own stream after the

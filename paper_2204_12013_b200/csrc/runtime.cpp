@@ -1336,11 +1336,10 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     if (D > k::kMaxPipelines) throw RtError{BB_E_UNSUPPORTED, "at most 8 pipelines"};
     if (D > 1 && c.o.rc == BB_RC_EFEB)
       throw RtError{BB_E_UNSUPPORTED, "EFEB with more than one pipeline is not built"};
-    if (D > 1 && c.o.detect_ms > 0)
-      throw RtError{BB_E_UNSUPPORTED, "fail-stop detection with more than one pipeline"};
-    if (c.o.detect_ms > 0 && (c.o.world_size != P || c.o.node_rank))
+    if (c.o.detect_ms > 0 && (c.o.world_size != N || c.o.node_rank))
       // a process death takes all its nodes: only one node per rank is recoverable
-      throw RtError{BB_E_INVAL, "fail-stop mode needs one node per rank (world_size == stages)"};
+      throw RtError{BB_E_INVAL,
+                    "fail-stop mode needs one node per rank (world_size == pipelines * stages)"};
     if (c.o.prec == BB_PREC_BF16 && m->d_model < 64)
       // the transposed (MN-major) operands of dX / dW need >= 64 rows
       throw RtError{BB_E_UNSUPPORTED, "bf16 path needs d_model >= 64"};

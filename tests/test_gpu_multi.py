@@ -196,3 +196,28 @@ def test_multi_process_dp_bitwise(n, victim, pi):
         assert tot == np.float32(losses[t]), (t, parts, losses[t])
     for w in state:
         assert np.array_equal(merged(ranks, D * P, w), state[w]), w
+
+
+@pytest.mark.parametrize("victim,pi", [(1, 12), (2, 22), (3, 5)])
+def test_failstop_dp_bitwise(victim, pi):
+    """Fail-stop detection with D=2 pipelines of P=2, one node per process:
+    the victim's process goes silent and exits; the survivors (its pipeline
+    and the other one, which waits in its all-reduce) detect it, agree on the
+    cut and recover; every later step equals the failure-free D=2 run bit
+    for bit."""
+    cfg = get_config("C0")
+    D, P = 2, cfg.stages
+    losses, state = single_dp(cfg, D, 3)
+    ranks = run_mp(4, config="C0", stages=P, steps=3, pipelines=D, failstop=f"1:{victim}:{pi}",
+                   detect=300)
+    assert ranks[victim] is None
+    live = [r for r in ranks if r is not None]
+    for t in range(1, 3):   # step 0's share of a last-stage victim left with it
+        parts = [np.float32(r["losses"][t]) for r in live if not np.isnan(r["losses"][t])]
+        assert len(parts) == D, (t, parts)
+        tot = np.float32(0)
+        for x in parts:
+            tot = np.float32(tot + x)
+        assert tot == np.float32(losses[t]), (t, parts, losses[t])
+    for w in state:
+        assert np.array_equal(merged(live, D * P, w), state[w]), w
