@@ -304,8 +304,10 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
 /* Transport microbenchmark (no context): two processes (rank 0 / 1, device
  * ordinals of their own, same 32-byte session id) ping-pong `iters`
  * messages of `bytes` through the library's transport (copy-engine write into
- * the peer's HBM, completion published by a host callback, receiver polling
- * host shared memory). *us = mean one-way time per message, on rank 0. */
+ * the peer's HBM, interprocess event, sequence number in host shared
+ * memory); each reply's copy waits on the arrival of the message it answers.
+ * *us = mean one-way time per message including the data movement, on
+ * rank 0. */
 bb_status bb_xport_pingpong(int rank, int world, int device, const void *session_id,
                             size_t bytes, int iters, float *us);
 

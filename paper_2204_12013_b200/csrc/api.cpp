@@ -234,10 +234,13 @@ bb_status bb_plan_dump(const bb_model *m, int stages, int microbatches, const bb
 }
 
 // Transport microbenchmark: two ranks ping-pong `iters` messages of `bytes`
-// over the library's transport (copy into the peer's HBM + completion
-// published by a host callback, the receiver polls host shared memory);
-// *us = mean one-way latency per message (host wall time), measured on rank
-// 0. Compare with NCCL send/recv of the same bytes (tools/xport_vs_nccl.py).
+// over the library's transport (copy into the peer's HBM, the sender's
+// interprocess event, sequence number in host shared memory). A reply is
+// ordered after the arrival of the message it answers (its copy's stream
+// waits on that message's event), so the chain of 2 * iters copies is
+// serial on the devices and the host time to its end is the one-way latency
+// including the data movement; *us = that time / (2 * iters), on rank 0.
+// Compare with NCCL send/recv of the same bytes (tools/xport_vs_nccl.py).
 bb_status bb_xport_pingpong(int rank, int world, int device, const void *session_id,
                             size_t bytes, int iters, float *us) {
   if (world != 2 || rank < 0 || rank > 1 || !session_id || bytes == 0 || iters < 1)
@@ -261,7 +264,10 @@ bb_status bb_xport_pingpong(int rank, int world, int device, const void *session
   auto recv = [&] {
     while (!x.available(in)) {
     }
+    const int slot = (int)(in.consumed % (uint64_t)in.cap);
     x.consume(in);
+    // the next send (and the final synchronise) waits for this payload
+    if (cudaEvent_t ev = x.wait_event(in, slot)) cudaStreamWaitEvent(out.stream, ev, 0);
   };
   x.barrier();
   const auto t0 = std::chrono::steady_clock::now();
