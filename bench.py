@@ -387,7 +387,7 @@ def run_ours(args, rank, ws, local):
     for rc in (False, True):
         log(rank, f"init rc={rc} P={P} M={M} mb={mb}")
         extra = dict(frc_retain_bytes=AUTO if args.retain == "auto" else int(args.retain),
-                     timing=True) if rc else {}
+                     timing=True, frc_persistent=args.frc_persistent) if rc else {}
         pipe = bb.Pipeline(m, P, M, rc=rc, session_id=fresh_id(), **common, **extra)
         pipe.load_params(flat)
         pipe.stage_inputs(tok, tgt)
@@ -619,6 +619,9 @@ def main():
     ap.add_argument("--retain", default="auto",
                     help="frc_retain_bytes per node: auto (free HBM) or bytes (0 = all M)")
     ap.add_argument("--no-recovery", dest="recovery", action="store_false")
+    ap.add_argument("--frc-persistent", action="store_true",
+                    help="FRC GEMMs on persistent full-device grids (bb_opts.frc_persistent) "
+                         "instead of one CTA per tile")
     ap.add_argument("--pipelines", type=int, default=1,
                     help="D data-parallel pipelines (bb_opts.pipelines; the recovery matrix "
                          "runs only at D=1)")
