@@ -79,24 +79,7 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA / integer pipes for x <= 0 (same construction as the
-// forward's ex2_fma in k_attn_umma.cu: round by the 1.5 * 2^23 magic add,
-// cubic for 2^f on [-0.5, 0.5], max relative error 7.7e-5, exponent add).
-__device__ __forceinline__ float ex2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.05508877f, 0.24260466f);
-  p = fmaf(p, f, 0.69327628f);
-  p = fmaf(p, f, 0.9999289f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-constexpr int kEmuDefaultBwd = 0;
-
 // 14 warps: at most 4 per SM sub-partition, so 128 registers per thread.
-// EMU: exponentials per 4 of P^T recomputed on the FMA pipe (0 = all MUFU).
-template <int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_umma_kernel(const __grid_constant__ CUtensorMap map_qkv,
                        const __grid_constant__ CUtensorMap map_do, float *__restrict__ ws,
@@ -318,10 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4 a = *reinterpret_cast<const float4 *>(ls + 64 * g + c);
           const float l2[4] = {a.x * LOG2E, a.y * LOG2E, a.z * LOG2E, a.w * LOG2E};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float x = fmaf(__uint_as_float(sv[(c + j) / 16][(c + j) % 16]), sl2, -l2[j]);
-            p[c + j] = j < EMU ? ex2_fma(x) : ex2(x);
-          }
+          for (int j = 0; j < 4; ++j)
+            p[c + j] = ex2(fmaf(__uint_as_float(sv[(c + j) / 16][(c + j) % 16]), sl2, -l2[j]));
         }
       }
       if (diag) {                                     // causal diagonal block: key > query -> 0
@@ -534,21 +515,15 @@ cudaError_t attention_umma_bwd(int B, int S, int H, int nh, bool causal, const v
   }
   cudaError_t e = attention_bwd_rowdot(B, S, H, nh, o, dout, Dv, s);
   if (e != cudaSuccess) return e;
-  // BB_ATTN_EMU_BWD = 0..2: exponentials per 4 on the FMA pipe
-  static const int emu = [] {
-    const char *v = std::getenv("BB_ATTN_EMU_BWD");
-    return v ? std::max(0, std::min(2, std::atoi(v))) : kEmuDefaultBwd;
-  }();
-  auto kern = emu == 0 ? fa_bwd_umma_kernel<0> : emu == 1 ? fa_bwd_umma_kernel<1>
-                                                          : fa_bwd_umma_kernel<2>;
-  static bool attr[3] = {false, false, false};
-  if (!attr[emu]) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::BYTES);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(fa_bwd_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Smem::BYTES);
     if (e != cudaSuccess) return e;
-    attr[emu] = true;
+    attr = true;
   }
   dim3 grid(nh * B, nkb);
-  kern<<<grid, kThreads, Smem::BYTES, s>>>(
+  fa_bwd_umma_kernel<<<grid, kThreads, Smem::BYTES, s>>>(
       mq, md, ws, S, H, nh, causal ? 1 : 0,
       (S % BLK == 0 && (reinterpret_cast<uintptr_t>(lse) & 15) == 0 &&
        (reinterpret_cast<uintptr_t>(Dv) & 15) == 0) ? 1 : 0,

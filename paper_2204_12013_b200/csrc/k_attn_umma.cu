@@ -48,30 +48,10 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA / integer pipes (no MUFU), for x <= 0: x = n + f with n =
-// round(x) by the 1.5 * 2^23 magic add, f in [-0.5, 0.5]; 2^f by a cubic
-// (relative-error least squares on Chebyshev nodes: max relative error
-// 7.7e-5, far inside the bf16 rounding of P, 3.9e-3); 2^n added to the
-// exponent field. Clamped at -126 (2^-126 stands in for exp2(-inf) = 0).
-// The softmax sends a fixed share of its exponentials here so MUFU.EX2,
-// which bounds the loop (2 CTAs x 128 x 128 exponentials per key block per
-// SM), shares the work with the FMA pipe (the FA4 split).
-__device__ __forceinline__ float ex2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;                 // round(x) in the low mantissa bits
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.05508877f, 0.24260466f);
-  p = fmaf(p, f, 0.69327628f);
-  p = fmaf(p, f, 0.9999289f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
 constexpr uint32_t idesc_f16(int m, int n, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
-
-constexpr int kEmuDefault = 0;
 
 struct SmemLayout {
   static constexpr int Q = 0;                         // 128 x 64 bf16 = 16 KB
@@ -82,8 +62,6 @@ struct SmemLayout {
   static constexpr int BYTES = BAR + 128 + 1024;
 };
 
-// EMU: pairs of scores per 4 whose exponentials run on the FMA pipe (0 = all MUFU)
-template <int EMU>
 __global__ void __launch_bounds__(kThreads, 2)
     fa_fwd_umma_kernel(const __grid_constant__ CUtensorMap map_qkv, int S, int H, int nh,
                        int causal, __nv_bfloat16 *__restrict__ o, float *__restrict__ lse,
@@ -256,11 +234,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        const bool emu = (i / 2) % 4 < EMU;      // compile-time per unrolled pair
-        const float x0 = fmaf(__uint_as_float(t[i]), sl2, -mnz);
-        const float x1 = fmaf(__uint_as_float(t[i + 1]), sl2, -mnz);
-        const float p0 = emu ? ex2_fma(x0) : ex2(x0);
-        const float p1 = emu ? ex2_fma(x1) : ex2(x1);
+        const float p0 = ex2(fmaf(__uint_as_float(t[i]), sl2, -mnz));
+        const float p1 = ex2(fmaf(__uint_as_float(t[i + 1]), sl2, -mnz));
         sum += p0 + p1;
         t[i / 2] = pack_bf2(p0, p1);
       }
@@ -324,19 +299,13 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
   CUtensorMap map;
   if (!tma_map_bf16_2d(&map, qkv, (uint64_t)3 * H, (uint64_t)B * S, (uint64_t)3 * H, 128))
     return cudaErrorInvalidValue;
-  // BB_ATTN_EMU = 0..2: pairs per 4 on the FMA pipe (default kEmuDefault)
-  static const int emu = [] {
-    const char *e = std::getenv("BB_ATTN_EMU");
-    return e ? std::max(0, std::min(2, std::atoi(e))) : kEmuDefault;
-  }();
-  auto kern = emu == 0 ? fa_fwd_umma_kernel<0> : emu == 1 ? fa_fwd_umma_kernel<1>
-                                                          : fa_fwd_umma_kernel<2>;
-  static bool attr[3] = {false, false, false};
-  if (!attr[emu]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fa_fwd_umma_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SmemLayout::BYTES);
     if (e != cudaSuccess) return e;
-    attr[emu] = true;
+    attr = true;
   }
   dim3 grid(nh, B, (S + BQ - 1) / BQ);
   static const bool tr = [] {
@@ -352,7 +321,7 @@ cudaError_t attention_umma_fwd(int B, int S, int H, int nh, bool causal, const v
     tn = ctas;
   }
   if (tr) cudaMemsetAsync(tbuf, 0, ctas * 64 * 8, s);
-  kern<<<grid, kThreads, SmemLayout::BYTES, s>>>(
+  fa_fwd_umma_kernel<<<grid, kThreads, SmemLayout::BYTES, s>>>(
       map, S, H, nh, causal ? 1 : 0, reinterpret_cast<__nv_bfloat16 *>(o), lse,
       tr ? tbuf : nullptr);
   ++g_launches;
