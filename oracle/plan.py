@@ -17,6 +17,10 @@ Sources:
   SEND_ACT(k); on the last stage right before RECV_ACT(k) (Q4 reading).
 * Lazy BRC via a failover schedule merging victim and shadow schedules with
   the four rules of P:538-545 (Q5 reading).
+* D > 1 data-parallel pipelines: each stage's gradient sum is
+  all-reduced over the pipelines after the node's last backward; a failed
+  pipeline's share is replayed by its shadow and the others wait (P:421;
+  DESIGN.md §2 "D > 1 pipelines"). Pinned in tests/test_oracle_dp.py.
 
 Instruction fields: (kind, mb, peer, stage). `stage` is the logical stage on
 whose behalf the node acts; `peer` is a NODE id (node n initially runs stage n).
