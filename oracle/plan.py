@@ -119,11 +119,12 @@ def stage_plan(s, P, M, rc, d=0, D=1):
     d, D: pipeline d of D data-parallel pipelines (node ids d*P + s, peers in
     the same pipeline); with D > 1 the step's gradient sum of the stage is
     all-reduced over the pipelines (AR_SEND to each other pipeline, AR_RECV
-    from each, AR_SUM) before the replica sync and the update."""
+    from each, AR_SUM) before the replica sync and the update. EFEB
+    with D > 1 (this build's reading): the replica's eager BRC gradient is
+    the pipeline's local one, so the replica is synced with the total like
+    EFLB's (REPLICA_SEND / RECV after the all-reduce); the eager BRC still
+    spares the recovery the lazy backward."""
     mode = rc_mode(rc)
-    if D > 1 and mode == "efeb":
-        raise PlanError("EFEB with D > 1 is not built (the replica's BRC gradient "
-                        "would need its own all-reduce)")
     rc, frc = mode != "none", mode in ("eflb", "efeb")
     efeb = mode == "efeb"
     r = (s + 1) % P
@@ -171,12 +172,15 @@ def stage_plan(s, P, M, rc, d=0, D=1):
     for i in range(M - W, M):
         bwd(i)
     base = d * P
+    if efeb and s == P - 1 and D > 1:   # the replica stage's eager BRCs, before the all-reduce
+        for k in range(M):
+            brc(k)
     if D > 1:
         others = [e * P + s - base for e in range(D) if e != d]   # local offsets
         I.extend(Instr(AR_SEND, None, o, s) for o in others)
         I.extend(Instr(AR_RECV, None, o, s) for o in others)
         I.append(Instr(AR_SUM, None, None, s))
-    if efeb:
+    if efeb and D == 1:
         if s == P - 1:
             for k in range(M):
                 brc(k)
@@ -411,6 +415,9 @@ def recovery_plans(plans, P, M, v, pcs, channels):
     # receive from it is rerouted to the shadow, which takes over the
     # victim's remaining sends (its duplicate gradients for node v-2).
     efeb = any(i.kind == BRC_BWD for seq in plans.values() for i in seq)
+    # D > 1: the update reads the all-reduced total, so the victim stage's
+    # APPLY follows its all-reduce in B (EFEB too)
+    dp = any(i.kind == AR_SEND for seq in plans.values() for i in seq)
 
     def executed(n):
         return plans[n][:pcs[n]]
@@ -447,7 +454,7 @@ def recovery_plans(plans, P, M, v, pcs, channels):
             continue                                  # becomes v's FWD (in B)
         if ins.kind in SENDS and ins.peer == v:
             continue                                  # victim<->shadow (rule 2)
-        if ins.kind == APPLY and ins.stage == sv and not commit and not efeb:
+        if ins.kind == APPLY and ins.stage == sv and not commit and (not efeb or dp):
             continue                                  # v's update runs from B
         A.append(ins)
     A = delivered_filter(u, A, lambda ins: None)
@@ -460,7 +467,7 @@ def recovery_plans(plans, P, M, v, pcs, channels):
             kd = ins.kind
             if kd in (LOAD_INPUTS, FRC_FWD, REPLICA_SEND, REPLICA_RECV):
                 continue
-            if kd == APPLY and (ins.stage != sv or efeb):
+            if kd == APPLY and (ins.stage != sv or (efeb and not dp)):
                 continue
             if efeb and kd in (BWD, BRC_BWD, RECV_GRAD, RECV_DGRAD):
                 continue                              # the shadow's BRC_BWD does it
@@ -478,7 +485,7 @@ def recovery_plans(plans, P, M, v, pcs, channels):
         if n == v:
             continue
         seq = A if n == u else list(plans[n][pcs[n]:])
-        if efeb and n != u:
+        if efeb and n != u and n // P == v // P:
             seq = [i for i in seq if not (i.kind in SENDS and i.peer == v)]
             seq = delivered_filter(n, seq, lambda ins: u)
         elif n != w and n != u:

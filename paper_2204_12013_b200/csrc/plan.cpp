@@ -135,7 +135,6 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode, int d, int D) {
   const bool rc = mode != 0, frc = mode == 1 || mode == 3, efeb = mode == 3;
   if (rc && P < 2) throw PlanError("RC needs stages >= 2");
   if (D < 1 || d < 0 || d >= D) throw PlanError("bad pipeline index");
-  if (efeb && D > 1) throw PlanError("EFEB with more than one pipeline is not built");
   const int r = (s + 1) % P;
   std::vector<Instr> I;
   const bool need_tok = s == 0 || (rc && s == P - 1);
@@ -173,6 +172,12 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode, int d, int D) {
   // D > 1: the stage's gradient sum meets the same stage of the other
   // pipelines before anything reads it (replica sync, update); peers are
   // global node ids, marked here by an offset past the pipeline-local ids
+  // EFEB with D > 1: the last node's eager BRCs of stage 0 come before its
+  // all-reduce, and every replica is synced with the all-reduced total (the
+  // EFLB tail below), since its own eager-BRC gradient is the pipeline's
+  // local one
+  if (efeb && D > 1 && s == P - 1)
+    for (int k = 0; k < M; ++k) brc(k);
   std::vector<int> partners;
   for (int e = 0; e < D; ++e)
     if (e != d) partners.push_back(e * P + s);
@@ -181,7 +186,7 @@ std::vector<Instr> stage_plan(int s, int P, int M, int mode, int d, int D) {
   for (int o : partners) I.push_back({AR_RECV, -1, o, s});
   if (D > 1) I.push_back({AR_SUM, -1, -1, s});
   const size_t ar_end = I.size();
-  if (efeb) {
+  if (efeb && D == 1) {
     if (s == P - 1)   // stage 1's gradients come last: after the own backwards
       for (int k = 0; k < M; ++k) brc(k);
     I.push_back({APPLY, -1, -1, s});
@@ -296,6 +301,7 @@ struct Loss {
   int P, M, v, u, w;
   int sv;   // the victim's stage in its pipeline (instructions name stages)
   bool efeb = false, commit = false;
+  bool dp = false;   // D > 1: the victim stage's update follows its all-reduce (in B)
   std::set<int> frc_done;
   const std::map<int, int> *pcs = nullptr;
   const Channels *ch = nullptr;
@@ -319,14 +325,14 @@ std::map<int, std::deque<Msg>> undelivered_queue(const Loss &x, int n) {
 Fate shadow_fate(const Loss &x, const Instr &i) {
   if (i.kind == FRC_FWD && i.stage == x.sv) return DROP;
   if (is_send(i.kind) && i.peer == x.v) return DROP;
-  if (i.kind == APPLY && i.stage == x.sv && !x.commit && !x.efeb) return DROP;
+  if (i.kind == APPLY && i.stage == x.sv && !x.commit && (!x.efeb || x.dp)) return DROP;
   return KEEP;
 }
 
 Fate survivor_fate(const Loss &x, int /*n*/, const Instr &i) {
   if (!is_send(i.kind) || i.peer != x.v) return KEEP;
-  if (x.efeb) return DROP;
   if (i.kind == AR_SEND) return TO_SHADOW;   // the shadow replays v's all-reduce
+  if (x.efeb) return DROP;
   if (i.kind == REPLICA_SEND) return DROP;   // w's replica on v is gone (Q21)
   return TO_SHADOW;
 }
@@ -341,7 +347,7 @@ bool victim_work(const Loss &x, const Instr &i, int idx) {
     case REPLICA_RECV:
       return false;
     case APPLY:
-      return i.stage == x.sv && !x.efeb;
+      return i.stage == x.sv && (!x.efeb || x.dp);
     case BWD:
       return !x.efeb;
     case RECV_GRAD:
@@ -512,7 +518,10 @@ Plans recovery_plans(const Plans &plans, int P, int M, int v, const std::map<int
   const std::vector<Instr> &pv = plans.at(v), &pu = plans.at(x.u);
   for (int i = 0; i < pcs.at(v); ++i) x.commit = x.commit || pv[i].kind == REPLICA_SEND;
   for (auto &kv : plans)
-    for (const Instr &i : kv.second) x.efeb = x.efeb || i.kind == BRC_BWD;
+    for (const Instr &i : kv.second) {
+      x.efeb = x.efeb || i.kind == BRC_BWD;
+      x.dp = x.dp || i.kind == AR_SEND;
+    }
   for (int i = 0; i < pcs.at(x.u); ++i)
     if (pu[i].kind == FRC_FWD && pu[i].stage == x.sv) x.frc_done.insert(pu[i].mb);
 

@@ -1334,8 +1334,6 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
     if (c.o.micro_batch < 1) throw RtError{BB_E_INVAL, "micro_batch < 1"};
     const int D = c.o.pipelines < 1 ? 1 : c.o.pipelines, N = D * P;   // pipelines, nodes
     if (D > k::kMaxPipelines) throw RtError{BB_E_UNSUPPORTED, "at most 8 pipelines"};
-    if (D > 1 && c.o.rc == BB_RC_EFEB)
-      throw RtError{BB_E_UNSUPPORTED, "EFEB with more than one pipeline is not built"};
     if (c.o.detect_ms > 0 && (c.o.world_size != N || c.o.node_rank))
       // a process death takes all its nodes: only one node per rank is recoverable
       throw RtError{BB_E_INVAL,

@@ -119,7 +119,7 @@ def _same(a, b):
         assert np.array_equal(a[1][k], b[1][k]), k
 
 
-@pytest.mark.parametrize("rc", ["eflb", "lflb", "none"])
+@pytest.mark.parametrize("rc", ["eflb", "lflb", "efeb", "none"])
 def test_dp_pipelines_bit_identical(rc):
     cfg = get_config("C0")
     flat = make_params(cfg.model)
@@ -134,7 +134,8 @@ def test_dp_pipelines_bit_identical(rc):
     p.close()
 
 
-def test_dp_recovery_bitwise_every_node():
+@pytest.mark.parametrize("rc", ["eflb", "efeb"])
+def test_dp_recovery_bitwise_every_node(rc):
     """Each of the 4 nodes at sampled points of the step (incl. before its
     all-reduce, between its sends and receives, after its commit): the
     interrupted step and a failover step equal the failure-free run bit for
@@ -142,17 +143,17 @@ def test_dp_recovery_bitwise_every_node():
     cfg = get_config("C0")
     P, M = cfg.stages, cfg.microbatches
     flat = make_params(cfg.model)
-    p, ref, _ = _run(cfg, flat, 2)
+    p, ref, _ = _run(cfg, flat, 2, rc=rc)
     p.close()
-    plans = opl.normal_plans(P, M, True, D)
+    plans = opl.normal_plans(P, M, rc, D)
     for v in range(D * P):
         kinds = [i.kind for i in plans[v]]
         n = len(kinds)
         pts = {0, 5, n // 2, kinds.index(opl.AR_SEND), kinds.index(opl.AR_SEND) + 1,
                kinds.index(opl.AR_SUM), kinds.index(opl.REPLICA_SEND) + 1, n}
         for pi in sorted(pts):
-            q, out, rec = _run(cfg, flat, 2, events={0: (v, pi)})
-            assert rec[0] == opl.recovery_dump(P, M, v, pi, True, D=D), (v, pi)
+            q, out, rec = _run(cfg, flat, 2, events={0: (v, pi)}, rc=rc)
+            assert rec[0] == opl.recovery_dump(P, M, v, pi, rc, D=D), (v, pi)
             _same(out[0], ref[0])
             _same(out[1], ref[1])
             q.close()

@@ -152,12 +152,12 @@ def test_multi_process_modes_bitwise(mode):
             assert np.array_equal(merged(ranks, 3, w), state[w]), (mode, extra, w)
 
 
-def single_dp(cfg, D, steps):
+def single_dp(cfg, D, steps, rc="eflb"):
     """D pipelines in one process, failure-free: per-step losses and every
     pipeline's copy of every stage (index d*P + s)."""
     import dataclasses
     import paper_2204_12013_b200 as bb
-    p = bb.Pipeline(cfg.model, cfg.stages, cfg.microbatches, micro_batch=cfg.micro_batch, rc=True,
+    p = bb.Pipeline(cfg.model, cfg.stages, cfg.microbatches, micro_batch=cfg.micro_batch, rc=rc,
                     lr=1e-4, pipelines=D)
     p.load_params(make_params(cfg.model))
     bcfg = dataclasses.replace(cfg, microbatches=D * cfg.microbatches)
@@ -221,3 +221,23 @@ def test_failstop_dp_bitwise(victim, pi):
         assert tot == np.float32(losses[t]), (t, parts, losses[t])
     for w in state:
         assert np.array_equal(merged(live, D * P, w), state[w]), w
+
+
+@pytest.mark.parametrize("victim,pi", [(-1, 0), (1, 12), (2, 30)])
+def test_multi_process_dp_efeb_bitwise(victim, pi):
+    """EFEB with D=2 pipelines of P=2 over 4 processes (eager BRC, replicas
+    synced with the all-reduced total): equals the single-process run bit
+    for bit, also after a preemption."""
+    cfg = get_config("C0")
+    D, P = 2, cfg.stages
+    losses, state = single_dp(cfg, D, 2, rc="efeb")
+    extra = {"victim": victim, "pi": pi} if victim >= 0 else {}
+    ranks = run_mp(4, config="C0", stages=P, steps=2, pipelines=D, rc="efeb", **extra)
+    for t in range(2):
+        parts = [np.float32(r["losses"][t]) for r in ranks if not np.isnan(r["losses"][t])]
+        tot = np.float32(0)
+        for x in parts:
+            tot = np.float32(tot + x)
+        assert len(parts) == D and tot == np.float32(losses[t]), (t, parts, losses[t])
+    for w in state:
+        assert np.array_equal(merged(ranks, D * P, w), state[w]), w

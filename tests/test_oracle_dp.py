@@ -67,7 +67,8 @@ def same(a, b):
 
 
 @pytest.mark.parametrize("P,M,D,rc", [(2, 2, 2, "none"), (2, 2, 2, "eflb"), (3, 2, 2, "lflb"),
-                                      (2, 1, 3, "eflb"), (3, 3, 2, "eflb")])
+                                      (2, 1, 3, "eflb"), (3, 3, 2, "eflb"), (3, 2, 2, "efeb"),
+                                      (2, 2, 2, "efeb")])
 def test_dp_equals_brute_force(P, M, D, rc):
     cfg = tiny(P, M)
     flat = make_params(cfg.model)
@@ -204,3 +205,24 @@ def test_dp_recovery_dump_golden_shape():
     """The recovery dump of a D>1 cut names the pipeline-local shadow."""
     txt = pl.recovery_dump(2, 2, 3, 5, "eflb", D=2)
     assert txt.startswith("# bamboo-recovery v1 P=2 M=2 victim=3 shadow=2 successor=2")
+
+
+@pytest.mark.parametrize("mode", ["efeb", "lflb"])
+def test_dp_modes_injection_sweep_exact(mode):
+    """EFEB and LFLB with D = 2: every node, sampled points; exact equality
+    with the failure-free run on the interrupted and the next step."""
+    r = random.Random(17)
+    for P, M in ((2, 2), (3, 2)):
+        cfg = tiny(P, M)
+        flat = make_params(cfg.model)
+        _, ref = run(cfg, 2, flat, 2, rc=mode)
+        plans = pl.normal_plans(P, M, mode, 2)
+        for v in range(2 * P):
+            n = len(plans[v])
+            for pi in sorted({0, n, n // 2} | {r.randint(0, n) for _ in range(4)}):
+                _, res = run(cfg, 2, flat, 2, rc=mode, events={0: (v, pi)})
+                if np.isnan(res[0][0]):   # LFLB: a last stage lost after its commit point
+                    assert mode == "lflb" and v % P == P - 1   # took its losses with it
+                    res[0] = (ref[0][0],) + tuple(res[0][1:])
+                same(res[0], ref[0])
+                same(res[1], ref[1])

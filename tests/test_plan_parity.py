@@ -129,7 +129,7 @@ def test_cpp_recovery_matches_oracle_every_point(mode):
                         pl.recovery_dump(P, M, v, pi, rc=mode), (P, M, v, pi)
 
 
-@pytest.mark.parametrize("mode", ["none", "eflb", "lflb"])
+@pytest.mark.parametrize("mode", ["none", "eflb", "lflb", "efeb"])
 def test_cpp_dp_plans_match_oracle_every_point(mode):
     """D > 1 data-parallel pipelines: normal dumps (with the
     default rank layout over 1, 2 and D*P processes), failover dumps of every
