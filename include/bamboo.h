@@ -130,8 +130,8 @@ typedef struct {
                                    every pipeline applies the same bits) before the replica
                                    sync and Adam; a preempted pipeline's all-reduce is run
                                    by its shadow after the recovery and the others wait for
-                                   it. node_rank then has D*stages entries. Not
-                                   with EFEB                                               */
+                                   it. node_rank then has D*stages entries. EFEB:
+                                   the replica is synced with the total as in EFLB        */
   size_t frc_swap_bytes;        /* per replica: pinned host memory for the FRC saved sets
                                    beyond frc_retain_bytes ("swap out these data"):
                                    each is copied to the host on its own stream after the
