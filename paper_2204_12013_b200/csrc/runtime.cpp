@@ -723,9 +723,14 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         c.bytes_rerouted += bytes;
       if (is_local(c, ins.peer)) {
         Node &dst = c.nodes.at(ins.peer);
-        void *dp = m.kind == MSG_GRADSUM ? (void *)dst.copies.at(X).grad
-                   : m.kind == MSG_AR    ? (void *)dst.copies.at(X).ar_in.at(nd.n / P)
-                                         : arena_alloc(dst, bytes);
+        // a replica gradient sum lands in the replica's accumulator, except
+        // under EFEB (D > 1), where the replica's own eager BRC may still be
+        // accumulating there on the receiver's FRC stream: then it is a
+        // message of its own and the update reads it from there
+        const bool into_grad = m.kind == MSG_GRADSUM && c.o.rc != BB_RC_EFEB;
+        void *dp = into_grad               ? (void *)dst.copies.at(X).grad
+                   : m.kind == MSG_AR      ? (void *)dst.copies.at(X).ar_in.at(nd.n / P)
+                                           : arena_alloc(dst, bytes);
         wait_ev(nd.main, pl.ev);
         // the receiver's step-start memset of that buffer ran on ITS stream:
         // order this cross-node write after it explicitly
@@ -765,7 +770,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
         // event mode: consumers wait on the sender's event for this slot;
         // callback mode: the number was published after the payload landed
         cudaEvent_t ready = c.x.wait_event(e, slot);
-        if (m.kind == MSG_GRADSUM) {
+        if (m.kind == MSG_GRADSUM && c.o.rc != BB_RC_EFEB) {   // (EFEB: read in place)
           wait_ev(nd.main, ready);
           CK(cudaMemcpyAsync(nd.copies.at(X).grad, src, msg_bytes(c, m.kind, m.stage),
                              cudaMemcpyDeviceToDevice, nd.main));
@@ -781,7 +786,7 @@ bool exec(Ctx &c, Node &nd, const Instr &ins, const Phase &ph) {
       else if (ins.kind == RECV_GRAD || ins.kind == RECV_DGRAD)
         nd.store[{K_DACT, X + 1, k}] = got;
       else
-        nd.store[{K_GRADSUM, X, 0}] = {nd.copies.at(X).grad, got.ev};
+        nd.store[{K_GRADSUM, X, 0}] = {c.o.rc == BB_RC_EFEB ? got.p : nd.copies.at(X).grad, got.ev};
       return true;
     }
     case AR_SUM: {
