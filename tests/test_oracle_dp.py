@@ -90,10 +90,11 @@ def test_dp_equals_brute_force(P, M, D, rc):
             assert np.abs(gm - m).max() <= 1e-12 * np.abs(m).max()
 
 
-def test_dp_pipelines_and_replicas_identical():
+@pytest.mark.parametrize("rc", ["eflb", "efeb", "lflb"])
+def test_dp_pipelines_and_replicas_identical(rc):
     P, M, D = 3, 2, 3
     cfg = tiny(P, M)
-    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc="eflb", D=D)
+    pp = pipeline.Pipeline(cfg, make_params(cfg.model), rc=rc, D=D)
     for t in range(3):
         pp.step(*batch(cfg, D, t))
         for d in range(1, D):
