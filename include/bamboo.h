@@ -261,9 +261,10 @@ bb_status bb_read_state(void *ctx, int stage, int replica, int what, float *host
 
 /* Overwrite stage `stage`'s fp32 state (what = BB_STATE_PARAMS, _ADAM_M or
  * _ADAM_V; PARAMS also refreshes the bf16 working copy) in every copy this
- * process hosts (primary and replica, so replica == primary is kept), from
- * host[n]. For starting a step from a given state (e.g. an oracle's), at a
- * step boundary. BB_E_INVAL for a bad stage, kind or size. */
+ * process hosts (primary and replica, so replica == primary is kept; with
+ * D > 1 the copies of every local pipeline), from host[n]. For starting a
+ * step from a given state (e.g. an oracle's), at a step boundary. BB_E_INVAL
+ * for a bad stage (0 <= stage < stages), kind or size. */
 bb_status bb_write_state(void *ctx, int stage, int what, const float *host, size_t n);
 
 /* HBM plan of `stage`: bytes of one saved set (the activations its backward
