@@ -105,16 +105,31 @@ class Clocks:
 
 
 # ------------------------------------------------------------- distributed
+_HARNESS_DEV = "cuda"   # where the harness's max / sum reductions live
+
+
 def dist_setup(args):
+    global _HARNESS_DEV
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ngpu = max(1, torch.cuda.device_count())
+        if int(os.environ.get("LOCAL_WORLD_SIZE", ws)) > ngpu:
+            # more processes than GPUs (a rehearsal of a larger N on a smaller
+            # box): ranks share GPUs round-robin and the harness uses gloo,
+            # since NCCL refuses two ranks on one device (the library itself
+            # never uses NCCL)
+            local %= ngpu
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+            _HARNESS_DEV = "cpu"
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # (the harness's own barriers / max-over-ranks only: the library never uses NCCL)
     return rank, ws, local
 
@@ -130,7 +145,7 @@ def allreduce_max(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda")
+    t = torch.tensor([float(x)], device=_HARNESS_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item()
 
@@ -140,7 +155,7 @@ def allreduce_sum(x, ws):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda")
+    t = torch.tensor([float(x)], device=_HARNESS_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.item()
 
