@@ -1533,7 +1533,7 @@ bb_status rt_init(Ctx &c, const bb_model *m, int P, int M, const bb_opts *o) {
             if (nh > 0) {
               CK(cudaHostAlloc(&cp.hbase, nh * si.slot_bytes, cudaHostAllocDefault));
               for (size_t i = 0; i < nh; ++i) cp.hslots.push_back(cp.hbase + i * si.slot_bytes);
-              Node &hn = c.nodes.at(kv.first);
+              Node &hn = kv.second;
               if (!hn.swap) CK(cudaStreamCreateWithFlags(&hn.swap, cudaStreamNonBlocking));
             }
           }
