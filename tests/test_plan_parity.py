@@ -158,3 +158,12 @@ def test_cpp_dp_plans_match_oracle_every_point(mode):
                 assert bbl.plan_dump(m, P, M, victim=v, at_instr=pi, rc=mode, micro_batch=1,
                                      pipelines=D) == \
                     pl.recovery_dump(P, M, v, pi, rc=mode, D=D), (P, M, D, v, pi)
+
+
+def test_dp_recovery_golden():
+    """Hand-derived D=2 recovery (tests/golden/README.md): both planners."""
+    gold = open(os.path.join(ROOT, "tests", "golden", "dp2_p2_m1_v3_pi7_recovery.txt")).read()
+    assert pl.recovery_dump(2, 1, 3, 7, "eflb", D=2) == gold
+    _lib_or_skip()
+    m = dict(n_layer=2, d_model=64, n_head=2, d_ff=256, vocab=128, seq_len=32, causal=1)
+    assert bbl.plan_dump(m, 2, 1, victim=3, at_instr=7, micro_batch=1, pipelines=2) == gold
