@@ -188,6 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nk = (g.K + BK - 1) / BK;
   const int tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM * CG - 1) / (BM * CG);
   const int tiles = tiles_n * tiles_m;
+  // tile -> (row block, column block): N fastest (a wave shares its A rows),
+  // or M fastest for wide-N GEMMs whose B is far larger than A (the LM head:
+  // a wave then shares B tiles, so the weight is read once, not once per row
+  // block). Each tile is still one accumulator over the full K: same bits.
+  auto tile_mb = [&](int t) { return g.m_fast ? t % tiles_m : t / tiles_n; };
+  auto tile_nb = [&](int t) { return g.m_fast ? t / tiles_m : t % tiles_n; };
   // Work unit = (tile, K split). With ksplit > 1 (fp32-accumulating dW only)
   // the splits of a tile add into C in ascending split order, serialised by a
   // per-(tile, CTA) flag (epoch * 16 + split): deterministic; a split waits
@@ -237,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int unit = pid; unit < units; unit += npid) {
         const int tile = unit / ksplit, split = unit % ksplit;
         const int kb0 = split * nk / ksplit, kb1 = (split + 1) * nk / ksplit;
-        const int m0 = (tile / tiles_n) * BM * CG + rank * BM;
-        const int nb0 = (tile % tiles_n) * BN + rank * BNH;
+        const int m0 = tile_mb(tile) * BM * CG + rank * BM;
+        const int nb0 = tile_nb(tile) * BN + rank * BNH;
         // MN-major boxes lying entirely past M (N) are skipped: they only feed
         // output rows (columns) the epilogue masks. Partial boxes are zero-filled.
         // Except: CTA 1 of a pair must load at least one box per K slab. Its
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int j = 0;
     for (int unit = pid; unit < units; unit += npid, ++j) {
       const int tile = unit / ksplit, split = unit % ksplit;
-      const int m0 = (tile / tiles_n) * BM * CG + rank * BM, n0 = (tile % tiles_n) * BN;
+      const int m0 = tile_mb(tile) * BM * CG + rank * BM, n0 = tile_nb(tile) * BN;
       const int fl = tile * CG + rank;
       const int acc = j & 1;
       const int mr = m0 + q * 32;                         // this warp's first row
@@ -535,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int j = 0;
     for (int unit = pid; unit < units; unit += npid, ++j) {
       const int tile = unit / ksplit, split = unit % ksplit;
-      const int m0 = (tile / tiles_n) * BM * CG + rank * BM, n0 = (tile % tiles_n) * BN;
+      const int m0 = tile_mb(tile) * BM * CG + rank * BM, n0 = tile_nb(tile) * BN;
       const int fl = tile * CG + rank;
       const int acc = j & 1;
       mbar_wait(tfull_bar(acc), (j >> 1) & 1);
@@ -692,6 +698,10 @@ unsigned *trace_slot(const Gemm &g, int bn, int cg, int grid, int ksplit) {
 template <int BN, int EPI, int CG, bool TE>
 cudaError_t launch(const Gemm &g_in, cudaStream_t s) {
   Gemm g = g_in;
+  // M-fastest tile order when B (N x K) is several times A and too big to
+  // stay in L2 across row blocks (measured: the C3 LM-head forward read its
+  // 161 MB weight 16 times, 2.9 GB per launch, profiles/r02_gemm_shapes_c3.json)
+  g.m_fast = (long long)g.N >= 4LL * g.M && (long long)g.N * g.K * 2 > (64LL << 20);
   constexpr int BNH = BN / CG;
   using L = Smem<BN, CG, TE>;
   auto kern = gemm_tc_kernel<BN, EPI, CG, TE>;

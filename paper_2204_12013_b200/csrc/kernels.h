@@ -25,6 +25,7 @@ struct Gemm {
   bool tile_grid = false;   // one CTA (pair) per output tile instead of a persistent grid:
                             // a low-priority stream's GEMM then yields SMs tile by tile
   unsigned *trace = nullptr;   // BB_GEMM_TRACE: per-CTA progress words (mapped host memory)
+  bool m_fast = false;         // set by the launcher: tile order walks M fastest (see gemm_tc)
 };
 
 // BB_GEMM_TRACE diagnostics: print the GEMM launches that have not finished.
