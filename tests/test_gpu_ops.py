@@ -68,6 +68,25 @@ def test_gemm_layouts(prec, impl, layout, shape):
     assert np.abs(got - ref).max() <= tol * np.abs(ref).max() * max(1, K / 256)
 
 
+@pytest.mark.parametrize("M", [256, 600])
+def test_gemm_wide_n_m_fastest_order(M):
+    """A wide-N GEMM whose B (N x K bf16 > 64 MB) does not stay in L2 walks
+    its tiles M fastest (Gemm::m_fast, the LM-head forward): same result
+    as the oracle's D = A B^T (fp32 accumulation of exact bf16 products;
+    600 rows leave a ragged row block)."""
+    import paper_2204_12013_b200 as bb
+    N, K = 50304, 768
+    A = rnd(M, K)
+    B = rnd(N, K)
+    ref = om.linear_fwd(A, B)
+    dA, dB = dev(A, "bf16"), dev(B, "bf16")
+    C = torch.zeros((M, N), device="cuda", dtype=torch.float32)
+    bb.op_gemm("bf16", 0, M, N, K, dA.data_ptr(), K, 0, dB.data_ptr(), K, 0, 6, C.data_ptr(), N)
+    torch.cuda.synchronize()
+    got = host(C)
+    assert np.abs(got - ref).max() <= 2e-5 * np.abs(ref).max() * max(1, K / 256)
+
+
 @pytest.mark.parametrize("prec", ["bf16", "fp32"])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4, 6])
 @pytest.mark.parametrize("M,N,K", [(300, 200, 136), (300, 520, 136), (130, 768, 200),
