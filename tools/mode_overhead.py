@@ -36,7 +36,7 @@ def main():
     M, mb = cfg.microbatches, cfg.micro_batch
     flat = make_params(m)
     tok, tgt = make_tokens(cfg, 0)
-    lps = bench.balanced_partition(m, P)
+    lps = bench.device_partition(m, P, -(-P // ws))   # bench.py's default partition
     out = {"config": f"{cfg.name}, {P} stages on {ws} GPU(s), M={M}, mb={mb}", "modes": {}}
     for mode in args.modes:
         sid = bench.bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None

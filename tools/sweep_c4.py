@@ -59,7 +59,7 @@ def main():
     nid = bench.bcast_bytes(bb.session_id() if rank == 0 else None, ws) if ws > 1 else None
     pipe = bb.Pipeline(m, P, M, micro_batch=mb, rc=True, world_rank=rank, world_size=ws,
                        device=local, session_id=nid,
-                       layers_per_stage=bench.balanced_partition(m, P),
+                       layers_per_stage=bench.device_partition(m, P, -(-P // ws)),
                        frc_retain_bytes=bench.AUTO)   # bench.py's partition and FRC budget
     pipe.load_params(flat)
     pipe.stage_inputs(tok, tgt)
