@@ -498,10 +498,7 @@ def run_ours(args, rank, ws, local):
         "warmup": args.warmup, "ms_per_step": round(on["ms"], 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded tokens, random-init weights)",
-        "config": {"workload": f"{cfg.name}: {MODEL_NAMES.get(cfg.name, cfg.name)} {m.n_layer}L "
-                               f"H{m.d_model} S{m.seq_len} {'causal' if m.causal else 'bidirectional'}, "
-                               f"{P} stages, M={M}, mb={mb}, EFLB (eager FRC, lazy BRC)"
-                               + (f", {D} data-parallel pipelines" if D > 1 else ""),
+        "config": {"workload": workload_name(cfg, P, D),
                    "stages": P, "microbatches": M, "micro_batch": mb, "global_batch": samples,
                    "seq_len": m.seq_len,
                    "parallelism": (f"dp{D} x " if D > 1 else "") + f"pp{P} on {ws} GPU(s)",
@@ -585,6 +582,15 @@ def cpu_baseline(cfg, budget_s=20.0):
                       f" + head + FRC forward"}
 
 
+def workload_name(cfg, P, D=1):
+    """config.workload of a bench line (both arms use the same string)."""
+    m = cfg.model
+    return (f"{cfg.name}: {MODEL_NAMES.get(cfg.name, cfg.name)} {m.n_layer}L H{m.d_model} "
+            f"S{m.seq_len} {'causal' if m.causal else 'bidirectional'}, {P} stages, "
+            f"M={cfg.microbatches}, mb={cfg.micro_batch}, EFLB (eager FRC, lazy BRC)"
+            + (f", {D} data-parallel pipelines" if D > 1 else ""))
+
+
 def run_reference(args, rank, ws):
     if rank != 0:
         return
@@ -605,8 +611,13 @@ def run_reference(args, rank, ws):
             "ms_per_step": round(1e3 * wall / args.steps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded tokens, random-init weights)",
-            "config": {"workload": f"{cfg.name} (oracle, CPU)", "stages": cfg.stages,
-                       "microbatches": cfg.microbatches, "micro_batch": cfg.micro_batch},
+            # our arm's workload (the oracle times a bounded sample of it: cpu_baseline)
+            "config": {"workload": workload_name(cfg, max(cfg.stages, ws, args.stages),
+                                                 max(1, args.pipelines)),
+                       "stages": max(cfg.stages, ws, args.stages),
+                       "microbatches": cfg.microbatches, "micro_batch": cfg.micro_batch,
+                       "global_batch": max(1, args.pipelines) * cfg.microbatches * cfg.micro_batch,
+                       "seq_len": cfg.model.seq_len, "implementation": "fp64 oracle on the host"},
             "cpu_baseline": dict(last, value=v),
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
